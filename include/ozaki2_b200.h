@@ -1,0 +1,152 @@
+/* ozaki2_b200.h — C ABI of the B200-native Ozaki scheme II GEMM emulation.
+ *
+ * This is the drop-in boundary for the reference's public C++ entry points
+ * (/root/reference/proj/include/crtgemm). Plain pointers and sizes only: no
+ * torch, no C++ types. The C++ drop-in (include/crtgemm/emulator.hpp,
+ * built into the same library) and the Python host mirror
+ * (paper_2508_03984_b200/) both sit on top of these functions.
+ *
+ * Conventions (reference matrix.hpp:9-32): matrices are column-major; every
+ * GEMM computes C = alpha * (A x B) + beta * C with A m x k, B k x n, C m x n.
+ * The reference has no alpha/beta: alpha = 1, beta = 0
+ * reproduces it bit-for-bit; other values are applied in FP64 after
+ * reconstruction (extension named by BASELINE.json's north star).
+ *
+ * Status codes map the reference exception taxonomy (errors.hpp:8-27):
+ *   OZK_CONFIG_ERROR <- crtgemm::ConfigError, OZK_INPUT_ERROR <- InputError,
+ *   OZK_DOMAIN_ERROR <- std::domain_error (mod_inverse).
+ * A CUDA failure returns OZK_CUDA_ERROR; ozk_last_error() has the message.
+ * There is no CPU fallback: without a B200 every compute entry point fails
+ * with OZK_CUDA_ERROR.
+ */
+#ifndef OZAKI2_B200_H
+#define OZAKI2_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OZK_OK 0
+#define OZK_CONFIG_ERROR 1
+#define OZK_INPUT_ERROR 2
+#define OZK_CUDA_ERROR 3
+#define OZK_DOMAIN_ERROR 4
+#define OZK_INTERNAL_ERROR 5
+
+#define OZK_MAX_MODULI 20
+#define OZK_ENGINE_MAX_K (1 << 17) /* int8_engine.hpp:12 kEngineMaxK */
+
+/* Precision (crt_tables.hpp:11) and ScaleMode (scaling.hpp:12) */
+#define OZK_FP64 0
+#define OZK_FP32 1
+#define OZK_FAST 0
+#define OZK_ACCURATE 1
+
+/* storage types of A/B/C buffers */
+#define OZK_R64F 0
+#define OZK_R32F 1
+
+/* Stage-2 output kinds for ozk_stage_products (debug/parity export) */
+#define OZK_PRODUCTS_I32 0 /* raw wrapping int32 C'_i (int8_engine.hpp:19-24) */
+#define OZK_PRODUCTS_U8 1  /* U_i = mod(C'_i, p_i)      (reconstruct.hpp:28-37) */
+
+/* The constant table of crt_tables.hpp:40-61 (CrtConstants) in plain C. The
+ * arbitrary-precision P is exported as 6 little-endian 32-bit limbs. */
+typedef struct {
+    int32_t n_moduli;
+    int32_t precision;
+    int32_t moduli[OZK_MAX_MODULI];
+    int64_t q[OZK_MAX_MODULI];
+    int32_t beta[OZK_MAX_MODULI];
+    double P1, P2, P_inv;
+    float pp_fast, pp_accu;
+    double s1[OZK_MAX_MODULI], s2[OZK_MAX_MODULI];
+    double pinv64[OZK_MAX_MODULI];
+    float pinv32[OZK_MAX_MODULI];
+    int32_t pinv_mulhi[OZK_MAX_MODULI];
+    int32_t P_bits;
+    uint32_t P_limbs[6];
+} ozk_constants;
+
+/* EmuConfig (emulator.hpp:12-18) plus the buffer types of this call.
+ * constants == NULL means build_constants(n_moduli, precision)
+ * (emulator.cpp:102-108); a non-NULL table is used as given (the explicit-
+ * constants overloads emulator.hpp:28-32, e.g. for fault injection).
+ * With precision OZK_FP32 and R64F inputs, A and B are first rounded to FP32
+ * (emulator.cpp:84-91). */
+typedef struct {
+    int32_t n_moduli;
+    int32_t mode;      /* OZK_FAST | OZK_ACCURATE */
+    int32_t precision; /* OZK_FP64 | OZK_FP32 */
+    int32_t a_type;    /* OZK_R64F | OZK_R32F (also B's type) */
+    int32_t c_type;    /* OZK_R64F | OZK_R32F */
+    int32_t reserved;
+    int64_t block_k; /* validated in [1, 2^17] like the reference; results do not depend on it */
+    const ozk_constants* constants;
+} ozk_config;
+
+typedef struct ozk_context* ozk_handle;
+
+/* ---- lifetime ----------------------------------------------------------- */
+int ozk_create(ozk_handle* handle, int device);
+int ozk_destroy(ozk_handle handle);
+/* cudaStream_t as void*; NULL = legacy default stream */
+int ozk_set_stream(ozk_handle handle, void* stream);
+const char* ozk_last_error(void);
+int ozk_version(void);
+/* default config for (n_moduli, mode, precision): R64F buffers, block_k 2^17 */
+ozk_config ozk_default_config(int n_moduli, int mode, int precision);
+
+/* ---- constants (crt_tables.hpp:63-79) ---------------------------------- */
+int ozk_select_moduli(int n_moduli, int32_t* moduli_out);      /* select_moduli      crt_tables.cpp:15 */
+int64_t ozk_mod_inverse(int64_t a, int64_t m, int* status);    /* mod_inverse        crt_tables.cpp:32 */
+int ozk_build_constants(int n_moduli, int precision, ozk_constants* out); /* build_constants crt_tables.cpp:186 */
+int ozk_dump_tables_csv(const ozk_constants* c, char* buf, int64_t buflen); /* dump_tables_csv crt_tables.cpp:199 */
+
+/* ---- the GEMM (gemm_emulated, emulator.hpp:20-32) ---------------------- */
+/* Device pointers; runs on the handle's stream (asynchronous). */
+int ozk_gemm(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, double alpha, const void* A,
+             int64_t lda, const void* B, int64_t ldb, double beta, void* C, int64_t ldc);
+/* Host pointers (pageable or pinned): H2D, ozk_gemm, D2H, synchronous. This
+ * is the reference-facing call (Matrix<T> buffers live in host memory). */
+int ozk_gemm_host(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, double alpha,
+                  const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C, int64_t ldc);
+/* BLAS-style conveniences over ozk_gemm (device pointers) */
+int ozk_dgemm(ozk_handle h, int n_moduli, int mode, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+              int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
+int ozk_sgemm(ozk_handle h, int n_moduli, int mode, int64_t m, int64_t n, int64_t k, float alpha, const float* A,
+              int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc);
+
+/* ---- stage-level exports (device pointers; parity / debug) -------------- */
+/* K1a: scale exponents mu_i = 2^mu_exp[i], nu_j = 2^nu_exp[j]
+ *      (scale_fast / scale_accurate, scaling.hpp:28-36). */
+int ozk_stage_scale(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+                    const void* B, int64_t ldb, int32_t* mu_exp, int32_t* nu_exp);
+/* leading dimension (bytes) of one residue-plane row for inner size k */
+int64_t ozk_plane_ld(int64_t k);
+/* K1b: truncate_scale + to_residue_slices (residue.hpp:31-62). Planes are
+ * K-major for the tensor cores: a_planes[N][m][ld], b_planes[N][n][ld] with
+ * ld = ozk_plane_ld(k); plane i holds rmod(trunc(scaled x), p_i). */
+int ozk_stage_residues(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, const void* A,
+                       int64_t lda, const void* B, int64_t ldb, const int32_t* mu_exp, const int32_t* nu_exp,
+                       int8_t* a_planes, int8_t* b_planes);
+/* K2: the N residue GEMMs. out[N][n][ldo] column-major, ldo >= m:
+ * OZK_PRODUCTS_I32 -> int32 C'_i, OZK_PRODUCTS_U8 -> uint8 U_i. */
+int ozk_stage_products(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, const int8_t* a_planes,
+                       const int8_t* b_planes, int kind, void* out, int64_t ldo);
+/* K3: accumulate + crt_reduce + unscale (+ alpha/beta), reconstruct.hpp:46-59.
+ * U[N][n][ldu] uint8 as written by ozk_stage_products(OZK_PRODUCTS_U8). */
+int ozk_stage_reconstruct(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, const uint8_t* U, int64_t ldu,
+                          const int32_t* mu_exp, const int32_t* nu_exp, double alpha, double beta, void* C,
+                          int64_t ldc);
+
+/* number of this library's kernels launched on the handle since creation */
+int64_t ozk_kernel_launches(ozk_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,521 @@
+// K2 — the N residue GEMMs on the 5th-generation tensor cores
+// (reference: int8_engine.cpp:15-64 + the fused mod of emulator.cpp:45-53 /
+// reconstruct.hpp:31-37; accurate-mode bound product scaling.cpp:135-149).
+//
+// One persistent, warp-specialised kernel runs every (modulus, tile) work item:
+//   warp 0      TMA producer: A/B K-major int8 tiles (128 B rows, 128B swizzle)
+//               into a kStages-deep shared-memory ring (mbarrier full/empty);
+//   warp 1      MMA issuer (one elected lane of the leader CTA):
+//               tcgen05.mma.kind::i8, s32 accumulate in TMEM, no saturation,
+//               so the single k = 2^17 overflow wraps exactly like the
+//               reference's uint32 accumulator (int8_engine.cpp:12-38);
+//   warp 2      TMEM allocator (two 256-column accumulators: the epilogue of
+//               tile t overlaps the MMAs of tile t+1);
+//   warps 4-7   epilogue: tcgen05.ld 32 columns at a time, then
+//               U8  : U_i = mod_u8(C'_i)  -> 1 byte per element to HBM,
+//               I32 : raw C'_i (debug / parity export),
+//               MAX : row/column maxima of Cbar via atomics (the reference
+//                     materialises an m x n int64 Cbar; we never do).
+// CG = 2 pairs the two SMs of a TPC (cta_group::2, UMMA 256 x 256 x 32): each
+// CTA stages half of A's 256 rows and half of B's 256 columns, the leader
+// issues, and both CTAs drain their 128 TMEM lanes. CG = 1 is the single-SM
+// 128 x 256 variant (kept for small problems and as a bring-up fallback).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "ozk_device.cuh"
+
+namespace ozk {
+namespace {
+
+constexpr int kBK = 128;  // bytes (= int8 elements) of K per stage: one 128B swizzle atom
+constexpr int kAccCols = 256;
+constexpr int kThreads = 256;
+constexpr int kEpiWarp0 = 4;
+
+template <int CG>
+struct Cfg {
+    static constexpr int kBM = 128;                 // A rows per CTA
+    static constexpr int kTileM = 128 * CG;         // rows per work tile
+    static constexpr int kTileN = 256;              // columns per work tile (UMMA N)
+    static constexpr int kBRows = kTileN / CG;      // B rows staged per CTA
+    static constexpr int kStageA = kBM * kBK;       // 16 KB
+    static constexpr int kStageB = kBRows * kBK;    // 16 KB (CG 2) / 32 KB (CG 1)
+    static constexpr int kStages = CG == 2 ? 6 : 4;
+    static constexpr int kSmem = kStages * (kStageA + kStageB) + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr uint32_t kTxBytes = static_cast<uint32_t>(CG * (kStageA + kStageB));
+};
+
+struct K2Params {
+    int m, n, k;
+    int n_mod;
+    int tiles_m, tiles_n, num_kb;
+    void* out;
+    long long ldo;
+    long long plane_out;
+    int* rowmax;
+    int* colmax;
+    int p[OZK_MAX_MODULI];
+    int pinv[OZK_MAX_MODULI];
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+        "[%2];" ::"r"(dst),
+        "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+// 2-SM variant: the completion bytes land on the leader CTA's barrier.
+__device__ __forceinline__ void tma_load_3d_2sm(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4, %5}], [%2];" ::"r"(dst),
+        "l"(map), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+template <int CG>
+__device__ __forceinline__ void tmem_alloc(uint32_t slot_addr, uint32_t cols) {
+    if constexpr (CG == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot_addr), "r"(cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot_addr), "r"(cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+}
+template <int CG>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
+    if constexpr (CG == 2)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
+    else
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
+}
+template <int CG>
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    if constexpr (CG == 2)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// tcgen05.commit: the barrier fires once all previously issued MMAs finish.
+template <int CG>
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    if constexpr (CG == 2)
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                bar),
+            "h"(static_cast<uint16_t>(3))
+            : "memory");
+    else
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                     : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+          "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor: K-major, 128B swizzle, 8-row core groups
+// 1024 B apart (SBO), Blackwell descriptor version 1.
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(1) << 16) |
+           (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+           (static_cast<uint64_t>(2) << 61);
+}
+// Instruction descriptor: s8 x s8 -> s32, K-major A and B, no saturate.
+template <int CG>
+__host__ __device__ constexpr uint32_t idesc_i8() {
+    return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(Cfg<CG>::kTileN >> 3) << 17) |
+           (static_cast<uint32_t>(Cfg<CG>::kTileM >> 4) << 24);
+}
+
+// work item t -> (modulus, tile row, tile column), grouped raster of 8 tile
+// rows per modulus so the co-resident tiles share A/B panels in L2
+__device__ __forceinline__ void decode_tile(int t, int tiles_m, int tiles_n, int& mod, int& tm, int& tn) {
+    const int per_mod = tiles_m * tiles_n;
+    mod = t / per_mod;
+    const int r = t - mod * per_mod;
+    constexpr int G = 8;
+    const int group = r / (G * tiles_n);
+    const int first = group * G;
+    const int gsize = tiles_m - first < G ? tiles_m - first : G;
+    const int w = r - group * G * tiles_n;
+    tm = first + w % gsize;
+    tn = w / gsize;
+}
+
+// max over the 32 lanes of column `lane` of a 32 x 32 register tile
+// (reduce-scatter butterfly: 31 shuffles instead of 32 x 5)
+__device__ __forceinline__ int32_t column_max_scatter(uint32_t (&v)[32], int lane) {
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const bool upper = (lane & s) != 0;
+#pragma unroll
+        for (int j = 0; j < s; ++j) {
+            const int32_t keep = static_cast<int32_t>(upper ? v[j + s] : v[j]);
+            const int32_t send = static_cast<int32_t>(upper ? v[j] : v[j + s]);
+            const int32_t recv = __shfl_xor_sync(0xffffffffu, send, s);
+            v[j] = static_cast<uint32_t>(keep > recv ? keep : recv);
+        }
+    }
+    return static_cast<int32_t>(v[0]);
+}
+
+template <int CG, int KIND>
+__global__ void __launch_bounds__(kThreads, 1)
+    residue_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const K2Params P) {
+    using C = Cfg<CG>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + C::kStages * C::kStageA;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::kStages * C::kStageB);
+    uint64_t* empty = full + C::kStages;
+    uint64_t* tfull = empty + C::kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+    const bool leader = rank == 0;
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmA);
+        prefetch_tmap(&tmB);
+    }
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull + a, 1);
+            mbar_init(tempty + a, 4 * CG);  // one arrival per epilogue warp of every CTA
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<CG>(smem_u32(tmem_slot), 2 * kAccCols);
+    tc_fence_before();
+    if constexpr (CG == 2)
+        cluster_sync();
+    else
+        __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int total = P.n_mod * P.tiles_m * P.tiles_n;
+    const int cluster_id = blockIdx.x / CG, nclusters = gridDim.x / CG;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer ----------------
+            int stage = 0;
+            uint32_t phase = 0;
+            const uint32_t full0_leader = CG == 2 ? mapa(smem_u32(full), 0) : smem_u32(full);
+            for (int t = cluster_id; t < total; t += nclusters) {
+                int mod, tm, tn;
+                decode_tile(t, P.tiles_m, P.tiles_n, mod, tm, tn);
+                const int m0 = tm * C::kTileM + static_cast<int>(rank) * C::kBM;
+                const int n0 = tn * C::kTileN + static_cast<int>(rank) * C::kBRows;
+                for (int kb = 0; kb < P.num_kb; ++kb) {
+                    mbar_wait(smem_u32(empty + stage), phase ^ 1);
+                    const uint32_t fb = smem_u32(full + stage);
+                    if (leader) mbar_arrive_expect_tx(fb, C::kTxBytes);
+                    const uint32_t dA = smem_u32(sA + stage * C::kStageA);
+                    const uint32_t dB = smem_u32(sB + stage * C::kStageB);
+                    if constexpr (CG == 2) {
+                        const uint32_t lb = full0_leader + 8u * stage;
+                        tma_load_3d_2sm(dA, &tmA, lb, kb * kBK, m0, mod);
+                        tma_load_3d_2sm(dB, &tmB, lb, kb * kBK, n0, mod);
+                    } else {
+                        tma_load_3d(dA, &tmA, fb, kb * kBK, m0, mod);
+                        tma_load_3d(dB, &tmB, fb, kb * kBK, n0, mod);
+                    }
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader) {
+            // ---------------- MMA issuer ----------------
+            constexpr uint32_t idesc = idesc_i8<CG>();
+            int stage = 0;
+            uint32_t phase = 0;
+            int lt = 0;
+            for (int t = cluster_id; t < total; t += nclusters, ++lt) {
+                const int acc = lt & 1;
+                const uint32_t acc_phase = (lt >> 1) & 1;
+                mbar_wait(smem_u32(tempty + acc), acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * kAccCols;
+                for (int kb = 0; kb < P.num_kb; ++kb) {
+                    mbar_wait(smem_u32(full + stage), phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t a0 = smem_u32(sA + stage * C::kStageA);
+                        const uint32_t b0 = smem_u32(sB + stage * C::kStageB);
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 32; ++kk)
+                            mma_i8<CG>(d_tmem, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idesc,
+                                       (kb | kk) != 0);
+                        mma_commit<CG>(smem_u32(empty + stage));
+                    }
+                    __syncwarp();
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                if (lane == 0) mma_commit<CG>(smem_u32(tfull + acc));
+                __syncwarp();
+            }
+        }
+    } else if (warp >= kEpiWarp0) {
+        // ---------------- epilogue ----------------
+        const int q = warp - kEpiWarp0;  // TMEM lane quarter
+        const uint32_t tempty0_leader = CG == 2 ? mapa(smem_u32(tempty), 0) : smem_u32(tempty);
+        int lt = 0;
+        for (int t = cluster_id; t < total; t += nclusters, ++lt) {
+            const int acc = lt & 1;
+            const uint32_t acc_phase = (lt >> 1) & 1;
+            int mod, tm, tn;
+            decode_tile(t, P.tiles_m, P.tiles_n, mod, tm, tn);
+            mbar_wait(smem_u32(tfull + acc), acc_phase);
+            tc_fence_after();
+            const int row = tm * C::kTileM + static_cast<int>(rank) * C::kBM + q * 32 + lane;
+            const bool row_ok = row < P.m;
+            int32_t rmax = 0;
+            for (int cb = 0; cb < C::kTileN / 32; ++cb) {
+                uint32_t v[32];
+                tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kAccCols + cb * 32, v);
+                const int col0 = tn * C::kTileN + cb * 32;
+                if constexpr (KIND == K2_U8) {
+                    uint8_t* dst = static_cast<uint8_t*>(P.out) + static_cast<long long>(mod) * P.plane_out + row;
+                    const int pm = P.p[mod], pinv = P.pinv[mod];
+                    if (row_ok) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col0 + j < P.n)
+                                dst[static_cast<long long>(col0 + j) * P.ldo] =
+                                    static_cast<uint8_t>(mod_u8(static_cast<int32_t>(v[j]), pm, pinv));
+                    }
+                } else if constexpr (KIND == K2_I32) {
+                    int32_t* dst = static_cast<int32_t*>(P.out) + static_cast<long long>(mod) * P.plane_out + row;
+                    if (row_ok) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col0 + j < P.n) dst[static_cast<long long>(col0 + j) * P.ldo] = static_cast<int32_t>(v[j]);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) rmax = max(rmax, static_cast<int32_t>(v[j]));
+                    const int32_t cmax = column_max_scatter(v, lane);
+                    if (col0 + lane < P.n) atomicMax(P.colmax + col0 + lane, cmax);
+                }
+            }
+            if constexpr (KIND == K2_MAX) {
+                if (row_ok) atomicMax(P.rowmax + row, rmax);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty0_leader + 8u * acc);
+        }
+    }
+
+    // ---------------- teardown ----------------
+    __syncwarp();
+    tc_fence_before();
+    if constexpr (CG == 2)
+        cluster_sync();
+    else
+        __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<CG>(tmem_base, 2 * kAccCols);
+    }
+}
+
+// ------------------------------------------------------------- host helpers
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 3-D map over planes[n_mod][rows][ld] bytes, box {128 B of K, box_rows, 1}
+bool make_plane_map(CUtensorMap* map, const int8_t* base, int64_t k, int64_t rows, int64_t ld, int n_mod,
+                    int box_rows) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(n_mod)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(ld * rows)};
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int CG, int KIND>
+int launch_impl(const K2Launch& L, cudaStream_t s) {
+    using C = Cfg<CG>;
+    CUtensorMap ma, mb;
+    if (!make_plane_map(&ma, L.a_planes, L.k, L.m, L.ld, L.n_mod, C::kBM) ||
+        !make_plane_map(&mb, L.b_planes, L.k, L.n, L.ld, L.n_mod, C::kBRows)) {
+        set_error("cuTensorMapEncodeTiled failed");
+        return OZK_CUDA_ERROR;
+    }
+    K2Params P{};
+    P.m = static_cast<int>(L.m);
+    P.n = static_cast<int>(L.n);
+    P.k = static_cast<int>(L.k);
+    P.n_mod = L.n_mod;
+    P.tiles_m = static_cast<int>((L.m + C::kTileM - 1) / C::kTileM);
+    P.tiles_n = static_cast<int>((L.n + C::kTileN - 1) / C::kTileN);
+    P.num_kb = static_cast<int>((L.k + kBK - 1) / kBK);
+    P.out = L.out;
+    P.ldo = L.ldo;
+    P.plane_out = L.ldo * L.n;
+    P.rowmax = L.rowmax;
+    P.colmax = L.colmax;
+    for (int i = 0; i < L.n_mod && L.c; ++i) {
+        P.p[i] = L.c->p[i];
+        P.pinv[i] = L.c->pinv_mulhi[i];
+    }
+    const long long total = static_cast<long long>(L.n_mod) * P.tiles_m * P.tiles_n;
+    long long clusters = L.num_sms / CG;
+    if (clusters > total) clusters = total;
+    if (clusters < 1) clusters = 1;
+
+    auto kern = residue_gemm_kernel<CG, KIND>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, P);
+    if (e != cudaSuccess) {
+        set_error(std::string("residue_gemm launch: ") + cudaGetErrorString(e));
+        return OZK_CUDA_ERROR;
+    }
+    return OZK_OK;
+}
+
+template <int CG>
+int launch_kind(const K2Launch& L, cudaStream_t s) {
+    switch (L.kind) {
+        case K2_I32:
+            return launch_impl<CG, K2_I32>(L, s);
+        case K2_U8:
+            return launch_impl<CG, K2_U8>(L, s);
+        default:
+            return launch_impl<CG, K2_MAX>(L, s);
+    }
+}
+
+}  // namespace
+
+int k2_cta_group() {
+    static int cg = 0;
+    if (!cg) {
+        const char* env = std::getenv("OZK_CTA_GROUP");
+        cg = (env && env[0] == '1') ? 1 : 2;
+    }
+    return cg;
+}
+
+int launch_k2(const K2Launch& L, cudaStream_t s) {
+    if (L.m > (1LL << 31) - 1 || L.n > (1LL << 31) - 1 || L.k > (1LL << 31) - 1) {
+        set_error("residue_gemm: dimension exceeds 2^31");
+        return OZK_INPUT_ERROR;
+    }
+    return k2_cta_group() == 1 ? launch_kind<1>(L, s) : launch_kind<2>(L, s);
+}
+
+}  // namespace ozk

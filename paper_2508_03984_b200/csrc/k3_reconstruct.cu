@@ -1,0 +1,85 @@
+// K3 — CRT reconstruction (reference: emulator.cpp:49-53 weighted sum,
+// reconstruct.hpp:51-54 crt_reduce_element, reconstruct.cpp:49-69 unscale).
+//
+// One pass over the N uint8 residue planes U_i (column-major, ld = ldu) per
+// output element, in the reference's per-element order:
+//   c1 += s1_i * u  (exact by the beta_i construction, crt_tables.cpp:165-169)
+//   c2 += s2_i * u  (mul then add: two roundings, as in emulator.cpp:53)
+//   Q  = rint(P_inv * c1);  C'' = fma(-P2, Q, fma(-P1, Q, c1) + c2)
+//   C  = ldexp(C'', -(e_mu_i + e_nu_j))
+// then the optional alpha/beta extension in FP64 and the FP32 down-cast of
+// to_fp32 (emulator.cpp:110-115) when C is single precision. Each thread owns
+// four consecutive rows: one 32-bit load per plane, 32 B of C out, so a warp
+// moves 128 B per plane and 1 KB of C — HBM-bound at N + 8 bytes per element.
+#include "ozk_device.cuh"
+
+namespace ozk {
+namespace {
+
+template <bool kF32Out, bool kPlain>
+__global__ void __launch_bounds__(128)
+    reconstruct_kernel(const uint8_t* __restrict__ u, int64_t ldu, int64_t plane_stride, int64_t m, int64_t n,
+                       const int32_t* __restrict__ mu_exp, const int32_t* __restrict__ nu_exp, const DevConsts c,
+                       double alpha, double beta, void* __restrict__ C, int64_t ldc) {
+    const int64_t j = blockIdx.x;
+    const int64_t i0 = (static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x) * 4;
+    if (i0 >= m) return;
+    double c1[4] = {0.0, 0.0, 0.0, 0.0}, c2[4] = {0.0, 0.0, 0.0, 0.0};
+    const uint8_t* src = u + j * ldu + i0;
+    for (int t = 0; t < c.n; ++t) {
+        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(src + t * plane_stride));
+        const double s1 = c.s1[t], s2 = c.s2[t];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double v = static_cast<double>((w >> (8 * q)) & 0xffu);
+            c1[q] = __dadd_rn(c1[q], __dmul_rn(s1, v));
+            c2[q] = __dadd_rn(c2[q], __dmul_rn(s2, v));
+        }
+    }
+    const int ne = nu_exp[j];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int64_t i = i0 + q;
+        if (i >= m) break;
+        const double qv = rint(__dmul_rn(c.P_inv, c1[q]));
+        const double cpp = __fma_rn(-c.P2, qv, __dadd_rn(__fma_rn(-c.P1, qv, c1[q]), c2[q]));
+        double r = ldexp(cpp, -(mu_exp[i] + ne));
+        if (!kPlain) {
+            const double old = beta != 0.0 ? (kF32Out ? static_cast<double>(static_cast<float*>(C)[i + j * ldc])
+                                                      : static_cast<double*>(C)[i + j * ldc])
+                                           : 0.0;
+            r = __dadd_rn(__dmul_rn(alpha, r), __dmul_rn(beta, old));
+        }
+        if (kF32Out)
+            static_cast<float*>(C)[i + j * ldc] = __double2float_rn(r);
+        else
+            static_cast<double*>(C)[i + j * ldc] = r;
+    }
+}
+
+}  // namespace
+
+void launch_reconstruct(const uint8_t* u, int64_t ldu, int64_t m, int64_t n, const int32_t* mu_exp,
+                        const int32_t* nu_exp, const DevConsts& c, double alpha, double beta, void* C, int64_t ldc,
+                        int c_is_f32, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>(n), static_cast<unsigned>((m + 511) / 512));
+    const int64_t stride = ldu * n;
+    const bool plain = alpha == 1.0 && beta == 0.0;
+    if (c_is_f32) {
+        if (plain)
+            reconstruct_kernel<true, true><<<grid, 128, 0, s>>>(u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta,
+                                                                C, ldc);
+        else
+            reconstruct_kernel<true, false><<<grid, 128, 0, s>>>(u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha,
+                                                                 beta, C, ldc);
+    } else {
+        if (plain)
+            reconstruct_kernel<false, true><<<grid, 128, 0, s>>>(u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha,
+                                                                 beta, C, ldc);
+        else
+            reconstruct_kernel<false, false><<<grid, 128, 0, s>>>(u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha,
+                                                                  beta, C, ldc);
+    }
+}
+
+}  // namespace ozk

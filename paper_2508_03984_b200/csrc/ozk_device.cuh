@@ -1,0 +1,80 @@
+// Device-side arithmetic shared by the kernels. Every FP operation that the
+// reference performs as separately rounded ops is spelled with the explicit
+// _rn intrinsics (the library is also compiled with --fmad=false), so no
+// multiply-add pair is contracted behind our back (SURVEY §7 "hard parts").
+#pragma once
+
+#include <cstdint>
+
+#include "ozk_internal.h"
+
+namespace ozk {
+
+// 2^e as a double for e in [-1022, 1023] (exact).
+__device__ __forceinline__ double pow2d(int e) {
+    return __longlong_as_double(static_cast<long long>(e + 1023) << 52);
+}
+// 2^e as a float for e in [-126, 127] (exact).
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((e + 127) << 23); }
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// truncate_scale element (residue.cpp:15,18): trunc(x * (T)scale), scale = 2^e.
+__device__ __forceinline__ double trunc_scaled(double x, int e) { return trunc(__dmul_rn(x, pow2d(e))); }
+__device__ __forceinline__ float trunc_scaled(float x, int e) { return truncf(__fmul_rn(x, pow2f(e))); }
+
+// rmod_fast (residue.hpp:39-53) with the refinement thresholds of :17-20.
+__device__ __forceinline__ int8_t rmod_fast(double x, int p, double pinv64, float pinv32, int n) {
+    float y = __double2float_rn(__fma_rn(rint(__dmul_rn(x, pinv64)), -static_cast<double>(p), x));
+    const float pf = static_cast<float>(p);
+    if (n >= 13) y = __fmaf_rn(rintf(__fmul_rn(y, pinv32)), -pf, y);
+    if (n >= 19) y = __fmaf_rn(rintf(__fmul_rn(y, pinv32)), -pf, y);
+    return static_cast<int8_t>(__float2int_rz(y));
+}
+__device__ __forceinline__ int8_t rmod_fast(float x, int p, double /*pinv64*/, float pinv32, int n) {
+    const float pf = static_cast<float>(p);
+    float y = __fmaf_rn(rintf(__fmul_rn(x, pinv32)), -pf, x);
+    if (n >= 5) y = __fmaf_rn(rintf(__fmul_rn(y, pinv32)), -pf, y);
+    if (n >= 11) y = __fmaf_rn(rintf(__fmul_rn(y, pinv32)), -pf, y);
+    return static_cast<int8_t>(__float2int_rz(y));
+}
+
+// mod_u8 (reconstruct.hpp:31-37): high-half multiply by floor(2^32/p - 1)
+// then two one-sided corrections. The true y lies in (-p, 2p), so the 32-bit
+// wrapping difference is exact.
+__device__ __forceinline__ uint32_t mod_u8(int32_t x, int32_t p, int32_t pinv) {
+    const int32_t hi = __mulhi(x, pinv);
+    int32_t y = static_cast<int32_t>(static_cast<uint32_t>(x) - static_cast<uint32_t>(hi) * static_cast<uint32_t>(p));
+    y = y >= p ? y - p : y;
+    y = y < 0 ? y + p : y;
+    return static_cast<uint32_t>(y);
+}
+
+// scaling.cpp:15,18
+__device__ __forceinline__ int magnitude_cap(int prec) { return prec == OZK_FP64 ? 72 : 44; }
+__device__ __forceinline__ int exponent_clamp(int prec) { return prec == OZK_FP64 ? 1021 : 125; }
+
+// The fast-mode budget y = pp_fast - max(1, 0.51 log2 ub) of fast_exponent
+// (scaling.cpp:50-52), ub = sum_upper_bound(s, k) (scaling.cpp:45-47).
+__device__ __forceinline__ double fast_budget(double s, int64_t k, float pp_fast) {
+    const double factor = __dadd_rn(1.0, __dmul_rn(__dmul_rn(2.0, static_cast<double>(k + 2)), 0x1.0p-53));
+    const double ub = __dmul_rn(s, factor);
+    const double l = __dmul_rn(0.51, log2(ub));
+    const double t = l > 1.0 ? l : 1.0;
+    return __dsub_rn(static_cast<double>(pp_fast), t);
+}
+// fast_exponent tail (scaling.cpp:52-55); the reference omits the "- g" term
+// and so do we.
+__device__ __forceinline__ int fast_exponent_from_budget(double y, int g, int prec) {
+    int e = static_cast<int>(floor(y));
+    const int cap = magnitude_cap(prec) - 1 - g;
+    e = e < cap ? e : cap;
+    const int cl = exponent_clamp(prec);
+    return clampi(e, -cl, cl);
+}
+
+__device__ __forceinline__ double load_as_double(const void* p, int64_t idx, int is_f32) {
+    return is_f32 ? static_cast<double>(static_cast<const float*>(p)[idx]) : static_cast<const double*>(p)[idx];
+}
+
+}  // namespace ozk

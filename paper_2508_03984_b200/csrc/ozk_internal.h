@@ -1,0 +1,98 @@
+// Internal declarations shared by the host orchestration (api.cu), the
+// constant tables (constants.cpp) and the kernels (k1_*.cu, k2_gemm.cu,
+// k3_reconstruct.cu). Not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "ozaki2_b200.h"
+
+namespace ozk {
+
+void set_error(const std::string& msg);
+const ozk_constants* cached_constants(int n, int precision);
+
+// Per-call constants as a by-value kernel parameter (about 1 KB).
+struct DevConsts {
+    int n;
+    int precision;
+    int p[OZK_MAX_MODULI];
+    int pinv_mulhi[OZK_MAX_MODULI];
+    double pinv64[OZK_MAX_MODULI];
+    float pinv32[OZK_MAX_MODULI];
+    double s1[OZK_MAX_MODULI];
+    double s2[OZK_MAX_MODULI];
+    double P1, P2, P_inv;
+    float pp_fast, pp_accu;
+};
+
+DevConsts to_dev(const ozk_constants& c);
+
+// Inner-dimension row pitch of the K-major int8 planes: a multiple of 16 bytes
+// (TMA global strides must be 16-byte multiples).
+inline int64_t plane_ld(int64_t k) { return (k + 15) / 16 * 16; }
+// Leading dimension of the uint8 U planes (16-byte aligned columns).
+inline int64_t u_ld(int64_t m) { return (m + 15) / 16 * 16; }
+
+// ---- K1 launchers (k1_scale.cu / k1_residue.cu) ----------------------------
+// Partial reductions per line (row of A / column of B): max |x| and sum x^2.
+struct LineStats {
+    double* amax;  // [splits][m]
+    double* asum;  // [splits][m]
+    double* bmax;  // [n]
+    double* bsum;  // [n]
+    int splits;
+};
+int row_stats_splits(int64_t m, int64_t k);
+void launch_row_stats(const void* a, int a_is_f32, int64_t m, int64_t k, int64_t lda, const LineStats& st,
+                      cudaStream_t s);
+void launch_col_stats(const void* b, int b_is_f32, int64_t k, int64_t n, int64_t ldb, const LineStats& st,
+                      cudaStream_t s);
+// fast mode: exponents + near-boundary flags -> exact sequential recompute
+void launch_fast_finalize(const LineStats& st, int64_t m, int64_t n, int64_t k, const DevConsts& c, int32_t* mu_exp,
+                          int32_t* nu_exp, int32_t* flag_count, int32_t* flag_rows, int32_t* flag_cols,
+                          cudaStream_t s);
+void launch_fast_exact(const void* a, const void* b, int is_f32, int64_t m, int64_t n, int64_t k, int64_t lda,
+                       int64_t ldb, const DevConsts& c, const int32_t* flag_count, const int32_t* flag_rows,
+                       const int32_t* flag_cols, int32_t* mu_exp, int32_t* nu_exp, cudaStream_t s);
+// accurate mode: mu' / nu' exponents (5 - ilogb max), zero lines marked with INT32_MIN
+void launch_accurate_base(const LineStats& st, int64_t m, int64_t n, int32_t* ma, int32_t* nb, cudaStream_t s);
+void launch_accurate_budget(const int32_t* ma, const int32_t* nb, const int32_t* rowmax, const int32_t* colmax,
+                            int64_t m, int64_t n, const DevConsts& c, int32_t* mu_exp, int32_t* nu_exp,
+                            cudaStream_t s);
+
+// Plane writers. kind 0: residues of trunc(x * 2^exp) (N planes);
+// kind 1: Abar/Bbar = ceil(|x| * 2^exp) (1 plane; exp INT32_MIN = zero line).
+void launch_a_planes(const void* a, int is_f32, int64_t m, int64_t k, int64_t lda, const int32_t* row_exp,
+                     const DevConsts& c, int kind, int8_t* planes, int64_t ld, cudaStream_t s);
+void launch_b_planes(const void* b, int is_f32, int64_t k, int64_t n, int64_t ldb, const int32_t* col_exp,
+                     const DevConsts& c, int kind, int8_t* planes, int64_t ld, cudaStream_t s);
+// FP64 -> FP32 rounding of an input (emulator.cpp:84-91), column-major with ld
+void launch_round_to_f32(const double* x, int64_t rows, int64_t cols, int64_t ld, float* out, cudaStream_t s);
+
+// ---- K2 (k2_gemm.cu) -------------------------------------------------------
+enum K2Kind { K2_I32 = 0, K2_U8 = 1, K2_MAX = 2 };
+struct K2Launch {
+    const int8_t* a_planes;  // [n_mod][m][ld]
+    const int8_t* b_planes;  // [n_mod][n][ld]
+    int64_t m, n, k, ld;
+    int n_mod;
+    int kind;
+    void* out;  // I32 / U8: [n_mod][n][ldo]
+    int64_t ldo;
+    int32_t* rowmax;  // MAX
+    int32_t* colmax;
+    const DevConsts* c;
+    int num_sms;
+};
+int launch_k2(const K2Launch& L, cudaStream_t s);
+
+// ---- K3 (k3_reconstruct.cu) -----------------------------------------------
+void launch_reconstruct(const uint8_t* u, int64_t ldu, int64_t m, int64_t n, const int32_t* mu_exp,
+                        const int32_t* nu_exp, const DevConsts& c, double alpha, double beta, void* C, int64_t ldc,
+                        int c_is_f32, cudaStream_t s);
+
+}  // namespace ozk

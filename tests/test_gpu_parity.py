@@ -1,0 +1,200 @@
+"""GPU parity: every stage of the CUDA path against the CPU oracle, bit-exact.
+
+Each test calls through the C ABI (paper_2508_03984_b200.Context -> ozk_*),
+on cuda:0, and compares with oracle/ozk_oracle.c (the restatement pinned to
+the reference in tests/test_oracle.py), or directly with the compiled
+reference (oracle/_ref) where noted.
+"""
+import numpy as np
+import pytest
+
+from paper_2508_03984_b200 import EmuConfig, Precision, ScaleMode, gemm_emulated, gen_int_matrix, gen_matrix
+from paper_2508_03984_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _dev_colmajor(x: np.ndarray):
+    """host Fortran array -> CUDA tensor (rows, cols) with stride (1, rows)"""
+    t = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+    return t.t()
+
+
+def _bits(x):
+    return np.ascontiguousarray(x).view(np.int64 if x.dtype == np.float64 else np.int32)
+
+
+def _planes_kmajor(mats, ld):
+    """list of (rows x k) int8 matrices -> [N][rows][ld] K-major device buffer"""
+    n_mod = len(mats)
+    rows, k = mats[0].shape
+    buf = np.zeros((n_mod, rows, ld), np.int8)
+    for i, m in enumerate(mats):
+        buf[i, :, :k] = m
+    return torch.from_numpy(buf).cuda()
+
+
+SHAPES = [(1, 1, 1), (17, 33, 45), (128, 256, 128), (256, 256, 256), (300, 500, 1000), (513, 260, 2049)]
+
+
+@pytest.mark.parametrize("m,n,k", SHAPES)
+def test_products_int32_and_u8(ctx, oracle, m, n, k):
+    rng = np.random.default_rng(m * 1000 + n + k)
+    n_mod = 3
+    cfg = EmuConfig(n_moduli=n_mod)
+    consts = oracle.constants(n_mod)
+    A = [rng.integers(-128, 128, size=(m, k), dtype=np.int8) for _ in range(n_mod)]
+    B = [rng.integers(-128, 128, size=(k, n), dtype=np.int8) for _ in range(n_mod)]
+    ld = ctx.plane_ld(k)
+    pa = _planes_kmajor(A, ld)
+    pb = _planes_kmajor([b.T for b in B], ld)
+    out = torch.zeros((n_mod, n, m), dtype=torch.int32, device="cuda")
+    ctx.stage_products(cfg, m, n, k, pa, pb, _lib.OZK_PRODUCTS_I32, out, m)
+    u = torch.zeros((n_mod, n, m), dtype=torch.uint8, device="cuda")
+    ctx.stage_products(cfg, m, n, k, pa, pb, _lib.OZK_PRODUCTS_U8, u, m)
+    got = out.cpu().numpy()
+    got_u = u.cpu().numpy()
+    for i in range(n_mod):
+        want = oracle.int8_gemm(A[i], B[i])
+        np.testing.assert_array_equal(got[i].T, want)
+        p, pinv = consts.moduli[i], consts.pinv_mulhi[i]
+        want_u = np.vectorize(lambda x: oracle.mod_u8(int(x), p, pinv))(want).astype(np.uint8)
+        np.testing.assert_array_equal(got_u[i].T, want_u)
+
+
+def test_products_wraparound_k_2_17(ctx, oracle):
+    """SPEC.md:239 / :493: k = 2^17 all -128 -> 2^31 wraps to INT32_MIN; mod 256 = 0."""
+    m, n, k = 4, 4, 1 << 17
+    cfg = EmuConfig(n_moduli=2)
+    ld = ctx.plane_ld(k)
+    pa = torch.full((2, m, ld), -128, dtype=torch.int8, device="cuda")
+    pb = torch.full((2, n, ld), -128, dtype=torch.int8, device="cuda")
+    out = torch.zeros((2, n, m), dtype=torch.int32, device="cuda")
+    ctx.stage_products(cfg, m, n, k, pa, pb, _lib.OZK_PRODUCTS_I32, out, m)
+    assert (out == -(2 ** 31)).all()
+    u = torch.ones((2, n, m), dtype=torch.uint8, device="cuda")
+    ctx.stage_products(cfg, m, n, k, pa, pb, _lib.OZK_PRODUCTS_U8, u, m)
+    assert (u[0] == 0).all()  # p = 256
+    assert (u[1] == oracle.mod_u8(-(2 ** 31), 255, oracle.constants(2).pinv_mulhi[1])).all()
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("phi", [0.0, 0.5, 2.0, 4.0])
+def test_scale_exponents(ctx, oracle, prec, mode, phi):
+    m, n, k = 190, 130, 777
+    N = 14 if prec == 0 else 8
+    dt = np.float64 if prec == 0 else np.float32
+    a = gen_matrix(m, k, phi, 11, dt)
+    b = gen_matrix(k, n, phi, 12, dt)
+    a[5, :] = 0.0  # zero row -> sentinel mu = 1
+    b[:, 7] = 0.0
+    cfg = EmuConfig(n_moduli=N, mode=ScaleMode(mode), precision=Precision(prec))
+    mu = torch.zeros(m, dtype=torch.int32, device="cuda")
+    nu = torch.zeros(n, dtype=torch.int32, device="cuda")
+    ctx.stage_scale(_dev_colmajor(a), _dev_colmajor(b), cfg, mu, nu)
+    wmu, wnu = oracle.scale(a, b, N, mode, prec)
+    np.testing.assert_array_equal(mu.cpu().numpy(), wmu)
+    np.testing.assert_array_equal(nu.cpu().numpy(), wnu)
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("N", [2, 8, 12, 13, 16, 19, 20])
+def test_residue_planes(ctx, oracle, prec, N):
+    if prec == 1 and N > 18:
+        pytest.skip("fp32 tables stop at N = 18")
+    m, n, k = 70, 90, 300
+    dt = np.float64 if prec == 0 else np.float32
+    a = gen_matrix(m, k, 2.0, 21, dt)
+    b = gen_matrix(k, n, 2.0, 22, dt)
+    cfg = EmuConfig(n_moduli=N, mode=ScaleMode.Accurate, precision=Precision(prec))
+    mu, nu = oracle.scale(a, b, N, 1, prec)
+    ld = ctx.plane_ld(k)
+    pa = torch.zeros((N, m, ld), dtype=torch.int8, device="cuda")
+    pb = torch.zeros((N, n, ld), dtype=torch.int8, device="cuda")
+    ctx.stage_residues(_dev_colmajor(a), _dev_colmajor(b), cfg, torch.from_numpy(mu).cuda(),
+                       torch.from_numpy(nu).cuda(), pa, pb)
+    wa = oracle.residues(oracle.truncate(a, mu, 0, prec), N, prec)  # (N, m, k)
+    wb = oracle.residues(oracle.truncate(b, nu, 1, prec), N, prec)  # (N, k, n)
+    np.testing.assert_array_equal(pa.cpu().numpy()[:, :, :k], wa)
+    np.testing.assert_array_equal(pb.cpu().numpy()[:, :, :k], wb.transpose(0, 2, 1))
+
+
+@pytest.mark.parametrize("N", [2, 9, 14, 20])
+@pytest.mark.parametrize("c_f32", [False, True])
+def test_reconstruct(ctx, oracle, N, c_f32):
+    m, n = 61, 37
+    rng = np.random.default_rng(N)
+    consts = oracle.constants(N)
+    U = np.stack([rng.integers(0, p, size=(m, n)) for p in consts.moduli[:N]]).astype(np.uint8)
+    mu = rng.integers(-60, 60, size=m).astype(np.int32)
+    nu = rng.integers(-60, 60, size=n).astype(np.int32)
+    c1, c2 = oracle.accumulate(U, N)
+    want = oracle.unscale(oracle.crt_reduce(c1, c2, N), mu, nu)
+    ldu = (m + 15) // 16 * 16
+    Ud = np.zeros((N, n, ldu), np.uint8)
+    Ud[:, :, :m] = U.transpose(0, 2, 1)
+    cdt = torch.float32 if c_f32 else torch.float64
+    Cd = torch.zeros((n, m), dtype=cdt, device="cuda").t()
+    ctx.stage_reconstruct(EmuConfig(n_moduli=N), m, n, torch.from_numpy(Ud).cuda(), ldu,
+                          torch.from_numpy(mu).cuda(), torch.from_numpy(nu).cuda(), Cd)
+    got = Cd.cpu().numpy()
+    if c_f32:
+        np.testing.assert_array_equal(got, want.astype(np.float32))
+    else:
+        np.testing.assert_array_equal(_bits(got), _bits(want))
+
+
+GEMM_CASES = [
+    (64, 64, 64, 0.5, 14),
+    (100, 130, 257, 0.0, 14),
+    (257, 129, 1000, 0.5, 12),
+    (300, 300, 300, 2.0, 16),
+    (33, 500, 4000, 1.0, 20),
+    (520, 260, 130, 4.0, 17),
+    (1, 1, 1, 0.5, 2),
+]
+
+
+@pytest.mark.parametrize("m,n,k,phi,N", GEMM_CASES)
+@pytest.mark.parametrize("mode", [ScaleMode.Fast, ScaleMode.Accurate])
+def test_gemm_fp64_bitexact(oracle, m, n, k, phi, N, mode):
+    a = gen_matrix(m, k, phi, 1)
+    b = gen_matrix(k, n, phi, 2)
+    got = gemm_emulated(a, b, EmuConfig(n_moduli=N, mode=mode)).c
+    want = oracle.gemm(a, b, N, int(mode))
+    np.testing.assert_array_equal(_bits(got), _bits(want))
+
+
+@pytest.mark.parametrize("m,n,k,phi,N", [(64, 64, 64, 0.5, 8), (200, 150, 700, 1.0, 6), (129, 257, 513, 0.5, 18)])
+@pytest.mark.parametrize("mode", [ScaleMode.Fast, ScaleMode.Accurate])
+@pytest.mark.parametrize("f32_inputs", [True, False])
+def test_gemm_fp32_bitexact(oracle, m, n, k, phi, N, mode, f32_inputs):
+    a = gen_matrix(m, k, phi, 3)
+    b = gen_matrix(k, n, phi, 4)
+    cfg = EmuConfig(n_moduli=N, mode=mode, precision=Precision.Fp32)
+    if f32_inputs:
+        a, b = a.astype(np.float32), b.astype(np.float32)
+    got = gemm_emulated(a, b, cfg).c
+    want = oracle.gemm(a.astype(np.float32), b.astype(np.float32), N, int(mode), prec=1)
+    np.testing.assert_array_equal(_bits(got), _bits(want))
+
+
+def test_gemm_matches_compiled_reference(ref):
+    """Direct cross-check against the unmodified reference (oracle/_ref)."""
+    a = gen_matrix(150, 700, 0.5, 5)
+    b = gen_matrix(700, 90, 0.5, 6)
+    for mode in (ScaleMode.Fast, ScaleMode.Accurate):
+        got = gemm_emulated(a, b, EmuConfig(n_moduli=15, mode=mode)).c
+        want = ref.gemm(a, b, 15, int(mode))
+        np.testing.assert_array_equal(_bits(got), _bits(want))
+
+
+def test_integer_exactness(oracle):
+    """SPEC.md:357 in accurate mode: B = I, small-integer A -> C == A exactly."""
+    a = gen_int_matrix(50, 50, 100, seed=7)
+    b = np.asfortranarray(np.eye(50))
+    got = gemm_emulated(a, b, EmuConfig(n_moduli=15, mode=ScaleMode.Accurate)).c
+    np.testing.assert_array_equal(got, a)
