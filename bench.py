@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark: emulated DGEMM (Ozaki scheme II) TFLOPS at n = 16384 on B200.
+
+Metric (BASELINE.json): emulated DGEMM/SGEMM TFLOPS = 2mnk / time, at
+m = n = k = 16384, next to native FP64 and FP32 (cuBLAS on the same GPU).
+Headline workload (configs[1]): DGEMM 16384^3, 14 moduli, fast mode — the
+paper's headline point (OS II-fast-14); the accurate-mode and
+moduli-sweep points ride along in "extra".
+
+One step = one full ozk_gemm (K1 scale -> K1 residues -> K2 N int8 GEMMs ->
+K3 CRT reconstruction) on device-resident inputs. Inputs (2 x 2.1 GB FP64)
+exceed the 126 MB L2, so no explicit flush is needed between steps.
+``e2e`` runs the same GEMM through the reference-facing host call
+(ozk_gemm_host): H2D of A and B from pinned memory, compute, D2H of C.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun, one rank per GPU): weak scaling by column blocks of B/C
+(SURVEY §8e); every rank owns an n = 16384 column block, rank 0's A is
+broadcast over NCCL inside each step (the north star's A broadcast), and
+"value" is the aggregate 2 m n_total k / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DEFAULT_N = 16384
+MODULI = 14
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--n", type=int, default=DEFAULT_N)
+    p.add_argument("--moduli", type=int, default=MODULI)
+    p.add_argument("--mode", choices=["fast", "accurate"], default="fast")
+    p.add_argument("--phi", type=float, default=0.5)
+    p.add_argument("--no-extra", action="store_true", help="skip the sweep / native / accuracy extras")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-sample", type=int, default=256, help="rows/cols of the CPU baseline sample (full k)")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ CPU baselines
+def cpu_reference_sample(n: int, k: int, moduli: int, mode: int, phi: float, min_seconds: float = 10.0):
+    """Time the UNMODIFIED reference (oracle/_ref) on a bounded sample of the
+    workload: an s x s block of C with the full inner dimension k, all host
+    threads (only its INT8 GEMMs are threaded: int8_engine.cpp:49-62)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from _oracle import RefLib
+
+    from paper_2508_03984_b200.gen import gen_matrix
+
+    ref = RefLib()
+    a = gen_matrix(n, k, phi, 1)
+    b = gen_matrix(k, n, phi, 2)
+    threads = os.cpu_count() or 1
+    runs, t0 = 0, time.perf_counter()
+    while True:
+        ref.gemm(a, b, moduli, mode, threads=threads)
+        runs += 1
+        el = time.perf_counter() - t0
+        if el >= min_seconds or runs >= 50:
+            break
+    per = el / runs
+    return {"seconds_per_sample": per, "threads": threads, "runs": runs,
+            "tflops": 2.0 * n * n * k / per / 1e12}
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference's own CPU path, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    k = args.n
+    s = args.cpu_sample
+    mode = 0 if args.mode == "fast" else 1
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from _oracle import RefLib
+
+    from paper_2508_03984_b200.gen import gen_matrix
+
+    if not RefLib.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcrtgemm_ref.so not built"}))
+        return
+    ref = RefLib()
+    a = gen_matrix(s, k, args.phi, 1)
+    b = gen_matrix(k, s, args.phi, 2)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        ref.gemm(a, b, args.moduli, mode, threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ref.gemm(a, b, args.moduli, mode, threads=threads)
+        times.append(time.perf_counter() - t0)
+    per = sum(times) / len(times)
+    v = 2.0 * s * s * k / per / 1e12
+    sample = f"C block {s}x{s} of the {args.n}^3 problem (full k={k}), oracle/_ref gemm_emulated, threads={threads}"
+    print(json.dumps({
+        "impl": "reference",
+        "metric": f"emulated DGEMM TFLOPS (2mnk/s), N={args.moduli} {args.mode}",
+        "value": v, "unit": "TFLOPS", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (rand-0.5)*exp(phi*randn), phi=%g" % args.phi,
+        "config": {"workload": f"DGEMM m=n=k={args.n}, {args.moduli} moduli, {args.mode} mode",
+                   "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "TFLOPS", "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": v, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        else:
+            self.lines = []
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, val in zip(names, f[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        load = [x for x in sm if x > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ GPU helpers
+def gen_device(rows, cols, phi, seed, dtype, device):
+    """paper generator on the device: column-major (rows x cols) tensor"""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    x = torch.rand((cols, rows), generator=g, device=device, dtype=torch.float64)
+    x = (1.0 - x) - 0.5  # rand in (0, 1]
+    if phi:
+        x.mul_(torch.exp(phi * torch.randn((cols, rows), generator=g, device=device, dtype=torch.float64)))
+    return x.to(dtype).t()
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        return {}
+
+
+def load_traffic():
+    """DRAM bytes per K2 launch from the committed ncu --set full summary (or None)"""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
+    except OSError:
+        return {}
+
+
+def native_gemm_tflops(n, dtype, steps=5):
+    import torch
+
+    a = torch.randn(n, n, device="cuda", dtype=dtype)
+    b = torch.randn(n, n, device="cuda", dtype=dtype)
+    for _ in range(2):
+        torch.mm(a, b)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(steps):
+        torch.mm(a, b)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    return 2.0 * n ** 3 / (ms * 1e-3) / 1e12
+
+
+def int8_library_tops(n):
+    """cuBLASLt int8 GEMM (torch._int_mm) on the same GPU: the library baseline for K2"""
+    import torch
+
+    a = torch.randint(-128, 127, (n, n), device="cuda", dtype=torch.int8)
+    b = torch.randint(-128, 127, (n, n), device="cuda", dtype=torch.int8).t().contiguous().t()
+    for _ in range(2):
+        torch._int_mm(a, b)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(5):
+        torch._int_mm(a, b)
+    e1.record()
+    torch.cuda.synchronize()
+    return 2.0 * n ** 3 / (e0.elapsed_time(e1) / 5 * 1e-3) / 1e12
+
+
+# ------------------------------------------------------------------ main arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2508_03984_b200 import Context, EmuConfig, Precision, ScaleMode
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    n = args.n
+    m = k = n
+    mode = ScaleMode.Fast if args.mode == "fast" else ScaleMode.Accurate
+    cfg = EmuConfig(n_moduli=args.moduli, mode=mode, precision=Precision.Fp64)
+    stream = torch.cuda.current_stream()
+    ctx = Context(local)
+    ctx.set_stream(stream.cuda_stream)
+
+    A = gen_device(m, k, args.phi, 1, torch.float64, dev)
+    B = gen_device(k, n, args.phi, 2 + rank, torch.float64, dev)  # this rank's column block
+    C = torch.empty((n, m), dtype=torch.float64, device=dev).t()
+    A_root = A.t().contiguous() if world > 1 else None  # rank 0's A, broadcast each step
+
+    def step():
+        if world > 1:
+            dist.broadcast(A_root, src=0)
+            ctx.gemm(A_root.t(), B, cfg, C)
+        else:
+            ctx.gemm(A, B, cfg, C)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    ctx.profile(True)
+    ctx.profile_read(reset=True)
+    launches0 = ctx.kernel_launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = ctx.kernel_launches - launches0
+    prof = ctx.profile_read(reset=True)
+    ctx.profile(False)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    flop = 2.0 * m * n * k
+    value = flop * world / (ms * 1e-3) / 1e12
+
+    # ---- roofline of the dominant kernel (K2, tensor-bound) ------------------------
+    peaks = load_peaks()
+    k2_ms = prof["products"][0] / max(prof["products"][1], 1)
+    k2_ops = args.moduli * 2.0 * m * n * k  # algorithmic int8 ops per launch
+    achieved = k2_ops / (k2_ms * 1e-3) / 1e12
+    bf16 = peaks.get("bf16_tflops")
+    peak = 2.0 * bf16 if bf16 else 2.0 * 1590.0
+    traffic = load_traffic().get(f"products_n{n}_N{args.moduli}_{args.mode}")
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "residue_gemm_kernel (K2, tcgen05.mma kind::i8)",
+                "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (dense INT8 = 2 x dense BF16 on sm_100)"
+                                if bf16 else "2 x fallback 1.59 PFLOP/s bf16 (B200_PROFILING.md)"),
+                "stage_ms": {kname: v[0] / max(v[1], 1) for kname, v in prof.items()}}
+
+    out = {
+        "metric": f"emulated DGEMM TFLOPS (2mnk/s) at n={n}, {args.moduli} moduli, {args.mode} mode",
+        "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (rand-0.5)*exp(phi*randn), phi={args.phi}, generated on device",
+        "config": {"workload": f"DGEMM m=n=k={n} per GPU (column block of B/C), {args.moduli} moduli, {args.mode}",
+                   "l2": "inputs (2 x 2.1 GB) larger than L2; no flush", "parallelism": f"colshard{world}"},
+        "gpu_launches": int(launches), "roofline": roofline, "clocks": clk.summary(),
+    }
+
+    # ---- end to end through the host-pointer C ABI (ozk_gemm_host) ----------------
+    if not args.no_e2e and world == 1:
+        import numpy as np
+
+        Ah = torch.empty((k, m), dtype=torch.float64, pin_memory=True)
+        Bh = torch.empty((n, k), dtype=torch.float64, pin_memory=True)
+        Ch = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
+        Ah.copy_(A.t())
+        Bh.copy_(B.t())
+        an, bn, cn = (np.asfortranarray(x.numpy().T) for x in (Ah, Bh, Ch))  # zero-copy column-major views
+        for _ in range(1):
+            ctx.gemm_host(an, bn, cfg, c=cn)
+        e_steps = max(2, min(args.steps, 4))
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            ctx.gemm_host(an, bn, cfg, c=cn)
+        e_s = (time.perf_counter() - t0) / e_steps
+        out["e2e"] = {"value": flop / e_s / 1e12, "unit": "TFLOPS", "h2d_bytes_per_step": 2 * 8 * m * k,
+                      "d2h_bytes_per_step": 8 * m * n, "ms_per_step": e_s * 1e3,
+                      "path": "ozk_gemm_host (pinned host A, B, C)"}
+
+    # ---- extras: native FP64/FP32, moduli sweep, accuracy, int8 library -----------
+    if not args.no_extra and world == 1:
+        extra = {}
+        extra["native_fp64_tflops"] = native_gemm_tflops(n, torch.float64, 3)
+        extra["native_fp32_tflops"] = native_gemm_tflops(n, torch.float32, 3)
+        extra["int8_cublaslt_tops"] = int8_library_tops(n)
+        sweep = {}
+        for N in (12, 14, 16, 18, 20):
+            for md in (ScaleMode.Fast, ScaleMode.Accurate):
+                c2 = EmuConfig(n_moduli=N, mode=md)
+                ctx.gemm(A, B, c2, C)
+                torch.cuda.synchronize()
+                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s0.record(stream)
+                for _ in range(2):
+                    ctx.gemm(A, B, c2, C)
+                s1.record(stream)
+                torch.cuda.synchronize()
+                sweep[f"{md.name.lower()}{N}"] = flop / (s0.elapsed_time(s1) / 2 * 1e-3) / 1e12
+        extra["dgemm_sweep_tflops"] = sweep
+        # accuracy vs native FP64 on a sampled block (emulated vs torch fp64 vs exact-ish fp64 reference)
+        extra["accuracy"] = accuracy_probe(ctx, A, B, cfg)
+        out["extra"] = extra
+
+    if rank == 0 and not os.environ.get("OZK_BENCH_NO_CPU"):
+        cb = cpu_reference_sample(args.cpu_sample, k, args.moduli, 0 if args.mode == "fast" else 1, args.phi)
+        out["cpu_baseline"] = {
+            "value": cb["tflops"], "unit": "TFLOPS", "cores": cb["threads"], "kind": "reference",
+            "sample": f"C block {args.cpu_sample}x{args.cpu_sample} of the {n}^3 problem (full k={k}), "
+                      f"oracle/_ref gemm_emulated, {cb['runs']} runs, {cb['seconds_per_sample']:.2f} s each"}
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def accuracy_probe(ctx, A, B, cfg):
+    """Max componentwise relative error on a 1024 x 1024 block of C (full k),
+    for this configuration and for native FP64 (cuBLAS), against the N = 20
+    accurate-mode emulation of the same block, which is exact to about one
+    ulp at phi <= 2 (2.2e-16 .. 8.5e-16)."""
+    import torch
+
+    from paper_2508_03984_b200 import EmuConfig, ScaleMode
+
+    rows = cols = 1024
+    a = A[:rows, :].t().contiguous().t()
+    b = B[:, :cols].t().contiguous().t()
+
+    def emu(n_mod, mode):
+        out = torch.empty((cols, rows), dtype=torch.float64, device=A.device).t()
+        ctx.gemm(a, b, EmuConfig(n_moduli=n_mod, mode=mode), out)
+        return out
+
+    ref = emu(20, ScaleMode.Accurate)
+    den = ref.abs().clamp_min(1e-300)
+    got = emu(cfg.n_moduli, cfg.mode)
+    native = a @ b
+    return {"block": f"{rows}x{cols}, full k", "against": "emulated N=20 accurate (~1 ulp)",
+            "emulated_max_rel": float(((got - ref).abs() / den).max()),
+            "emulated_median_rel": float(((got - ref).abs() / den).median()),
+            "native_fp64_max_rel": float(((native - ref).abs() / den).max()),
+            "native_fp64_median_rel": float(((native - ref).abs() / den).median())}
+
+
+if __name__ == "__main__":
+    main()

@@ -145,6 +145,20 @@ int ozk_stage_reconstruct(ozk_handle h, const ozk_config* cfg, int64_t m, int64_
 /* number of this library's kernels launched on the handle since creation */
 int64_t ozk_kernel_launches(ozk_handle h);
 
+/* ---- stage timing ---------------------------------------------------------
+ * With profiling enabled, ozk_gemm brackets each stage with CUDA events on
+ * the handle's stream. ozk_profile_read synchronises on them and returns the
+ * accumulated milliseconds and call counts per slot (arrays of
+ * OZK_PROFILE_SLOTS), optionally resetting the accumulators. */
+#define OZK_PROFILE_SCALE 0       /* K1a (+ the accurate-mode bound GEMM) */
+#define OZK_PROFILE_RESIDUES 1    /* K1b */
+#define OZK_PROFILE_PRODUCTS 2    /* K2  */
+#define OZK_PROFILE_RECONSTRUCT 3 /* K3  */
+#define OZK_PROFILE_TOTAL 4       /* scale .. reconstruct */
+#define OZK_PROFILE_SLOTS 5
+int ozk_profile(ozk_handle h, int enable);
+int ozk_profile_read(ozk_handle h, double* ms, int64_t* calls, int reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,8 +27,9 @@ EXPORTED_SYMBOLS = (
     "ozk_select_moduli", "ozk_mod_inverse", "ozk_build_constants", "ozk_dump_tables_csv",
     "ozk_gemm", "ozk_gemm_host", "ozk_dgemm", "ozk_sgemm",
     "ozk_stage_scale", "ozk_plane_ld", "ozk_stage_residues", "ozk_stage_products", "ozk_stage_reconstruct",
-    "ozk_kernel_launches",
+    "ozk_kernel_launches", "ozk_profile", "ozk_profile_read",
 )
+PROFILE_SLOTS = ("scale", "residues", "products", "reconstruct", "total")
 
 
 class ConfigError(ValueError):
@@ -117,6 +118,8 @@ def load() -> C.CDLL:
                                         p, i64]
     L.ozk_kernel_launches.restype = i64
     L.ozk_kernel_launches.argtypes = [p]
+    L.ozk_profile.argtypes = [p, i32]
+    L.ozk_profile_read.argtypes = [p, p, p, i32]
     _lib = L
     return L
 

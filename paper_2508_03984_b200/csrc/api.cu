@@ -16,6 +16,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "ozaki2_b200.h"
 #include "ozk_internal.h"
@@ -53,21 +55,6 @@ DevConsts to_dev(const ozk_constants& c) {
     return d;
 }
 
-// device-side non-finite scan folded into one tiny kernel per operand
-__global__ void finite_scan_kernel(const void* x, int is_f32, int64_t rows, int64_t cols, int64_t ld,
-                                   int32_t* flag) {
-    const int64_t total = rows * cols;
-    bool bad = false;
-    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = e % rows, j = e / rows;
-        const double v = is_f32 ? static_cast<double>(static_cast<const float*>(x)[i + j * ld])
-                                : static_cast<const double*>(x)[i + j * ld];
-        bad |= !isfinite(v);
-    }
-    if (__any_sync(0xffffffffu, bad) && (threadIdx.x % 32) == 0) atomicOr(flag, 1);
-}
-
 }  // namespace ozk
 
 using namespace ozk;
@@ -79,6 +66,11 @@ struct ozk_context {
     int64_t launches = 0;
     Buf planes_a, planes_b, u, stats, ints, flags, f32a, f32b, host_a, host_b, host_c;
     int32_t* flags_host = nullptr;  // pinned mirror of the device flag word
+    // stage timing (ozk_profile): CUDA events on the launching stream
+    bool profiling = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    double stage_ms[OZK_PROFILE_SLOTS] = {};
+    int64_t stage_calls[OZK_PROFILE_SLOTS] = {};
 };
 
 namespace {
@@ -104,6 +96,24 @@ int ensure(Buf& b, size_t bytes) {
     b.bytes = want;
     return OZK_OK;
 }
+
+// RAII bracket recording a start/stop event pair for one stage slot
+struct StageTimer {
+    ozk_context* h;
+    int slot;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    StageTimer(ozk_context* hh, int s) : h(hh), slot(s) {
+        if (!h->profiling) return;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, h->stream);
+    }
+    ~StageTimer() {
+        if (!h->profiling) return;
+        cudaEventRecord(e1, h->stream);
+        h->pending.push_back({slot, {e0, e1}});
+    }
+};
 
 int check_launch(ozk_context* h, int n_kernels) {
     h->launches += n_kernels;
@@ -185,11 +195,6 @@ int prepare_inputs(ozk_context* h, const ozk_config* cfg, const ozk_constants& c
     return OZK_OK;
 }
 
-int scan_finite(ozk_context* h, const Inputs& in, int64_t m, int64_t n, int64_t k, int32_t* flag) {
-    finite_scan_kernel<<<148 * 4, 256, 0, h->stream>>>(in.a, in.is_f32, m, k, in.lda, flag);
-    finite_scan_kernel<<<148 * 4, 256, 0, h->stream>>>(in.b, in.is_f32, k, n, in.ldb, flag);
-    return check_launch(h, 2);
-}
 
 // int32 scratch layout inside h->ints
 struct IntScratch {
@@ -222,6 +227,7 @@ int run_scale(ozk_context* h, const ozk_constants& c, int mode, int64_t m, int64
     ls.asum = d + ls.splits * m;
     ls.bmax = d + 2 * ls.splits * m;
     ls.bsum = ls.bmax + n;
+    ls.nonfinite = flags_dev;
     if ((st = ensure(h->ints, sizeof(int32_t) * 5 * (m + n)))) return st;
     IntScratch is = carve_ints(h, m, n);
 
@@ -319,7 +325,6 @@ int gemm_device(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, i
 
     Inputs in;
     if ((st = prepare_inputs(h, cfg, c, m, n, k, A, lda, B, ldb, in))) return st;
-    if ((st = scan_finite(h, in, m, n, k, flags_dev))) return st;
 
     const int64_t ld = plane_ld(k), ldu = u_ld(m);
     const int N = c.n_moduli;
@@ -329,15 +334,30 @@ int gemm_device(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, i
     if ((st = ensure(h->ints, sizeof(int32_t) * 5 * (m + n)))) return st;
     IntScratch is = carve_ints(h, m, n);
 
-    if ((st = run_scale(h, c, cfg->mode, m, n, k, in, is.mu, is.nu, flags_dev))) return st;
-    is = carve_ints(h, m, n);  // ints may have been re-allocated
-    int8_t* pa = static_cast<int8_t*>(h->planes_a.p);
-    int8_t* pb = static_cast<int8_t*>(h->planes_b.p);
-    if ((st = run_residues(h, c, m, n, k, in, is.mu, is.nu, pa, pb))) return st;
-    if ((st = run_products(h, c, m, n, k, pa, pb, OZK_PRODUCTS_U8, h->u.p, ldu))) return st;
-    launch_reconstruct(static_cast<const uint8_t*>(h->u.p), ldu, m, n, is.mu, is.nu, to_dev(c), alpha, beta, C, ldc,
-                       cfg->c_type == OZK_R32F, h->stream);
-    if ((st = check_launch(h, 1))) return st;
+    {
+        StageTimer total(h, OZK_PROFILE_TOTAL);
+        {
+            StageTimer t(h, OZK_PROFILE_SCALE);
+            if ((st = run_scale(h, c, cfg->mode, m, n, k, in, is.mu, is.nu, flags_dev))) return st;
+        }
+        is = carve_ints(h, m, n);  // ints may have been re-allocated
+        int8_t* pa = static_cast<int8_t*>(h->planes_a.p);
+        int8_t* pb = static_cast<int8_t*>(h->planes_b.p);
+        {
+            StageTimer t(h, OZK_PROFILE_RESIDUES);
+            if ((st = run_residues(h, c, m, n, k, in, is.mu, is.nu, pa, pb))) return st;
+        }
+        {
+            StageTimer t(h, OZK_PROFILE_PRODUCTS);
+            if ((st = run_products(h, c, m, n, k, pa, pb, OZK_PRODUCTS_U8, h->u.p, ldu))) return st;
+        }
+        {
+            StageTimer t(h, OZK_PROFILE_RECONSTRUCT);
+            launch_reconstruct(static_cast<const uint8_t*>(h->u.p), ldu, m, n, is.mu, is.nu, to_dev(c), alpha, beta, C,
+                               ldc, cfg->c_type == OZK_R32F, h->stream);
+            if ((st = check_launch(h, 1))) return st;
+        }
+    }
     return sync_check ? finish_check(h, flags_dev) : OZK_OK;
 }
 
@@ -410,6 +430,36 @@ int ozk_set_stream(ozk_handle h, void* stream) {
 }
 
 int64_t ozk_kernel_launches(ozk_handle h) { return h ? h->launches : 0; }
+
+int ozk_profile(ozk_handle h, int enable) {
+    if (!h) return OZK_INPUT_ERROR;
+    h->profiling = enable != 0;
+    return OZK_OK;
+}
+
+int ozk_profile_read(ozk_handle h, double* ms, int64_t* calls, int reset) {
+    if (!h) return OZK_INPUT_ERROR;
+    OZK_CUDA(cudaSetDevice(h->device));
+    for (auto& p : h->pending) {
+        float t = 0.f;
+        OZK_CUDA(cudaEventSynchronize(p.second.second));
+        OZK_CUDA(cudaEventElapsedTime(&t, p.second.first, p.second.second));
+        h->stage_ms[p.first] += t;
+        h->stage_calls[p.first] += 1;
+        cudaEventDestroy(p.second.first);
+        cudaEventDestroy(p.second.second);
+    }
+    h->pending.clear();
+    for (int i = 0; i < OZK_PROFILE_SLOTS; ++i) {
+        if (ms) ms[i] = h->stage_ms[i];
+        if (calls) calls[i] = h->stage_calls[i];
+        if (reset) {
+            h->stage_ms[i] = 0.0;
+            h->stage_calls[i] = 0;
+        }
+    }
+    return OZK_OK;
+}
 
 int64_t ozk_plane_ld(int64_t k) { return plane_ld(k); }
 

@@ -30,7 +30,7 @@ constexpr int kColGroups = 4; // column groups per block in row_stats
 
 __global__ void __launch_bounds__(kRowTile* kColGroups)
     row_stats_kernel(const void* __restrict__ a, int is_f32, int64_t m, int64_t k, int64_t lda, int64_t k_per_split,
-                     double* __restrict__ pmax, double* __restrict__ psum) {
+                     double* __restrict__ pmax, double* __restrict__ psum, int32_t* __restrict__ nonfinite) {
     __shared__ double smax[kColGroups][kRowTile];
     __shared__ double ssum[kColGroups][kRowTile];
     const int r = threadIdx.x % kRowTile, g = threadIdx.x / kRowTile;
@@ -68,6 +68,10 @@ __global__ void __launch_bounds__(kRowTile* kColGroups)
             }
         }
     }
+    // non-finite inputs (emulator.cpp:19-22): +-Inf shows up in the max, NaN
+    // (ignored by fmax) propagates into the sum of squares, which otherwise
+    // only adds non-negative terms and so cannot turn NaN by itself
+    if (__any_sync(0xffffffffu, isinf(mx) || isnan(s0 + s1)) && (threadIdx.x % 32) == 0) atomicOr(nonfinite, 1);
     smax[g][r] = mx;
     ssum[g][r] = s0 + s1;
     __syncthreads();
@@ -85,7 +89,7 @@ __global__ void __launch_bounds__(kRowTile* kColGroups)
 // one warp per column of B (contiguous), 8 loads in flight per lane
 __global__ void __launch_bounds__(256)
     col_stats_kernel(const void* __restrict__ b, int is_f32, int64_t k, int64_t n, int64_t ldb,
-                     double* __restrict__ cmax, double* __restrict__ csum) {
+                     double* __restrict__ cmax, double* __restrict__ csum, int32_t* __restrict__ nonfinite) {
     const int lane = threadIdx.x % 32;
     const int64_t col = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
     if (col >= n) return;
@@ -131,6 +135,7 @@ __global__ void __launch_bounds__(256)
     if (lane == 0) {
         cmax[col] = mx;
         csum[col] = sum;
+        if (isinf(mx) || isnan(sum)) atomicOr(nonfinite, 1);
     }
 }
 
@@ -286,12 +291,12 @@ void launch_row_stats(const void* a, int is_f32, int64_t m, int64_t k, int64_t l
                       cudaStream_t s) {
     const int64_t kps = (k + st.splits - 1) / st.splits;
     dim3 grid(static_cast<unsigned>((m + kRowTile - 1) / kRowTile), static_cast<unsigned>(st.splits));
-    row_stats_kernel<<<grid, kRowTile * kColGroups, 0, s>>>(a, is_f32, m, k, lda, kps, st.amax, st.asum);
+    row_stats_kernel<<<grid, kRowTile * kColGroups, 0, s>>>(a, is_f32, m, k, lda, kps, st.amax, st.asum, st.nonfinite);
 }
 
 void launch_col_stats(const void* b, int is_f32, int64_t k, int64_t n, int64_t ldb, const LineStats& st,
                       cudaStream_t s) {
-    col_stats_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, s>>>(b, is_f32, k, n, ldb, st.bmax, st.bsum);
+    col_stats_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, s>>>(b, is_f32, k, n, ldb, st.bmax, st.bsum, st.nonfinite);
 }
 
 void launch_fast_finalize(const LineStats& st, int64_t m, int64_t n, int64_t k, const DevConsts& c, int32_t* mu_exp,

@@ -45,6 +45,7 @@ struct LineStats {
     double* bmax;  // [n]
     double* bsum;  // [n]
     int splits;
+    int32_t* nonfinite;  // set to 1 if any input entry is NaN/Inf
 };
 int row_stats_splits(int64_t m, int64_t k);
 void launch_row_stats(const void* a, int a_is_f32, int64_t m, int64_t k, int64_t lda, const LineStats& st,

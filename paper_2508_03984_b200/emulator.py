@@ -128,6 +128,16 @@ class Context:
     def kernel_launches(self) -> int:
         return int(self._lib.ozk_kernel_launches(self.handle))
 
+    def profile(self, enable: bool = True) -> None:
+        _lib.check(self._lib.ozk_profile(self.handle, int(enable)))
+
+    def profile_read(self, reset: bool = True) -> dict:
+        """{stage: (total_ms, calls)} accumulated since the last reset"""
+        ms = (C.c_double * len(_lib.PROFILE_SLOTS))()
+        calls = (C.c_int64 * len(_lib.PROFILE_SLOTS))()
+        _lib.check(self._lib.ozk_profile_read(self.handle, ms, calls, int(reset)))
+        return {name: (ms[i], calls[i]) for i, name in enumerate(_lib.PROFILE_SLOTS)}
+
     # ---- host (reference-facing) GEMM ----------------------------------------------
     def gemm_host(self, a: np.ndarray, b: np.ndarray, cfg: EmuConfig, alpha: float = 1.0, beta: float = 0.0,
                   c: np.ndarray | None = None, c_dtype=np.float64, constants=None) -> np.ndarray:
