@@ -6,13 +6,18 @@
 // Data layout in HBM: plane t of A is m rows x ld bytes
 // (row i holds a'_i. mod p_t along k, K-major); plane t of B is n rows x ld
 // bytes (column j of B along k). ld = round_up(k, 16).
-//   * A is column-major, so a 64-row x 128-k tile is read with 256-byte
-//     coalesced column segments, transposed through shared memory one plane at
-//     a time, and written back as 128-byte row segments.
+//   * A is column-major, so a 32-row x 128-k tile is read with 256-byte
+//     coalesced column segments (one warp = 32 consecutive rows of one
+//     column); each thread owns 4 consecutive k of a row, packs its 4 residue
+//     bytes into one 32-bit shared-memory word (conflict-free: 33-word row
+//     pitch), and the tile leaves as 128-byte row segments. The shared tile is
+//     double-buffered so each plane costs one __syncthreads.
 //   * B columns are already contiguous along k: each thread reads 4 consecutive
 //     elements and writes one 32-bit word per plane (128 B per warp).
-// Each input element is read once per call of this pass and every plane byte
-// written once, so the pass is HBM-bound at (s + N) bytes per element.
+// Residues use the exact conversion-free symmetric-residue form where it
+// provably equals rmod_fast (ozk_device.cuh), else the literal sequence.
+// Each input element is read once and each plane byte written once: the pass
+// is HBM-bound at (s + N) bytes per element.
 #include <climits>
 
 #include "ozk_device.cuh"
@@ -20,64 +25,90 @@
 namespace ozk {
 namespace {
 
-constexpr int kTileRows = 64;
+constexpr int kTileRows = 32;
 constexpr int kTileK = 128;
-constexpr int kPerThread = kTileK / 4;  // 4 column groups x 32 columns
+constexpr int kWords = kTileK / 4;            // 32 packed words per tile row
+constexpr int kGroups = 256 / kTileRows;      // 8 column-quad groups
+constexpr int kQuads = kWords / kGroups;      // 4 quads (16 elements) per thread
 
-// Abar/Bbar entry (scaling.cpp:124-132): ceil(ldexp(|x|, e)) in [0, 64].
-__device__ __forceinline__ int8_t bound_entry(double x, int e) {
+// Abar/Bbar entry (scaling.cpp:124-132): ceil(ldexp(|x|, e)) in [0, 64], with
+// the power of two applied as one (correctly rounded) multiply when 2^e is a
+// normal double and the ceiling as a round-up add against 2^52.
+__device__ __forceinline__ uint32_t bound_entry(double x, int e) {
     if (e == INT32_MIN) return 0;
-    return static_cast<int8_t>(ceil(ldexp(fabs(x), e)));
+    const double v = (e >= -1022 && e <= 1023) ? __dmul_rn(fabs(x), pow2d(e)) : ldexp(fabs(x), e);
+    return static_cast<uint32_t>(__double2loint(__dadd_ru(v, 0x1.0p52))) & 0xffu;
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t literal_byte(T x, const DevConsts& c, int t) {
+    return static_cast<uint32_t>(static_cast<uint8_t>(rmod_fast(x, c.p[t], c.pinv64[t], c.pinv32[t], c.n)));
 }
 
 template <typename T, int KIND>
 __global__ void __launch_bounds__(256)
     a_planes_kernel(const T* __restrict__ a, int64_t m, int64_t k, int64_t lda, const int32_t* __restrict__ row_exp,
                     const DevConsts c, int8_t* __restrict__ planes, int64_t ld, int64_t plane_stride) {
-    __shared__ uint32_t tile[kTileRows][kTileK / 4 + 1];  // +1 word: conflict-free byte column writes
-    uint8_t* tb = reinterpret_cast<uint8_t*>(&tile[0][0]);
-    constexpr int kRowBytes = (kTileK / 4 + 1) * 4;
-
+    __shared__ uint32_t tile[2][kTileRows][kWords + 1];
     const int r = threadIdx.x % kTileRows, g = threadIdx.x / kTileRows;
     const int64_t row = static_cast<int64_t>(blockIdx.y) * kTileRows + r;
     const int64_t k0 = static_cast<int64_t>(blockIdx.x) * kTileK;
     const bool row_ok = row < m;
     const int e = row_ok ? row_exp[row] : 0;
 
-    T x[kPerThread];
-    int8_t bar[KIND == 1 ? kPerThread : 1];
+    T x[kQuads * 4];
+    bool fast = true;
 #pragma unroll
-    for (int q = 0; q < kPerThread; ++q) {
-        const int64_t col = k0 + g + 4 * q;
-        const bool ok = row_ok && col < k;
-        const T v = ok ? a[row + col * lda] : T(0);
-        if constexpr (KIND == 0)
-            x[q] = trunc_scaled(v, e);
-        else
-            bar[q] = ok ? bound_entry(static_cast<double>(v), e) : int8_t(0);
+    for (int q = 0; q < kQuads; ++q)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t col = k0 + 4 * (g + kGroups * q) + u;
+            const T v = (row_ok && col < k) ? a[row + col * lda] : T(0);
+            if constexpr (KIND == 0) {
+                x[4 * q + u] = trunc_scaled(v, e);
+                fast &= symmetric_residue_domain(static_cast<double>(x[4 * q + u]), c.precision, c.n);
+            } else {
+                x[4 * q + u] = v;
+            }
+        }
+    fast = __all_sync(0xffffffffu, fast);
+    double xm[KIND == 0 ? kQuads * 4 : 1];
+    if constexpr (KIND == 0) {
+#pragma unroll
+        for (int i = 0; i < kQuads * 4; ++i) xm[i] = __dadd_rn(static_cast<double>(x[i]), kMagic52);
     }
+
     const int nplanes = KIND == 0 ? c.n : 1;
     for (int t = 0; t < nplanes; ++t) {
+        uint32_t(*buf)[kWords + 1] = tile[t & 1];
 #pragma unroll
-        for (int q = 0; q < kPerThread; ++q) {
-            int8_t v;
-            if constexpr (KIND == 0)
-                v = rmod_fast(x[q], c.p[t], c.pinv64[t], c.pinv32[t], c.n);
-            else
-                v = bar[q];
-            tb[r * kRowBytes + g + 4 * q] = static_cast<uint8_t>(v);
+        for (int q = 0; q < kQuads; ++q) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = 4 * q + u;
+                uint32_t byte;
+                if constexpr (KIND == 0)
+                    byte = fast ? symmetric_residue_byte(static_cast<double>(x[i]), xm[i], c.p[t], c.pinv64[t])
+                                : literal_byte(x[i], c, t);
+                else
+                    byte = bound_entry(static_cast<double>(x[i]), e);
+                word |= byte << (8 * u);
+            }
+            buf[r][g + kGroups * q] = word;
         }
         __syncthreads();
         int8_t* dst = planes + t * plane_stride;
 #pragma unroll
-        for (int q = 0; q < (kTileRows * kTileK / 4) / 256; ++q) {
-            const int idx = q * 256 + threadIdx.x;
-            const int rr = idx / (kTileK / 4), w = idx % (kTileK / 4);
+        for (int it = 0; it < (kTileRows * kWords) / 256; ++it) {
+            const int idx = it * 256 + threadIdx.x;
+            const int rr = idx / kWords, w = idx % kWords;
             const int64_t grow = static_cast<int64_t>(blockIdx.y) * kTileRows + rr;
             const int64_t gcol = k0 + 4 * w;
-            if (grow < m && gcol < ld) *reinterpret_cast<uint32_t*>(dst + grow * ld + gcol) = tile[rr][w];
+            if (grow < m && gcol < ld) *reinterpret_cast<uint32_t*>(dst + grow * ld + gcol) = buf[rr][w];
         }
-        __syncthreads();
+        // the next plane writes the other buffer; its previous readers finished
+        // before this iteration's barrier
     }
 }
 
@@ -87,31 +118,41 @@ __global__ void __launch_bounds__(128)
                     const DevConsts c, int8_t* __restrict__ planes, int64_t ld, int64_t plane_stride) {
     const int64_t j = blockIdx.x;
     const int64_t i0 = (static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x) * 4;
-    if (i0 >= ld) return;
+    const bool active = i0 < ld;
     const int e = col_exp[j];
     const T* col = b + j * ldb;
     T x[4];
-    int8_t bar[4];
+    bool fast = true;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const int64_t i = i0 + u;
-        const T v = i < k ? col[i] : T(0);
-        if constexpr (KIND == 0)
+        const T v = (active && i < k) ? col[i] : T(0);
+        if constexpr (KIND == 0) {
             x[u] = trunc_scaled(v, e);
-        else
-            bar[u] = i < k ? bound_entry(static_cast<double>(v), e) : int8_t(0);
+            fast &= symmetric_residue_domain(static_cast<double>(x[u]), c.precision, c.n);
+        } else {
+            x[u] = v;
+        }
     }
-    const int nplanes = KIND == 0 ? c.n : 1;
-    for (int t = 0; t < nplanes; ++t) {
+    fast = __all_sync(0xffffffffu, fast);
+    if (!active) return;
+    if constexpr (KIND == 1) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) word |= bound_entry(static_cast<double>(x[u]), e) << (8 * u);
+        *reinterpret_cast<uint32_t*>(planes + j * ld + i0) = word;
+        return;
+    }
+    double xm[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xm[u] = __dadd_rn(static_cast<double>(x[u]), kMagic52);
+    for (int t = 0; t < c.n; ++t) {
         uint32_t word = 0;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            int8_t v;
-            if constexpr (KIND == 0)
-                v = rmod_fast(x[u], c.p[t], c.pinv64[t], c.pinv32[t], c.n);
-            else
-                v = bar[u];
-            word |= static_cast<uint32_t>(static_cast<uint8_t>(v)) << (8 * u);
+            const uint32_t byte = fast ? symmetric_residue_byte(static_cast<double>(x[u]), xm[u], c.p[t], c.pinv64[t])
+                                       : literal_byte(x[u], c, t);
+            word |= byte << (8 * u);
         }
         *reinterpret_cast<uint32_t*>(planes + t * plane_stride + j * ld + i0) = word;
     }

@@ -26,13 +26,19 @@ __global__ void __launch_bounds__(128)
     if (i0 >= m) return;
     double c1[4] = {0.0, 0.0, 0.0, 0.0}, c2[4] = {0.0, 0.0, 0.0, 0.0};
     const uint8_t* src = u + j * ldu + i0;
+    const bool fp64_tables = c.precision == OZK_FP64;
     for (int t = 0; t < c.n; ++t) {
         const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(src + t * plane_stride));
         const double s1 = c.s1[t], s2 = c.s2[t];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const double v = static_cast<double>((w >> (8 * q)) & 0xffu);
-            c1[q] = __dadd_rn(c1[q], __dmul_rn(s1, v));
+            // u -> double without a conversion instruction: 2^52 + u, minus 2^52
+            const double v = __dsub_rn(__hiloint2double(0x43300000, (w >> (8 * q)) & 0xffu), 0x1.0p52);
+            // FP64 tables: s1*u is exact and so is the running sum (beta_i
+            // construction), so the fused form equals the reference's
+            // mul-then-add bit for bit. FP32 tables carry the full-width s1
+            // (crt_tables.cpp:160-163): keep the two roundings there.
+            c1[q] = fp64_tables ? __fma_rn(s1, v, c1[q]) : __dadd_rn(c1[q], __dmul_rn(s1, v));
             c2[q] = __dadd_rn(c2[q], __dmul_rn(s2, v));
         }
     }

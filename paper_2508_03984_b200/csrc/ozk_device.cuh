@@ -39,6 +39,36 @@ __device__ __forceinline__ int8_t rmod_fast(float x, int p, double /*pinv64*/, f
     return static_cast<int8_t>(__float2int_rz(y));
 }
 
+// ---- exact fast residues ---------------------------------------------------
+// rmod_fast first forms q = rint(fl(x * fl(1/p))). Its total error against x/p
+// is below |x/p| 2^-52, while an integer x sits at least 1/(2p) from a
+// half-integer multiple of p (p odd; p = 256 is exact). So for |x| <= 2^50 the
+// first step already yields the symmetric residue r in [-(p-1)/2, (p-1)/2]
+// (p = 256: +-128 -> byte 0x80 either way), and the FP32 refinement passes of
+// residue.hpp:42-43 leave it unchanged (|r * pinv32| < 1/2). The FP32 path
+// (residue.hpp:47-53) gives the symmetric residue for |x| <= 2^21 at any N and
+// for all representable |x| < 2^44 once one refinement runs (N >= 5).
+// Inside that domain we compute the symmetric residue with three full-rate
+// FP64 ops and no conversion-class instructions (F2F/FRND/F2I run at 16/clk/SM
+// on sm_100 and made the literal sequence conversion-bound):
+//   qM = fma(x, pinv64, M) = M + nearest(x/p)      (M = 1.5 * 2^52)
+//   w  = fma(qM - M, -p, x + M) = M + r            (exact)
+//   r  = low 32 bits of w's encoding (M = 0 mod 2^32)
+// Outside it (huge scaled values) the literal reference sequence runs.
+constexpr double kMagic52 = 6755399441055744.0;  // 1.5 * 2^52
+
+__device__ __forceinline__ bool symmetric_residue_domain(double x, int prec, int n) {
+    const double ax = fabs(x);
+    if (prec == OZK_FP64) return ax <= 0x1.0p50;
+    return ax <= 0x1.0p21 || (n >= 5 && ax <= 0x1.0p43);
+}
+// x integer-valued, |x| <= 2^50, xm = x + kMagic52 (exact)
+__device__ __forceinline__ uint32_t symmetric_residue_byte(double x, double xm, int p, double pinv64) {
+    const double qm = __fma_rn(x, pinv64, kMagic52);
+    const double w = __fma_rn(__dsub_rn(qm, kMagic52), -static_cast<double>(p), xm);
+    return static_cast<uint32_t>(__double2loint(w)) & 0xffu;
+}
+
 // mod_u8 (reconstruct.hpp:31-37): high-half multiply by floor(2^32/p - 1)
 // then two one-sided corrections. The true y lies in (-p, 2p), so the 32-bit
 // wrapping difference is exact.
