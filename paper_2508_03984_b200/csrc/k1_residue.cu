@@ -72,30 +72,38 @@ __global__ void __launch_bounds__(256)
             }
         }
     fast = __all_sync(0xffffffffu, fast);
-    double xm[KIND == 0 ? kQuads * 4 : 1];
+    uint32_t xlo[KIND == 0 ? kQuads * 4 : 1];
     if constexpr (KIND == 0) {
 #pragma unroll
-        for (int i = 0; i < kQuads * 4; ++i) xm[i] = __dadd_rn(static_cast<double>(x[i]), kMagic52);
+        for (int i = 0; i < kQuads * 4; ++i)
+            xlo[i] = static_cast<uint32_t>(__double2loint(__dadd_rn(static_cast<double>(x[i]), kMagic52)));
     }
 
     const int nplanes = KIND == 0 ? c.n : 1;
-    for (int t = 0; t < nplanes; ++t) {
+    // fully unrolled to the compile-time bound so c.p[t] / c.pinv64[t] are
+    // immediate constant-bank operands (a runtime index turns every access into
+    // an LDC through the ADU pipe, which then bounds the kernel)
+#pragma unroll
+    for (int t = 0; t < OZK_MAX_MODULI; ++t) {
+        if (t >= nplanes) break;
         uint32_t(*buf)[kWords + 1] = tile[t & 1];
 #pragma unroll
         for (int q = 0; q < kQuads; ++q) {
-            uint32_t word = 0;
+            uint32_t v[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int i = 4 * q + u;
-                uint32_t byte;
-                if constexpr (KIND == 0)
-                    byte = fast ? symmetric_residue_byte(static_cast<double>(x[i]), xm[i], c.p[t], c.pinv64[t])
-                                : literal_byte(x[i], c, t);
-                else
-                    byte = bound_entry(static_cast<double>(x[i]), e);
-                word |= byte << (8 * u);
+                if constexpr (KIND == 0) {
+                    if (fast && t == 0 && c.p[0] == 256)  // p = 256: the residue is the low byte of x
+                        v[u] = xlo[i];
+                    else
+                        v[u] = fast ? symmetric_residue(static_cast<double>(x[i]), xlo[i], c.p[t], c.pinv64[t])
+                                    : literal_byte(x[i], c, t);
+                } else {
+                    v[u] = bound_entry(static_cast<double>(x[i]), e);
+                }
             }
-            buf[r][g + kGroups * q] = word;
+            buf[r][g + kGroups * q] = pack_low_bytes(v[0], v[1], v[2], v[3]);
         }
         __syncthreads();
         int8_t* dst = planes + t * plane_stride;
@@ -143,18 +151,23 @@ __global__ void __launch_bounds__(128)
         *reinterpret_cast<uint32_t*>(planes + j * ld + i0) = word;
         return;
     }
-    double xm[4];
+    uint32_t xlo[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) xm[u] = __dadd_rn(static_cast<double>(x[u]), kMagic52);
-    for (int t = 0; t < c.n; ++t) {
-        uint32_t word = 0;
+    for (int u = 0; u < 4; ++u)
+        xlo[u] = static_cast<uint32_t>(__double2loint(__dadd_rn(static_cast<double>(x[u]), kMagic52)));
+#pragma unroll
+    for (int t = 0; t < OZK_MAX_MODULI; ++t) {
+        if (t >= c.n) break;
+        uint32_t v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const uint32_t byte = fast ? symmetric_residue_byte(static_cast<double>(x[u]), xm[u], c.p[t], c.pinv64[t])
-                                       : literal_byte(x[u], c, t);
-            word |= byte << (8 * u);
+            if (fast && t == 0 && c.p[0] == 256)
+                v[u] = xlo[u];
+            else
+                v[u] = fast ? symmetric_residue(static_cast<double>(x[u]), xlo[u], c.p[t], c.pinv64[t])
+                            : literal_byte(x[u], c, t);
         }
-        *reinterpret_cast<uint32_t*>(planes + t * plane_stride + j * ld + i0) = word;
+        *reinterpret_cast<uint32_t*>(planes + t * plane_stride + j * ld + i0) = pack_low_bytes(v[0], v[1], v[2], v[3]);
     }
 }
 

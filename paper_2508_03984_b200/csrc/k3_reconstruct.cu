@@ -27,7 +27,9 @@ __global__ void __launch_bounds__(128)
     double c1[4] = {0.0, 0.0, 0.0, 0.0}, c2[4] = {0.0, 0.0, 0.0, 0.0};
     const uint8_t* src = u + j * ldu + i0;
     const bool fp64_tables = c.precision == OZK_FP64;
-    for (int t = 0; t < c.n; ++t) {
+#pragma unroll
+    for (int t = 0; t < OZK_MAX_MODULI; ++t) {  // compile-time bound: constants become immediates
+        if (t >= c.n) break;
         const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(src + t * plane_stride));
         const double s1 = c.s1[t], s2 = c.s2[t];
 #pragma unroll

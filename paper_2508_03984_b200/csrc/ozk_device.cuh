@@ -48,13 +48,13 @@ __device__ __forceinline__ int8_t rmod_fast(float x, int p, double /*pinv64*/, f
 // residue.hpp:42-43 leave it unchanged (|r * pinv32| < 1/2). The FP32 path
 // (residue.hpp:47-53) gives the symmetric residue for |x| <= 2^21 at any N and
 // for all representable |x| < 2^44 once one refinement runs (N >= 5).
-// Inside that domain we compute the symmetric residue with three full-rate
-// FP64 ops and no conversion-class instructions (F2F/FRND/F2I run at 16/clk/SM
-// on sm_100 and made the literal sequence conversion-bound):
-//   qM = fma(x, pinv64, M) = M + nearest(x/p)      (M = 1.5 * 2^52)
-//   w  = fma(qM - M, -p, x + M) = M + r            (exact)
-//   r  = low 32 bits of w's encoding (M = 0 mod 2^32)
-// Outside it (huge scaled values) the literal reference sequence runs.
+// Inside that domain we compute the symmetric residue with one full-rate FP64
+// FMA and one 32-bit IMAD, no conversion-class instructions (F2F/FRND/F2I run
+// at 16/clk/SM on sm_100 and made the literal sequence conversion-bound):
+//   qM = fma(x, pinv64, M) = M + q,  q = nearest(x/p)     (M = 1.5 * 2^52)
+//   r  = lo32(x + M) - lo32(qM) * p   (mod 2^32; exact because |r| <= 128)
+// since the low 32 bits of the encoding of M + v are v mod 2^32 for any
+// integer |v| < 2^51. Outside the domain the literal reference sequence runs.
 constexpr double kMagic52 = 6755399441055744.0;  // 1.5 * 2^52
 
 __device__ __forceinline__ bool symmetric_residue_domain(double x, int prec, int n) {
@@ -62,11 +62,15 @@ __device__ __forceinline__ bool symmetric_residue_domain(double x, int prec, int
     if (prec == OZK_FP64) return ax <= 0x1.0p50;
     return ax <= 0x1.0p21 || (n >= 5 && ax <= 0x1.0p43);
 }
-// x integer-valued, |x| <= 2^50, xm = x + kMagic52 (exact)
-__device__ __forceinline__ uint32_t symmetric_residue_byte(double x, double xm, int p, double pinv64) {
-    const double qm = __fma_rn(x, pinv64, kMagic52);
-    const double w = __fma_rn(__dsub_rn(qm, kMagic52), -static_cast<double>(p), xm);
-    return static_cast<uint32_t>(__double2loint(w)) & 0xffu;
+// x integer-valued, |x| <= 2^50; xlo = lo32(x + kMagic52). Returns r mod 2^32
+// (the int8 plane byte is its low byte).
+__device__ __forceinline__ uint32_t symmetric_residue(double x, uint32_t xlo, uint32_t p, double pinv64) {
+    const uint32_t qlo = static_cast<uint32_t>(__double2loint(__fma_rn(x, pinv64, kMagic52)));
+    return xlo - qlo * p;
+}
+// four residue words -> one packed word of their low bytes (3 PRMT)
+__device__ __forceinline__ uint32_t pack_low_bytes(uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+    return __byte_perm(__byte_perm(r0, r1, 0x0040), __byte_perm(r2, r3, 0x0040), 0x5410);
 }
 
 // mod_u8 (reconstruct.hpp:31-37): high-half multiply by floor(2^32/p - 1)

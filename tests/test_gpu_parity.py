@@ -201,3 +201,74 @@ def test_integer_exactness(oracle):
     got = gemm_emulated(a, b, EmuConfig(n_moduli=15, mode=ScaleMode.Accurate)).c
     np.testing.assert_array_equal(_bits(got), _bits(oracle.gemm(a, b, 15, 1)))
     assert np.all(np.abs(got - a) <= 2 * np.spacing(np.abs(a) + 1e-300))
+
+
+@pytest.mark.parametrize("prec,N,lo,hi", [(0, 12, 45, 62), (0, 14, 48, 71), (0, 2, 40, 60), (0, 20, 49, 71),
+                                          (1, 3, 18, 30), (1, 8, 35, 43), (1, 4, 20, 40)])
+def test_residue_planes_large_magnitudes(ctx, oracle, prec, N, lo, hi):
+    """Scaled values straddling the symmetric-residue domain bound (2^50 FP64,
+    2^21 / 2^43 FP32) so both the fast and the literal rmod_fast paths run."""
+    m, n, k = 40, 36, 200
+    dt = np.float64 if prec == 0 else np.float32
+    rng = np.random.default_rng(N + 100 * prec)
+    a = gen_matrix(m, k, 0.0, 31, dt)
+    b = gen_matrix(k, n, 0.0, 32, dt)
+    mu = rng.integers(lo, hi, size=m).astype(np.int32)
+    nu = rng.integers(lo, hi, size=n).astype(np.int32)
+    cfg = EmuConfig(n_moduli=N, mode=ScaleMode.Fast, precision=Precision(prec))
+    ld = ctx.plane_ld(k)
+    pa = torch.zeros((N, m, ld), dtype=torch.int8, device="cuda")
+    pb = torch.zeros((N, n, ld), dtype=torch.int8, device="cuda")
+    ctx.stage_residues(_dev_colmajor(a), _dev_colmajor(b), cfg, torch.from_numpy(mu).cuda(),
+                       torch.from_numpy(nu).cuda(), pa, pb)
+    wa = oracle.residues(oracle.truncate(a, mu, 0, prec), N, prec)
+    wb = oracle.residues(oracle.truncate(b, nu, 1, prec), N, prec)
+    np.testing.assert_array_equal(pa.cpu().numpy()[:, :, :k], wa)
+    np.testing.assert_array_equal(pb.cpu().numpy()[:, :, :k], wb.transpose(0, 2, 1))
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_nonfinite_is_input_error(bad):
+    """emulator.cpp:19-22: NaN/Inf anywhere in A or B -> InputError."""
+    from paper_2508_03984_b200 import InputError
+
+    a = gen_matrix(30, 40, 0.5, 1)
+    b = gen_matrix(40, 20, 0.5, 2)
+    a2 = a.copy()
+    a2[7, 11] = bad
+    with pytest.raises(InputError):
+        gemm_emulated(a2, b, EmuConfig(n_moduli=8))
+    b2 = b.copy()
+    b2[39, 19] = bad
+    with pytest.raises(InputError):
+        gemm_emulated(a, b2, EmuConfig(n_moduli=8, mode=ScaleMode.Accurate))
+    gemm_emulated(a, b, EmuConfig(n_moduli=8))  # the handle recovers
+
+
+def test_huge_finite_inputs(oracle):
+    """entries near the top of the FP64 range are legal (no false non-finite)"""
+    a = gen_matrix(20, 30, 1.0, 5) * 1e300
+    b = gen_matrix(30, 10, 1.0, 6) * 1e-300
+    for mode in (ScaleMode.Fast, ScaleMode.Accurate):
+        got = gemm_emulated(a, b, EmuConfig(n_moduli=14, mode=mode)).c
+        np.testing.assert_array_equal(_bits(got), _bits(oracle.gemm(a, b, 14, int(mode))))
+
+
+def test_zero_matrix_and_alpha_beta(ctx, oracle):
+    """zero inputs give exact zeros; alpha/beta extension applied in FP64"""
+    m, n, k = 64, 48, 80
+    a = gen_matrix(m, k, 0.5, 8)
+    b = gen_matrix(k, n, 0.5, 9)
+    A, B = _dev_colmajor(a), _dev_colmajor(b)
+    C0 = torch.zeros((n, m), dtype=torch.float64, device="cuda").t()
+    cfg = EmuConfig(n_moduli=14)
+    ctx.gemm(A, B, cfg, C0)
+    base = C0.cpu().numpy()
+    np.testing.assert_array_equal(_bits(base), _bits(oracle.gemm(a, b, 14, 0)))
+    Cin = torch.from_numpy(np.ascontiguousarray(gen_matrix(m, n, 0.5, 10).T)).cuda().t()
+    want = 2.5 * base + (-0.75) * Cin.cpu().numpy()
+    ctx.gemm(A, B, cfg, Cin, alpha=2.5, beta=-0.75)
+    np.testing.assert_array_equal(_bits(Cin.cpu().numpy()), _bits(want))
+    Z = torch.zeros((n, m), dtype=torch.float64, device="cuda").t()
+    ctx.gemm(_dev_colmajor(np.zeros((m, k))), B, cfg, Z)
+    assert (Z == 0).all()

@@ -242,3 +242,32 @@ def test_crt_exactness_integers(oracle, N):
         got = oracle.gemm(a, b, N, 1)
         ok = np.vectorize(lambda g, w: int(g) == w if abs(w) < 2 ** 53 else True)(got, want)
         assert ok.all(), (N, trial)
+
+
+# ---------------------------------------------------------------- symmetric-residue domain
+def _symmetric(x: int, p: int) -> int:
+    r = x % p
+    if r > p // 2 or (p % 2 == 0 and r == p // 2 and False):
+        r -= p
+    return ((r + 128) % 256) - 128  # int8 view (p = 256: +-128 -> -128)
+
+
+@pytest.mark.parametrize("n,prec,lim", [(2, 0, 2 ** 50), (12, 0, 2 ** 50), (14, 0, 2 ** 50), (20, 0, 2 ** 50),
+                                        (3, 1, 2 ** 21), (5, 1, 2 ** 43), (8, 1, 2 ** 43), (18, 1, 2 ** 43)])
+def test_rmod_fast_is_symmetric_in_domain(oracle, n, prec, lim):
+    """The claim behind the GPU's conversion-free residues (ozk_device.cuh):
+    inside |x| <= 2^50 (FP64) / the FP32 bounds, rmod_fast returns the
+    symmetric residue. Checked on random and near-half-multiple integers."""
+    c = oracle.constants(n, prec)
+    rng = np.random.default_rng(n * 10 + prec)
+    xs = [int(v) for v in rng.integers(-lim, lim, 300, dtype=np.int64)]
+    for p in c.moduli[:n]:
+        # integers whose quotient by p sits closest to a half-integer, near the bound
+        base = (lim // p) * p
+        xs += [base - p // 2, base - (p + 1) // 2, -base + p // 2, lim, -lim, lim - 1]
+    xs = np.array(xs, dtype=np.float64 if prec == 0 else np.float32)
+    planes = oracle.residues(xs.reshape(-1, 1), n, prec)
+    for i in range(n):
+        p = c.moduli[i]
+        for x, r in zip(xs, planes[i].ravel()):
+            assert int(r) == _symmetric(int(x), p), (n, prec, p, int(x), int(r))
