@@ -1,5 +1,5 @@
 // C-ABI implementation: context, workspace and the stage pipeline of
-// emulate<T> (reference: emulator.cpp:25-78), all on one CUDA stream:
+// emulate<T> (reference: emulator.cpp:25-78):
 //
 //   validate (emulator.cpp:12-23)            host checks + device finite flag
 //   [FP32 precision on FP64 data: round]     emulator.cpp:84-91
@@ -8,9 +8,17 @@
 //   K2  N residue GEMMs + mod epilogue       tcgen05 kind::i8 -> uint8 U_i
 //   K3  accumulate, CRT reduce, unscale      FP64/FP32 C (+ alpha/beta)
 //
-// Nothing here computes on the CPU: the host only validates arguments, sizes
-// the workspace and launches kernels. Without a usable CUDA device every
-// compute entry point fails with OZK_CUDA_ERROR (no fallback).
+// The pipeline is organised by column blocks of B and C (nu is
+// column-local, mu depends on A — fast mode — or on a max over all columns —
+// accurate mode). The device API runs one block; the host API runs several so
+// the H2D copy of B block j+1 and the D2H copy of C block j-1 overlap the
+// compute of block j on separate streams. Results do not depend on the
+// blocking (every stage is column-local apart from the accurate row bound,
+// which is an exact max).
+//
+// Nothing here computes on the CPU: the host validates arguments, sizes the
+// workspace and launches kernels. Without a usable CUDA device every compute
+// entry point fails with OZK_CUDA_ERROR (no fallback).
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -62,11 +70,12 @@ using namespace ozk;
 struct ozk_context {
     int device = 0;
     int num_sms = 148;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;              // compute stream (user-settable)
+    cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of ozk_gemm_host
     int64_t launches = 0;
     Buf planes_a, planes_b, u, stats, ints, flags, f32a, f32b, host_a, host_b, host_c;
     int32_t* flags_host = nullptr;  // pinned mirror of the device flag word
-    // stage timing (ozk_profile): CUDA events on the launching stream
+    // stage timing (ozk_profile): CUDA events on the compute stream
     bool profiling = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     double stage_ms[OZK_PROFILE_SLOTS] = {};
@@ -80,10 +89,15 @@ int cuda_fail(const char* what, cudaError_t e) {
     return OZK_CUDA_ERROR;
 }
 
-#define OZK_CUDA(call)                                         \
-    do {                                                       \
-        const cudaError_t e_ = (call);                         \
-        if (e_ != cudaSuccess) return cuda_fail(#call, e_);    \
+#define OZK_CUDA(call)                                      \
+    do {                                                    \
+        const cudaError_t e_ = (call);                      \
+        if (e_ != cudaSuccess) return cuda_fail(#call, e_); \
+    } while (0)
+#define OZK_TRY(call)                  \
+    do {                               \
+        const int st_ = (call);        \
+        if (st_ != OZK_OK) return st_; \
     } while (0)
 
 int ensure(Buf& b, size_t bytes) {
@@ -172,136 +186,232 @@ int validate(const ozk_config* cfg, const ozk_constants& c, int64_t m, int64_t n
     return OZK_OK;
 }
 
-struct Inputs {
-    const void* a;
+// One emulated GEMM: constants, operand views and the carved workspace.
+struct Job {
+    ozk_constants c;
+    DevConsts dc;
+    int mode;
+    int64_t m, n, k, ld, ldu;
+    const void* a;  // device operands as the kernels read them
     const void* b;
     int64_t lda, ldb;
-    int is_f32;
+    int in_f32;
+    int32_t *mu, *nu, *ma, *nb, *rowmax, *colmax, *flag_rows, *flag_cols;
+    int32_t* flags;  // [0] non-finite, [1] flagged rows, [2] flagged columns
+    double *amax, *asum, *bmax, *bsum;
+    int splits;
+    int8_t *pa, *pb;
+    uint8_t* u;
 };
 
-// FP32 precision with FP64 storage: round both operands first (emulator.cpp:84-91)
-int prepare_inputs(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int64_t m, int64_t n, int64_t k,
-                   const void* A, int64_t lda, const void* B, int64_t ldb, Inputs& in) {
-    in = {A, B, lda, ldb, cfg->a_type == OZK_R32F};
-    if (c.precision == OZK_FP32 && cfg->a_type == OZK_R64F) {
-        int st;
-        if ((st = ensure(h->f32a, sizeof(float) * m * k))) return st;
-        if ((st = ensure(h->f32b, sizeof(float) * k * n))) return st;
-        launch_round_to_f32(static_cast<const double*>(A), m, k, lda, static_cast<float*>(h->f32a.p), h->stream);
-        launch_round_to_f32(static_cast<const double*>(B), k, n, ldb, static_cast<float*>(h->f32b.p), h->stream);
-        if ((st = check_launch(h, 2))) return st;
-        in = {h->f32a.p, h->f32b.p, m, k, 1};
+int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c, int64_t m, int64_t n, int64_t k,
+          const void* A, int64_t lda, const void* B, int64_t ldb, bool need_products) {
+    J.c = c;
+    J.dc = to_dev(c);
+    J.mode = cfg->mode;
+    J.m = m;
+    J.n = n;
+    J.k = k;
+    J.ld = plane_ld(k);
+    J.ldu = u_ld(m);
+    const int N = c.n_moduli;
+    J.splits = row_stats_splits(m, k);
+    OZK_TRY(ensure(h->flags, 64));
+    OZK_TRY(ensure(h->stats, sizeof(double) * (2 * J.splits * m + 2 * n)));
+    OZK_TRY(ensure(h->ints, sizeof(int32_t) * 4 * (m + n)));
+    if (need_products) {
+        OZK_TRY(ensure(h->planes_a, static_cast<size_t>(N * m * J.ld)));
+        OZK_TRY(ensure(h->planes_b, static_cast<size_t>(N * n * J.ld)));
+        OZK_TRY(ensure(h->u, static_cast<size_t>(N * n * J.ldu)));
+    } else if (cfg->mode == OZK_ACCURATE) {  // the bound operands Abar/Bbar
+        OZK_TRY(ensure(h->planes_a, static_cast<size_t>(m * J.ld)));
+        OZK_TRY(ensure(h->planes_b, static_cast<size_t>(n * J.ld)));
     }
+    J.flags = static_cast<int32_t*>(h->flags.p);
+    double* d = static_cast<double*>(h->stats.p);
+    J.amax = d;
+    J.asum = d + J.splits * m;
+    J.bmax = d + 2 * J.splits * m;
+    J.bsum = J.bmax + n;
+    int32_t* p = static_cast<int32_t*>(h->ints.p);
+    J.mu = p;
+    J.nu = J.mu + m;
+    J.ma = J.nu + n;
+    J.nb = J.ma + m;
+    J.rowmax = J.nb + n;
+    J.colmax = J.rowmax + m;
+    J.flag_rows = J.colmax + n;
+    J.flag_cols = J.flag_rows + m;
+    J.pa = static_cast<int8_t*>(h->planes_a.p);
+    J.pb = static_cast<int8_t*>(h->planes_b.p);
+    J.u = static_cast<uint8_t*>(h->u.p);
+    J.a = A;
+    J.b = B;
+    J.lda = lda;
+    J.ldb = ldb;
+    J.in_f32 = cfg->a_type == OZK_R32F;
+    OZK_CUDA(cudaMemsetAsync(J.flags, 0, 64, h->stream));
     return OZK_OK;
 }
 
-
-// int32 scratch layout inside h->ints
-struct IntScratch {
-    int32_t *mu, *nu, *ma, *nb, *rowmax, *colmax, *flag_rows, *flag_cols;
-};
-IntScratch carve_ints(ozk_context* h, int64_t m, int64_t n) {
-    int32_t* p = static_cast<int32_t*>(h->ints.p);
-    IntScratch s;
-    s.mu = p;
-    s.nu = s.mu + m;
-    s.ma = s.nu + n;
-    s.nb = s.ma + m;
-    s.rowmax = s.nb + n;
-    s.colmax = s.rowmax + m;
-    s.flag_rows = s.colmax + n;
-    s.flag_cols = s.flag_rows + m;
-    return s;
+// FP32 precision on FP64 storage (emulator.cpp:84-91): the operands are rounded
+// into FP32 staging buffers (A whole, B by column range) before any stage reads them.
+bool rounds_inputs(const Job& J, const ozk_config* cfg) {
+    return J.c.precision == OZK_FP32 && cfg->a_type == OZK_R64F;
 }
 
-// K1a. mu/nu exponents into (mu, nu); may use planes_a/planes_b as scratch (accurate).
-int run_scale(ozk_context* h, const ozk_constants& c, int mode, int64_t m, int64_t n, int64_t k, const Inputs& in,
-              int32_t* mu, int32_t* nu, int32_t* flags_dev) {
-    int st;
-    const DevConsts dc = to_dev(c);
-    LineStats ls{};
-    ls.splits = row_stats_splits(m, k);
-    if ((st = ensure(h->stats, sizeof(double) * (2 * ls.splits * m + 2 * n)))) return st;
-    double* d = static_cast<double*>(h->stats.p);
-    ls.amax = d;
-    ls.asum = d + ls.splits * m;
-    ls.bmax = d + 2 * ls.splits * m;
-    ls.bsum = ls.bmax + n;
-    ls.nonfinite = flags_dev;
-    if ((st = ensure(h->ints, sizeof(int32_t) * 5 * (m + n)))) return st;
-    IntScratch is = carve_ints(h, m, n);
-
-    launch_row_stats(in.a, in.is_f32, m, k, in.lda, ls, h->stream);
-    launch_col_stats(in.b, in.is_f32, k, n, in.ldb, ls, h->stream);
-    if ((st = check_launch(h, 2))) return st;
-    if (mode == OZK_FAST) {
-        launch_fast_finalize(ls, m, n, k, dc, mu, nu, flags_dev + 1, is.flag_rows, is.flag_cols, h->stream);
-        launch_fast_exact(in.a, in.b, in.is_f32, m, n, k, in.lda, in.ldb, dc, flags_dev + 1, is.flag_rows,
-                          is.flag_cols, mu, nu, h->stream);
-        return check_launch(h, 2);
-    }
-    // accurate: mu' exponents, Abar/Bbar planes, bound GEMM with max epilogue, budget
-    launch_accurate_base(ls, m, n, is.ma, is.nb, h->stream);
-    const int64_t ld = plane_ld(k);
-    if ((st = ensure(h->planes_a, static_cast<size_t>(m * ld * (c.n_moduli > 1 ? c.n_moduli : 1))))) return st;
-    if ((st = ensure(h->planes_b, static_cast<size_t>(n * ld * (c.n_moduli > 1 ? c.n_moduli : 1))))) return st;
-    int8_t* abar = static_cast<int8_t*>(h->planes_a.p);
-    int8_t* bbar = static_cast<int8_t*>(h->planes_b.p);
-    launch_a_planes(in.a, in.is_f32, m, k, in.lda, is.ma, dc, 1, abar, ld, h->stream);
-    launch_b_planes(in.b, in.is_f32, k, n, in.ldb, is.nb, dc, 1, bbar, ld, h->stream);
-    OZK_CUDA(cudaMemsetAsync(is.rowmax, 0, sizeof(int32_t) * (m + n), h->stream));
-    if ((st = check_launch(h, 3))) return st;
-    K2Launch L{};
-    L.a_planes = abar;
-    L.b_planes = bbar;
-    L.m = m;
-    L.n = n;
-    L.k = k;
-    L.ld = ld;
-    L.n_mod = 1;
-    L.kind = K2_MAX;
-    L.rowmax = is.rowmax;
-    L.colmax = is.colmax;
-    L.c = &dc;
-    L.num_sms = h->num_sms;
-    if ((st = launch_k2(L, h->stream))) return st;
-    launch_accurate_budget(is.ma, is.nb, is.rowmax, is.colmax, m, n, dc, mu, nu, h->stream);
-    return check_launch(h, 2);
-}
-
-int run_residues(ozk_context* h, const ozk_constants& c, int64_t m, int64_t n, int64_t k, const Inputs& in,
-                 const int32_t* mu, const int32_t* nu, int8_t* pa, int8_t* pb) {
-    const DevConsts dc = to_dev(c);
-    const int64_t ld = plane_ld(k);
-    launch_a_planes(in.a, in.is_f32, m, k, in.lda, mu, dc, 0, pa, ld, h->stream);
-    launch_b_planes(in.b, in.is_f32, k, n, in.ldb, nu, dc, 0, pb, ld, h->stream);
-    return check_launch(h, 2);
-}
-
-int run_products(ozk_context* h, const ozk_constants& c, int64_t m, int64_t n, int64_t k, const int8_t* pa,
-                 const int8_t* pb, int kind, void* out, int64_t ldo) {
-    const DevConsts dc = to_dev(c);
-    K2Launch L{};
-    L.a_planes = pa;
-    L.b_planes = pb;
-    L.m = m;
-    L.n = n;
-    L.k = k;
-    L.ld = plane_ld(k);
-    L.n_mod = c.n_moduli;
-    L.kind = kind == OZK_PRODUCTS_I32 ? K2_I32 : K2_U8;
-    L.out = out;
-    L.ldo = ldo;
-    L.c = &dc;
-    L.num_sms = h->num_sms;
-    const int st = launch_k2(L, h->stream);
-    if (st) return st;
+int round_a(ozk_context* h, Job& J, const ozk_config* cfg) {
+    if (!rounds_inputs(J, cfg)) return OZK_OK;
+    OZK_TRY(ensure(h->f32a, sizeof(float) * J.m * J.k));
+    launch_round_to_f32(static_cast<const double*>(J.a), J.m, J.k, J.lda, static_cast<float*>(h->f32a.p), h->stream);
+    J.a = h->f32a.p;
+    J.lda = J.m;
+    J.in_f32 = 1;
     return check_launch(h, 1);
 }
 
-int finish_check(ozk_context* h, int32_t* flags_dev) {
-    OZK_CUDA(cudaMemcpyAsync(h->flags_host, flags_dev, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
-    OZK_CUDA(cudaStreamSynchronize(h->stream));
+// B is rounded block by block into a k x n FP32 staging buffer; src keeps the
+// caller's FP64 view for the later blocks
+int round_b(ozk_context* h, Job& J, const ozk_config* cfg, const void* src, int64_t src_ld, int64_t j0, int64_t nj) {
+    if (!rounds_inputs(J, cfg)) return OZK_OK;
+    OZK_TRY(ensure(h->f32b, sizeof(float) * J.k * J.n));
+    launch_round_to_f32(static_cast<const double*>(src) + j0 * src_ld, J.k, nj, src_ld,
+                        static_cast<float*>(h->f32b.p) + j0 * J.k, h->stream);
+    J.b = h->f32b.p;
+    J.ldb = J.k;
+    J.in_f32 = 1;
+    return check_launch(h, 1);
+}
+
+const void* b_block(const Job& J, int64_t j0) {
+    return J.in_f32 ? static_cast<const void*>(static_cast<const float*>(J.b) + j0 * J.ldb)
+                    : static_cast<const void*>(static_cast<const double*>(J.b) + j0 * J.ldb);
+}
+
+// ---- stages ----------------------------------------------------------------------
+// rows of A: stats, and fast-mode mu (or accurate-mode mu' + the Abar plane)
+int stage_rows(ozk_context* h, Job& J) {
+    launch_row_stats(J.a, J.in_f32, J.m, J.k, J.lda, J.splits, J.amax, J.asum, J.flags, h->stream);
+    OZK_TRY(check_launch(h, 1));
+    if (J.mode == OZK_FAST) {
+        launch_fast_finalize(J.amax, J.asum, J.splits, J.m, J.k, J.dc, J.mu, J.flags + 1, J.flag_rows, h->stream);
+        launch_fast_exact(J.a, J.in_f32, 1, J.lda, J.k, J.dc, J.flags + 1, J.flag_rows, J.mu, h->stream);
+        return check_launch(h, 2);
+    }
+    launch_accurate_base(J.amax, J.splits, J.m, J.ma, h->stream);
+    launch_a_planes(J.a, J.in_f32, J.m, J.k, J.lda, J.ma, J.dc, 1, J.pa, J.ld, h->stream);
+    OZK_CUDA(cudaMemsetAsync(J.rowmax, 0, sizeof(int32_t) * J.m, h->stream));
+    return check_launch(h, 2);
+}
+
+// columns [j0, j0+nj) of B: stats and fast-mode nu, or accurate-mode nu', the
+// Bbar block and the bound GEMM Abar * Bbar_block (row maxima accumulate)
+int stage_cols(ozk_context* h, Job& J, int64_t j0, int64_t nj) {
+    const void* bj = b_block(J, j0);
+    launch_col_stats(bj, J.in_f32, J.k, nj, J.ldb, J.bmax + j0, J.bsum + j0, J.flags, h->stream);
+    OZK_TRY(check_launch(h, 1));
+    if (J.mode == OZK_FAST) {
+        launch_fast_finalize(J.bmax + j0, J.bsum + j0, 1, nj, J.k, J.dc, J.nu + j0, J.flags + 2, J.flag_cols,
+                             h->stream);
+        launch_fast_exact(bj, J.in_f32, J.ldb, 1, J.k, J.dc, J.flags + 2, J.flag_cols, J.nu + j0, h->stream);
+        return check_launch(h, 2);
+    }
+    launch_accurate_base(J.bmax + j0, 1, nj, J.nb + j0, h->stream);
+    int8_t* bbar = J.pb + j0 * J.ld;
+    launch_b_planes(bj, J.in_f32, J.k, nj, J.ldb, J.nb + j0, J.dc, 1, bbar, J.ld, J.n * J.ld, h->stream);
+    OZK_CUDA(cudaMemsetAsync(J.colmax + j0, 0, sizeof(int32_t) * nj, h->stream));
+    OZK_TRY(check_launch(h, 2));
+    K2Launch L{};
+    L.a_planes = J.pa;
+    L.b_planes = bbar;
+    L.m = J.m;
+    L.n = nj;
+    L.k = J.k;
+    L.ld = J.ld;
+    L.a_stride = J.m * J.ld;
+    L.b_stride = J.n * J.ld;
+    L.n_mod = 1;
+    L.kind = K2_MAX;
+    L.rowmax = J.rowmax;
+    L.colmax = J.colmax + j0;
+    L.c = &J.dc;
+    L.num_sms = h->num_sms;
+    OZK_TRY(launch_k2(L, h->stream));
+    return check_launch(h, 1);
+}
+
+// accurate mode, after every column block: the budgets (scaling.cpp:151-165)
+int stage_budget(ozk_context* h, Job& J) {
+    launch_accurate_budget(J.ma, J.rowmax, J.m, J.dc, J.mu, h->stream);
+    launch_accurate_budget(J.nb, J.colmax, J.n, J.dc, J.nu, h->stream);
+    return check_launch(h, 2);
+}
+
+int stage_row_residues(ozk_context* h, Job& J, const int32_t* mu, int8_t* pa) {
+    launch_a_planes(J.a, J.in_f32, J.m, J.k, J.lda, mu, J.dc, 0, pa, J.ld, h->stream);
+    return check_launch(h, 1);
+}
+
+int stage_col_residues(ozk_context* h, Job& J, int64_t j0, int64_t nj, const int32_t* nu, int8_t* pb,
+                       int64_t pb_stride) {
+    launch_b_planes(b_block(J, j0), J.in_f32, J.k, nj, J.ldb, nu + j0, J.dc, 0, pb + j0 * J.ld, J.ld, pb_stride,
+                    h->stream);
+    return check_launch(h, 1);
+}
+
+int stage_products(ozk_context* h, Job& J, int64_t j0, int64_t nj, const int8_t* pa, int64_t pa_stride,
+                   const int8_t* pb, int64_t pb_stride, int kind, void* out, int64_t ldo, int64_t out_stride) {
+    K2Launch L{};
+    L.a_planes = pa;
+    L.b_planes = pb + j0 * J.ld;
+    L.m = J.m;
+    L.n = nj;
+    L.k = J.k;
+    L.ld = J.ld;
+    L.a_stride = pa_stride;
+    L.b_stride = pb_stride;
+    L.n_mod = J.c.n_moduli;
+    L.kind = kind == OZK_PRODUCTS_I32 ? K2_I32 : K2_U8;
+    const int64_t esz = kind == OZK_PRODUCTS_I32 ? 4 : 1;
+    L.out = static_cast<uint8_t*>(out) + j0 * ldo * esz;
+    L.ldo = ldo;
+    L.out_stride = out_stride;
+    L.c = &J.dc;
+    L.num_sms = h->num_sms;
+    OZK_TRY(launch_k2(L, h->stream));
+    return check_launch(h, 1);
+}
+
+int stage_reconstruct(ozk_context* h, Job& J, int64_t j0, int64_t nj, const uint8_t* u, int64_t ldu,
+                      int64_t u_stride, const int32_t* mu, const int32_t* nu, double alpha, double beta, void* C,
+                      int64_t ldc, int c_f32) {
+    void* cj = c_f32 ? static_cast<void*>(static_cast<float*>(C) + j0 * ldc)
+                     : static_cast<void*>(static_cast<double*>(C) + j0 * ldc);
+    launch_reconstruct(u + j0 * ldu, ldu, u_stride, J.m, nj, mu, nu + j0, J.dc, alpha, beta, cj, ldc, c_f32,
+                       h->stream);
+    return check_launch(h, 1);
+}
+
+// column block [j0, j0+nj) once mu (and, in accurate mode, every nu) is known:
+// B residues -> N GEMMs -> CRT reconstruction
+int compute_block(ozk_context* h, Job& J, int64_t j0, int64_t nj, double alpha, double beta, void* C, int64_t ldc,
+                  int c_f32) {
+    {
+        StageTimer t(h, OZK_PROFILE_RESIDUES);
+        OZK_TRY(stage_col_residues(h, J, j0, nj, J.nu, J.pb, J.n * J.ld));
+    }
+    {
+        StageTimer t(h, OZK_PROFILE_PRODUCTS);
+        OZK_TRY(stage_products(h, J, j0, nj, J.pa, J.m * J.ld, J.pb, J.n * J.ld, OZK_PRODUCTS_U8, J.u, J.ldu,
+                               J.n * J.ldu));
+    }
+    StageTimer t(h, OZK_PROFILE_RECONSTRUCT);
+    return stage_reconstruct(h, J, j0, nj, J.u, J.ldu, J.n * J.ldu, J.mu, J.nu, alpha, beta, C, ldc, c_f32);
+}
+
+int finish_check(ozk_context* h, Job& J, cudaStream_t s) {
+    OZK_CUDA(cudaMemcpyAsync(h->flags_host, J.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    OZK_CUDA(cudaStreamSynchronize(s));
     if (h->flags_host[0]) {
         set_error("gemm_emulated: non-finite entry in A or B");
         return OZK_INPUT_ERROR;
@@ -309,56 +419,152 @@ int finish_check(ozk_context* h, int32_t* flags_dev) {
     return OZK_OK;
 }
 
+// scale of the whole problem with device-resident operands (one column block)
+int scale_all(ozk_context* h, Job& J, const ozk_config* cfg) {
+    const void* b_src = J.b;
+    const int64_t b_ld = J.ldb;
+    OZK_TRY(round_a(h, J, cfg));
+    OZK_TRY(round_b(h, J, cfg, b_src, b_ld, 0, J.n));
+    OZK_TRY(stage_rows(h, J));
+    OZK_TRY(stage_cols(h, J, 0, J.n));
+    if (J.mode == OZK_ACCURATE) OZK_TRY(stage_budget(h, J));
+    return OZK_OK;
+}
+
 int gemm_device(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int64_t m, int64_t n, int64_t k,
                 double alpha, const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C,
-                int64_t ldc, bool sync_check) {
-    int st;
-    if ((st = validate(cfg, c, m, n, k, lda, ldb))) return st;
+                int64_t ldc) {
+    OZK_TRY(validate(cfg, c, m, n, k, lda, ldb));
     if (ldc < m) {
         set_error("gemm_emulated: ldc < m");
         return OZK_INPUT_ERROR;
     }
     OZK_CUDA(cudaSetDevice(h->device));
-    if ((st = ensure(h->flags, 64))) return st;
-    int32_t* flags_dev = static_cast<int32_t*>(h->flags.p);
-    OZK_CUDA(cudaMemsetAsync(flags_dev, 0, 64, h->stream));
-
-    Inputs in;
-    if ((st = prepare_inputs(h, cfg, c, m, n, k, A, lda, B, ldb, in))) return st;
-
-    const int64_t ld = plane_ld(k), ldu = u_ld(m);
-    const int N = c.n_moduli;
-    if ((st = ensure(h->planes_a, static_cast<size_t>(N * m * ld)))) return st;
-    if ((st = ensure(h->planes_b, static_cast<size_t>(N * n * ld)))) return st;
-    if ((st = ensure(h->u, static_cast<size_t>(N * n * ldu)))) return st;
-    if ((st = ensure(h->ints, sizeof(int32_t) * 5 * (m + n)))) return st;
-    IntScratch is = carve_ints(h, m, n);
-
+    Job J{};
+    OZK_TRY(setup(h, J, cfg, c, m, n, k, A, lda, B, ldb, true));
+    const int c_f32 = cfg->c_type == OZK_R32F;
     {
         StageTimer total(h, OZK_PROFILE_TOTAL);
         {
             StageTimer t(h, OZK_PROFILE_SCALE);
-            if ((st = run_scale(h, c, cfg->mode, m, n, k, in, is.mu, is.nu, flags_dev))) return st;
+            OZK_TRY(scale_all(h, J, cfg));
         }
-        is = carve_ints(h, m, n);  // ints may have been re-allocated
-        int8_t* pa = static_cast<int8_t*>(h->planes_a.p);
-        int8_t* pb = static_cast<int8_t*>(h->planes_b.p);
         {
             StageTimer t(h, OZK_PROFILE_RESIDUES);
-            if ((st = run_residues(h, c, m, n, k, in, is.mu, is.nu, pa, pb))) return st;
+            OZK_TRY(stage_row_residues(h, J, J.mu, J.pa));
+        }
+        OZK_TRY(compute_block(h, J, 0, n, alpha, beta, C, ldc, c_f32));
+    }
+    return finish_check(h, J, h->stream);
+}
+
+int64_t host_block_cols(int64_t n) {
+    if (n <= 1024) return n;
+    int64_t nb = (n + 7) / 8;     // about 8 blocks
+    nb = (nb + 255) / 256 * 256;  // whole 256-column GEMM tiles
+    return nb < 512 ? 512 : nb;
+}
+
+// Host operands: H2D of A, then of B column blocks, on one copy stream; the
+// compute of block j waits for its B block; C block j leaves on a second copy
+// stream while block j+1 computes.
+int gemm_host(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int64_t m, int64_t n, int64_t k,
+              double alpha, const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C,
+              int64_t ldc) {
+    OZK_TRY(validate(cfg, c, m, n, k, lda, ldb));
+    if (ldc < m) {
+        set_error("gemm_emulated: ldc < m");
+        return OZK_INPUT_ERROR;
+    }
+    OZK_CUDA(cudaSetDevice(h->device));
+    if (!h->h2d) OZK_CUDA(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
+    if (!h->d2h) OZK_CUDA(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
+    const size_t es = cfg->a_type == OZK_R32F ? 4 : 8, cs = cfg->c_type == OZK_R32F ? 4 : 8;
+    OZK_TRY(ensure(h->host_a, es * lda * k));
+    OZK_TRY(ensure(h->host_b, es * ldb * n));
+    OZK_TRY(ensure(h->host_c, cs * ldc * n));
+    Job J{};
+    OZK_TRY(setup(h, J, cfg, c, m, n, k, h->host_a.p, lda, h->host_b.p, ldb, true));
+    const void* b_src = h->host_b.p;
+    const int c_f32 = cfg->c_type == OZK_R32F;
+    const int64_t nb = host_block_cols(n);
+    const int nblk = static_cast<int>((n + nb - 1) / nb);
+    std::vector<cudaEvent_t> ev(2 * nblk + 2);
+    for (auto& e : ev) OZK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    struct EventGuard {
+        std::vector<cudaEvent_t>& v;
+        ~EventGuard() {
+            for (auto& e : v) cudaEventDestroy(e);
+        }
+    } guard{ev};
+    cudaEvent_t evA = ev[0], evStart = ev[1];
+    auto ev_b = [&](int b) { return ev[2 + b]; };
+    auto ev_c = [&](int b) { return ev[2 + nblk + b]; };
+    auto block = [&](int b, int64_t& j0, int64_t& nj) {
+        j0 = b * nb;
+        nj = (n - j0 < nb) ? n - j0 : nb;
+    };
+    // the copy stream starts after the compute stream's earlier work (workspace reuse)
+    OZK_CUDA(cudaEventRecord(evStart, h->stream));
+    OZK_CUDA(cudaStreamWaitEvent(h->h2d, evStart, 0));
+    OZK_CUDA(cudaStreamWaitEvent(h->d2h, evStart, 0));
+    OZK_CUDA(cudaMemcpyAsync(h->host_a.p, A, es * lda * k, cudaMemcpyHostToDevice, h->h2d));
+    OZK_CUDA(cudaEventRecord(evA, h->h2d));
+    for (int b = 0; b < nblk; ++b) {
+        int64_t j0, nj;
+        block(b, j0, nj);
+        OZK_CUDA(cudaMemcpyAsync(static_cast<char*>(h->host_b.p) + es * ldb * j0,
+                                 static_cast<const char*>(B) + es * ldb * j0, es * ldb * nj, cudaMemcpyHostToDevice,
+                                 h->h2d));
+        if (beta != 0.0)
+            OZK_CUDA(cudaMemcpyAsync(static_cast<char*>(h->host_c.p) + cs * ldc * j0,
+                                     static_cast<const char*>(C) + cs * ldc * j0, cs * ldc * nj,
+                                     cudaMemcpyHostToDevice, h->h2d));
+        OZK_CUDA(cudaEventRecord(ev_b(b), h->h2d));
+    }
+    {
+        StageTimer total(h, OZK_PROFILE_TOTAL);
+        OZK_CUDA(cudaStreamWaitEvent(h->stream, evA, 0));
+        OZK_TRY(round_a(h, J, cfg));
+        {
+            StageTimer t(h, OZK_PROFILE_SCALE);
+            OZK_TRY(stage_rows(h, J));
+        }
+        if (J.mode == OZK_ACCURATE) {
+            for (int b = 0; b < nblk; ++b) {  // bound GEMM per arriving block
+                int64_t j0, nj;
+                block(b, j0, nj);
+                OZK_CUDA(cudaStreamWaitEvent(h->stream, ev_b(b), 0));
+                OZK_TRY(round_b(h, J, cfg, b_src, ldb, j0, nj));
+                StageTimer t(h, OZK_PROFILE_SCALE);
+                OZK_TRY(stage_cols(h, J, j0, nj));
+            }
+            StageTimer t(h, OZK_PROFILE_SCALE);
+            OZK_TRY(stage_budget(h, J));
         }
         {
-            StageTimer t(h, OZK_PROFILE_PRODUCTS);
-            if ((st = run_products(h, c, m, n, k, pa, pb, OZK_PRODUCTS_U8, h->u.p, ldu))) return st;
+            StageTimer t(h, OZK_PROFILE_RESIDUES);
+            OZK_TRY(stage_row_residues(h, J, J.mu, J.pa));
         }
-        {
-            StageTimer t(h, OZK_PROFILE_RECONSTRUCT);
-            launch_reconstruct(static_cast<const uint8_t*>(h->u.p), ldu, m, n, is.mu, is.nu, to_dev(c), alpha, beta, C,
-                               ldc, cfg->c_type == OZK_R32F, h->stream);
-            if ((st = check_launch(h, 1))) return st;
+        for (int b = 0; b < nblk; ++b) {
+            int64_t j0, nj;
+            block(b, j0, nj);
+            if (J.mode == OZK_FAST) {
+                OZK_CUDA(cudaStreamWaitEvent(h->stream, ev_b(b), 0));
+                OZK_TRY(round_b(h, J, cfg, b_src, ldb, j0, nj));
+                StageTimer t(h, OZK_PROFILE_SCALE);
+                OZK_TRY(stage_cols(h, J, j0, nj));
+            }
+            OZK_TRY(compute_block(h, J, j0, nj, alpha, beta, h->host_c.p, ldc, c_f32));
+            OZK_CUDA(cudaEventRecord(ev_c(b), h->stream));
+            OZK_CUDA(cudaStreamWaitEvent(h->d2h, ev_c(b), 0));
+            OZK_CUDA(cudaMemcpyAsync(static_cast<char*>(C) + cs * ldc * j0,
+                                     static_cast<const char*>(h->host_c.p) + cs * ldc * j0, cs * ldc * nj,
+                                     cudaMemcpyDeviceToHost, h->d2h));
         }
     }
-    return sync_check ? finish_check(h, flags_dev) : OZK_OK;
+    OZK_CUDA(cudaStreamSynchronize(h->d2h));
+    return finish_check(h, J, h->stream);
 }
 
 }  // namespace
@@ -366,7 +572,7 @@ int gemm_device(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, i
 extern "C" {
 
 const char* ozk_last_error(void) { return g_error.c_str(); }
-int ozk_version(void) { return 1; }
+int ozk_version(void) { return 2; }
 
 ozk_config ozk_default_config(int n_moduli, int mode, int precision) {
     ozk_config c{};
@@ -419,6 +625,12 @@ int ozk_destroy(ozk_handle h) {
                    &h->host_b, &h->host_c})
         if (b->p) cudaFree(b->p);
     if (h->flags_host) cudaFreeHost(h->flags_host);
+    if (h->h2d) cudaStreamDestroy(h->h2d);
+    if (h->d2h) cudaStreamDestroy(h->d2h);
+    for (auto& p : h->pending) {
+        cudaEventDestroy(p.second.first);
+        cudaEventDestroy(p.second.second);
+    }
     delete h;
     return OZK_OK;
 }
@@ -467,36 +679,16 @@ int ozk_gemm(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t 
              int64_t lda, const void* B, int64_t ldb, double beta, void* C, int64_t ldc) {
     if (!h) return OZK_INPUT_ERROR;
     ozk_constants c;
-    int st = resolve(cfg, c);
-    if (st) return st;
-    return gemm_device(h, cfg, c, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, true);
+    OZK_TRY(resolve(cfg, c));
+    return gemm_device(h, cfg, c, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 
 int ozk_gemm_host(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, double alpha,
                   const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C, int64_t ldc) {
     if (!h) return OZK_INPUT_ERROR;
     ozk_constants c;
-    int st = resolve(cfg, c);
-    if (st) return st;
-    if ((st = validate(cfg, c, m, n, k, lda, ldb))) return st;
-    if (ldc < m) {
-        set_error("gemm_emulated: ldc < m");
-        return OZK_INPUT_ERROR;
-    }
-    OZK_CUDA(cudaSetDevice(h->device));
-    const size_t es = cfg->a_type == OZK_R32F ? 4 : 8, cs = cfg->c_type == OZK_R32F ? 4 : 8;
-    if ((st = ensure(h->host_a, es * lda * k))) return st;
-    if ((st = ensure(h->host_b, es * ldb * n))) return st;
-    if ((st = ensure(h->host_c, cs * ldc * n))) return st;
-    OZK_CUDA(cudaMemcpyAsync(h->host_a.p, A, es * lda * k, cudaMemcpyHostToDevice, h->stream));
-    OZK_CUDA(cudaMemcpyAsync(h->host_b.p, B, es * ldb * n, cudaMemcpyHostToDevice, h->stream));
-    if (beta != 0.0) OZK_CUDA(cudaMemcpyAsync(h->host_c.p, C, cs * ldc * n, cudaMemcpyHostToDevice, h->stream));
-    if ((st = gemm_device(h, cfg, c, m, n, k, alpha, h->host_a.p, lda, h->host_b.p, ldb, beta, h->host_c.p, ldc,
-                          true)))
-        return st;
-    OZK_CUDA(cudaMemcpyAsync(C, h->host_c.p, cs * ldc * n, cudaMemcpyDeviceToHost, h->stream));
-    OZK_CUDA(cudaStreamSynchronize(h->stream));
-    return OZK_OK;
+    OZK_TRY(resolve(cfg, c));
+    return gemm_host(h, cfg, c, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 
 int ozk_dgemm(ozk_handle h, int n_moduli, int mode, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
@@ -516,16 +708,14 @@ int ozk_stage_scale(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, i
                     const void* B, int64_t ldb, int32_t* mu_exp, int32_t* nu_exp) {
     if (!h) return OZK_INPUT_ERROR;
     ozk_constants c;
-    int st = resolve(cfg, c);
-    if (st) return st;
-    if ((st = validate(cfg, c, m, n, k, lda, ldb))) return st;
+    OZK_TRY(resolve(cfg, c));
+    OZK_TRY(validate(cfg, c, m, n, k, lda, ldb));
     OZK_CUDA(cudaSetDevice(h->device));
-    if ((st = ensure(h->flags, 64))) return st;
-    int32_t* flags_dev = static_cast<int32_t*>(h->flags.p);
-    OZK_CUDA(cudaMemsetAsync(flags_dev, 0, 64, h->stream));
-    Inputs in;
-    if ((st = prepare_inputs(h, cfg, c, m, n, k, A, lda, B, ldb, in))) return st;
-    if ((st = run_scale(h, c, cfg->mode, m, n, k, in, mu_exp, nu_exp, flags_dev))) return st;
+    Job J{};
+    OZK_TRY(setup(h, J, cfg, c, m, n, k, A, lda, B, ldb, false));
+    OZK_TRY(scale_all(h, J, cfg));
+    OZK_CUDA(cudaMemcpyAsync(mu_exp, J.mu, sizeof(int32_t) * m, cudaMemcpyDeviceToDevice, h->stream));
+    OZK_CUDA(cudaMemcpyAsync(nu_exp, J.nu, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, h->stream));
     OZK_CUDA(cudaStreamSynchronize(h->stream));
     return OZK_OK;
 }
@@ -535,13 +725,16 @@ int ozk_stage_residues(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n
                        int8_t* a_planes, int8_t* b_planes) {
     if (!h) return OZK_INPUT_ERROR;
     ozk_constants c;
-    int st = resolve(cfg, c);
-    if (st) return st;
-    if ((st = validate(cfg, c, m, n, k, lda, ldb))) return st;
+    OZK_TRY(resolve(cfg, c));
+    OZK_TRY(validate(cfg, c, m, n, k, lda, ldb));
     OZK_CUDA(cudaSetDevice(h->device));
-    Inputs in;
-    if ((st = prepare_inputs(h, cfg, c, m, n, k, A, lda, B, ldb, in))) return st;
-    if ((st = run_residues(h, c, m, n, k, in, mu_exp, nu_exp, a_planes, b_planes))) return st;
+    Job J{};
+    OZK_TRY(setup(h, J, cfg, c, m, n, k, A, lda, B, ldb, false));
+    const void* b_src = J.b;
+    OZK_TRY(round_a(h, J, cfg));
+    OZK_TRY(round_b(h, J, cfg, b_src, ldb, 0, n));
+    OZK_TRY(stage_row_residues(h, J, mu_exp, a_planes));
+    OZK_TRY(stage_col_residues(h, J, 0, n, nu_exp, b_planes, n * J.ld));
     OZK_CUDA(cudaStreamSynchronize(h->stream));
     return OZK_OK;
 }
@@ -550,8 +743,7 @@ int ozk_stage_products(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n
                        const int8_t* b_planes, int kind, void* out, int64_t ldo) {
     if (!h) return OZK_INPUT_ERROR;
     ozk_constants c;
-    int st = resolve(cfg, c);
-    if (st) return st;
+    OZK_TRY(resolve(cfg, c));
     if (m < 1 || n < 1 || k < 1 || ldo < m) {
         set_error("ozk_stage_products: bad dimensions");
         return OZK_INPUT_ERROR;
@@ -561,7 +753,14 @@ int ozk_stage_products(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n
         return OZK_INPUT_ERROR;
     }
     OZK_CUDA(cudaSetDevice(h->device));
-    if ((st = run_products(h, c, m, n, k, a_planes, b_planes, kind, out, ldo))) return st;
+    Job J{};
+    J.c = c;
+    J.dc = to_dev(c);
+    J.m = m;
+    J.n = n;
+    J.k = k;
+    J.ld = plane_ld(k);
+    OZK_TRY(stage_products(h, J, 0, n, a_planes, m * J.ld, b_planes, n * J.ld, kind, out, ldo, ldo * n));
     OZK_CUDA(cudaStreamSynchronize(h->stream));
     return OZK_OK;
 }
@@ -571,16 +770,19 @@ int ozk_stage_reconstruct(ozk_handle h, const ozk_config* cfg, int64_t m, int64_
                           int64_t ldc) {
     if (!h) return OZK_INPUT_ERROR;
     ozk_constants c;
-    int st = resolve(cfg, c);
-    if (st) return st;
+    OZK_TRY(resolve(cfg, c));
     if (m < 1 || n < 1 || ldu < m || ldc < m || (ldu % 4) != 0) {
         set_error("ozk_stage_reconstruct: bad dimensions (ldu must be a multiple of 4)");
         return OZK_INPUT_ERROR;
     }
     OZK_CUDA(cudaSetDevice(h->device));
-    launch_reconstruct(U, ldu, m, n, mu_exp, nu_exp, to_dev(c), alpha, beta, C, ldc, cfg->c_type == OZK_R32F,
-                       h->stream);
-    if ((st = check_launch(h, 1))) return st;
+    Job J{};
+    J.c = c;
+    J.dc = to_dev(c);
+    J.m = m;
+    J.n = n;
+    OZK_TRY(stage_reconstruct(h, J, 0, n, U, ldu, ldu * n, mu_exp, nu_exp, alpha, beta, C, ldc,
+                              cfg->c_type == OZK_R32F));
     OZK_CUDA(cudaStreamSynchronize(h->stream));
     return OZK_OK;
 }

@@ -30,6 +30,7 @@ constexpr int kTileK = 128;
 constexpr int kWords = kTileK / 4;            // 32 packed words per tile row
 constexpr int kGroups = 256 / kTileRows;      // 8 column-quad groups
 constexpr int kQuads = kWords / kGroups;      // 4 quads (16 elements) per thread
+constexpr int kBPerThread = 8;                // B elements per thread (8 bytes per plane)
 
 // Abar/Bbar entry (scaling.cpp:124-132): ceil(ldexp(|x|, e)) in [0, 64], with
 // the power of two applied as one (correctly rounded) multiply when 2^e is a
@@ -50,6 +51,15 @@ __global__ void __launch_bounds__(256)
     a_planes_kernel(const T* __restrict__ a, int64_t m, int64_t k, int64_t lda, const int32_t* __restrict__ row_exp,
                     const DevConsts c, int8_t* __restrict__ planes, int64_t ld, int64_t plane_stride) {
     __shared__ uint32_t tile[2][kTileRows][kWords + 1];
+    // per-modulus constants staged in shared memory: a rolled modulus loop keeps
+    // the code small (a 20-way unroll thrashed the instruction cache) and
+    // broadcast LDS avoids dynamically indexed constant-bank loads
+    __shared__ double s_pinv[OZK_MAX_MODULI];
+    __shared__ uint32_t s_p[OZK_MAX_MODULI];
+    if (threadIdx.x < OZK_MAX_MODULI) {
+        s_pinv[threadIdx.x] = c.pinv64[threadIdx.x];
+        s_p[threadIdx.x] = static_cast<uint32_t>(c.p[threadIdx.x]);
+    }
     const int r = threadIdx.x % kTileRows, g = threadIdx.x / kTileRows;
     const int64_t row = static_cast<int64_t>(blockIdx.y) * kTileRows + r;
     const int64_t k0 = static_cast<int64_t>(blockIdx.x) * kTileK;
@@ -72,6 +82,7 @@ __global__ void __launch_bounds__(256)
             }
         }
     fast = __all_sync(0xffffffffu, fast);
+    __syncthreads();  // s_p / s_pinv
     uint32_t xlo[KIND == 0 ? kQuads * 4 : 1];
     if constexpr (KIND == 0) {
 #pragma unroll
@@ -80,13 +91,11 @@ __global__ void __launch_bounds__(256)
     }
 
     const int nplanes = KIND == 0 ? c.n : 1;
-    // fully unrolled to the compile-time bound so c.p[t] / c.pinv64[t] are
-    // immediate constant-bank operands (a runtime index turns every access into
-    // an LDC through the ADU pipe, which then bounds the kernel)
-#pragma unroll
-    for (int t = 0; t < OZK_MAX_MODULI; ++t) {
-        if (t >= nplanes) break;
+#pragma unroll 1
+    for (int t = 0; t < nplanes; ++t) {
         uint32_t(*buf)[kWords + 1] = tile[t & 1];
+        const uint32_t pt = s_p[t];
+        const double pinvt = s_pinv[t];
 #pragma unroll
         for (int q = 0; q < kQuads; ++q) {
             uint32_t v[4];
@@ -94,10 +103,10 @@ __global__ void __launch_bounds__(256)
             for (int u = 0; u < 4; ++u) {
                 const int i = 4 * q + u;
                 if constexpr (KIND == 0) {
-                    if (fast && t == 0 && c.p[0] == 256)  // p = 256: the residue is the low byte of x
+                    if (fast && pt == 256)  // p = 256: the residue is the low byte of x
                         v[u] = xlo[i];
                     else
-                        v[u] = fast ? symmetric_residue(static_cast<double>(x[i]), xlo[i], c.p[t], c.pinv64[t])
+                        v[u] = fast ? symmetric_residue(static_cast<double>(x[i]), xlo[i], pt, pinvt)
                                     : literal_byte(x[i], c, t);
                 } else {
                     v[u] = bound_entry(static_cast<double>(x[i]), e);
@@ -124,15 +133,21 @@ template <typename T, int KIND>
 __global__ void __launch_bounds__(128)
     b_planes_kernel(const T* __restrict__ b, int64_t k, int64_t n, int64_t ldb, const int32_t* __restrict__ col_exp,
                     const DevConsts c, int8_t* __restrict__ planes, int64_t ld, int64_t plane_stride) {
+    __shared__ double s_pinv[OZK_MAX_MODULI];
+    __shared__ uint32_t s_p[OZK_MAX_MODULI];
+    if (threadIdx.x < OZK_MAX_MODULI) {
+        s_pinv[threadIdx.x] = c.pinv64[threadIdx.x];
+        s_p[threadIdx.x] = static_cast<uint32_t>(c.p[threadIdx.x]);
+    }
     const int64_t j = blockIdx.x;
-    const int64_t i0 = (static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x) * 4;
+    const int64_t i0 = (static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x) * kBPerThread;
     const bool active = i0 < ld;
     const int e = col_exp[j];
     const T* col = b + j * ldb;
-    T x[4];
+    T x[kBPerThread];
     bool fast = true;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kBPerThread; ++u) {
         const int64_t i = i0 + u;
         const T v = (active && i < k) ? col[i] : T(0);
         if constexpr (KIND == 0) {
@@ -143,31 +158,36 @@ __global__ void __launch_bounds__(128)
         }
     }
     fast = __all_sync(0xffffffffu, fast);
+    __syncthreads();  // s_p / s_pinv
+    // ld is a multiple of 16, so a thread's 8 bytes are either all in [0, ld) or all past it
     if (!active) return;
+    int8_t* dst0 = planes + j * ld + i0;
     if constexpr (KIND == 1) {
-        uint32_t word = 0;
+        uint32_t v[kBPerThread];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) word |= bound_entry(static_cast<double>(x[u]), e) << (8 * u);
-        *reinterpret_cast<uint32_t*>(planes + j * ld + i0) = word;
+        for (int u = 0; u < kBPerThread; ++u) v[u] = bound_entry(static_cast<double>(x[u]), e);
+        *reinterpret_cast<uint2*>(dst0) = make_uint2(pack_low_bytes(v[0], v[1], v[2], v[3]),
+                                                     pack_low_bytes(v[4], v[5], v[6], v[7]));
         return;
     }
-    uint32_t xlo[4];
+    uint32_t xlo[kBPerThread];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < kBPerThread; ++u)
         xlo[u] = static_cast<uint32_t>(__double2loint(__dadd_rn(static_cast<double>(x[u]), kMagic52)));
+#pragma unroll 1
+    for (int t = 0; t < c.n; ++t) {
+        const uint32_t pt = s_p[t];
+        const double pinvt = s_pinv[t];
+        uint32_t v[kBPerThread];
 #pragma unroll
-    for (int t = 0; t < OZK_MAX_MODULI; ++t) {
-        if (t >= c.n) break;
-        uint32_t v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (fast && t == 0 && c.p[0] == 256)
+        for (int u = 0; u < kBPerThread; ++u) {
+            if (fast && pt == 256)
                 v[u] = xlo[u];
             else
-                v[u] = fast ? symmetric_residue(static_cast<double>(x[u]), xlo[u], c.p[t], c.pinv64[t])
-                            : literal_byte(x[u], c, t);
+                v[u] = fast ? symmetric_residue(static_cast<double>(x[u]), xlo[u], pt, pinvt) : literal_byte(x[u], c, t);
         }
-        *reinterpret_cast<uint32_t*>(planes + t * plane_stride + j * ld + i0) = pack_low_bytes(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<uint2*>(dst0 + t * plane_stride) =
+            make_uint2(pack_low_bytes(v[0], v[1], v[2], v[3]), pack_low_bytes(v[4], v[5], v[6], v[7]));
     }
 }
 
@@ -196,9 +216,8 @@ void a_planes_dispatch(const void* a, int is_f32, int64_t m, int64_t k, int64_t 
 
 template <int KIND>
 void b_planes_dispatch(const void* b, int is_f32, int64_t k, int64_t n, int64_t ldb, const int32_t* col_exp,
-                       const DevConsts& c, int8_t* planes, int64_t ld, cudaStream_t s) {
-    dim3 grid(static_cast<unsigned>(n), static_cast<unsigned>((ld + 511) / 512));
-    const int64_t stride = n * ld;
+                       const DevConsts& c, int8_t* planes, int64_t ld, int64_t stride, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>(n), static_cast<unsigned>((ld + 128 * kBPerThread - 1) / (128 * kBPerThread)));
     if (is_f32)
         b_planes_kernel<float, KIND><<<grid, 128, 0, s>>>(static_cast<const float*>(b), k, n, ldb, col_exp, c, planes,
                                                           ld, stride);
@@ -218,11 +237,11 @@ void launch_a_planes(const void* a, int is_f32, int64_t m, int64_t k, int64_t ld
 }
 
 void launch_b_planes(const void* b, int is_f32, int64_t k, int64_t n, int64_t ldb, const int32_t* col_exp,
-                     const DevConsts& c, int kind, int8_t* planes, int64_t ld, cudaStream_t s) {
+                     const DevConsts& c, int kind, int8_t* planes, int64_t ld, int64_t plane_stride, cudaStream_t s) {
     if (kind == 0)
-        b_planes_dispatch<0>(b, is_f32, k, n, ldb, col_exp, c, planes, ld, s);
+        b_planes_dispatch<0>(b, is_f32, k, n, ldb, col_exp, c, planes, ld, plane_stride, s);
     else
-        b_planes_dispatch<1>(b, is_f32, k, n, ldb, col_exp, c, planes, ld, s);
+        b_planes_dispatch<1>(b, is_f32, k, n, ldb, col_exp, c, planes, ld, plane_stride, s);
 }
 
 void launch_round_to_f32(const double* x, int64_t rows, int64_t cols, int64_t ld, float* out, cudaStream_t s) {

@@ -150,60 +150,41 @@ __device__ __forceinline__ bool needs_exact(double y, double mx, int64_t k) {
     return d < guard_band(k) || mx >= 0x1.0p+500 || mx < 0x1.0p-400;
 }
 
+// One thread per line (a row of A or a column of a B block). Rows combine
+// `splits` k-partials laid out [split][lines].
 __global__ void fast_finalize_kernel(const double* __restrict__ pmax, const double* __restrict__ psum, int splits,
-                                     const double* __restrict__ cmax, const double* __restrict__ csum, int64_t m,
-                                     int64_t n, int64_t k, float pp_fast, int prec, int32_t* __restrict__ mu_exp,
-                                     int32_t* __restrict__ nu_exp, int32_t* __restrict__ flag_count,
-                                     int32_t* __restrict__ flag_rows, int32_t* __restrict__ flag_cols) {
+                                     int64_t lines, int64_t k, float pp_fast, int prec, int32_t* __restrict__ exp_out,
+                                     int32_t* __restrict__ flag_count, int32_t* __restrict__ flag_list) {
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= m + n) return;
-    const bool is_row = t < m;
-    double mx, s;
-    if (is_row) {
-        mx = pmax[t];
-        s = psum[t];
-        for (int q = 1; q < splits; ++q) {
-            mx = fmax(mx, pmax[q * m + t]);
-            s += psum[q * m + t];
-        }
-    } else {
-        mx = cmax[t - m];
-        s = csum[t - m];
+    if (t >= lines) return;
+    double mx = pmax[t], s = psum[t];
+    for (int q = 1; q < splits; ++q) {
+        mx = fmax(mx, pmax[q * lines + t]);
+        s += psum[q * lines + t];
     }
     int e = 0;  // zero line: sentinel mu = 1 (scaling.cpp:80, :88)
     if (mx != 0.0) {
         const int g = ilogb(mx);
         const double y = fast_budget(ldexp(s, -2 * g), k, pp_fast);
         e = fast_exponent_from_budget(y, g, prec);
-        if (needs_exact(y, mx, k)) {
-            const int slot = atomicAdd(flag_count + (is_row ? 0 : 1), 1);
-            (is_row ? flag_rows : flag_cols)[slot] = static_cast<int32_t>(is_row ? t : t - m);
-        }
+        if (needs_exact(y, mx, k)) flag_list[atomicAdd(flag_count, 1)] = static_cast<int32_t>(t);
     }
-    if (is_row)
-        mu_exp[t] = e;
-    else
-        nu_exp[t - m] = e;
+    exp_out[t] = e;
 }
 
-// One warp per flagged line: elements x[0..k) at base + h*stride.
+// One warp per flagged line: element h of line l sits at base[l*line_step + h*elem_step].
 // Reference order: s = 0; for h: nh = ldexp(x_h, -g); s += nh*nh (no FMA).
-__global__ void fast_exact_kernel(const void* __restrict__ a, const void* __restrict__ b, int is_f32, int64_t m,
-                                  int64_t n, int64_t k, int64_t lda, int64_t ldb, float pp_fast, int prec,
-                                  const int32_t* __restrict__ flag_count, const int32_t* __restrict__ flag_rows,
-                                  const int32_t* __restrict__ flag_cols, int32_t* __restrict__ mu_exp,
-                                  int32_t* __restrict__ nu_exp) {
+__global__ void fast_exact_kernel(const void* __restrict__ base, int is_f32, int64_t line_step, int64_t elem_step,
+                                  int64_t k, float pp_fast, int prec, const int32_t* __restrict__ flag_count,
+                                  const int32_t* __restrict__ flag_list, int32_t* __restrict__ exp_out) {
     const int lane = threadIdx.x % 32;
     const int warps = gridDim.x * (blockDim.x / 32);
-    const int nrows = flag_count[0], ncols = flag_count[1];
-    for (int w = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; w < nrows + ncols; w += warps) {
-        const bool is_row = w < nrows;
-        const int64_t line = is_row ? flag_rows[w] : flag_cols[w - nrows];
-        const void* base = is_row ? a : b;
-        const int64_t off = is_row ? line : line * ldb;
-        const int64_t stride = is_row ? lda : 1;
+    const int count = *flag_count;
+    for (int w = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; w < count; w += warps) {
+        const int64_t line = flag_list[w];
+        const int64_t off = line * line_step;
         double mx = 0.0;
-        for (int64_t h = lane; h < k; h += 32) mx = fmax(mx, fabs(load_as_double(base, off + h * stride, is_f32)));
+        for (int64_t h = lane; h < k; h += 32) mx = fmax(mx, fabs(load_as_double(base, off + h * elem_step, is_f32)));
 #pragma unroll
         for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         const int g = ilogb(mx);
@@ -212,53 +193,36 @@ __global__ void fast_exact_kernel(const void* __restrict__ a, const void* __rest
             const int64_t h = h0 + lane;
             double sq = 0.0;
             if (h < k) {
-                const double nh = ldexp(load_as_double(base, off + h * stride, is_f32), -g);
+                const double nh = ldexp(load_as_double(base, off + h * elem_step, is_f32), -g);
                 sq = __dmul_rn(nh, nh);
             }
             const int cnt = k - h0 < 32 ? static_cast<int>(k - h0) : 32;
             for (int q = 0; q < cnt; ++q) s = __dadd_rn(s, __shfl_sync(0xffffffffu, sq, q));
         }
-        if (lane == 0) {
-            const int e = fast_exponent_from_budget(fast_budget(s, k, pp_fast), g, prec);
-            if (is_row)
-                mu_exp[line] = e;
-            else
-                nu_exp[line] = e;
-        }
+        if (lane == 0) exp_out[line] = fast_exponent_from_budget(fast_budget(s, k, pp_fast), g, prec);
     }
 }
 
 // mu' = 2^(5 - ilogb max|a_i.|) (scaling.cpp:112-116); INT32_MIN marks a zero line
-__global__ void accurate_base_kernel(const double* __restrict__ pmax, int splits, const double* __restrict__ cmax,
-                                     int64_t m, int64_t n, int32_t* __restrict__ ma, int32_t* __restrict__ nb) {
+__global__ void accurate_base_kernel(const double* __restrict__ pmax, int splits, int64_t lines,
+                                     int32_t* __restrict__ out) {
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= m + n) return;
-    double mx;
-    if (t < m) {
-        mx = pmax[t];
-        for (int q = 1; q < splits; ++q) mx = fmax(mx, pmax[q * m + t]);
-    } else {
-        mx = cmax[t - m];
-    }
-    const int32_t e = mx != 0.0 ? 5 - ilogb(mx) : INT32_MIN;
-    if (t < m)
-        ma[t] = e;
-    else
-        nb[t - m] = e;
+    if (t >= lines) return;
+    double mx = pmax[t];
+    for (int q = 1; q < splits; ++q) mx = fmax(mx, pmax[q * lines + t]);
+    out[t] = mx != 0.0 ? 5 - ilogb(mx) : INT32_MIN;
 }
 
 // budget of scaling.cpp:151-165: e = min(floor(pp_accu - 0.51 log2 cmax), cap),
 // mu = 2^clamp(mu' exponent + e); cmax == 0 keeps mu'; zero lines keep 1.
-__global__ void accurate_budget_kernel(const int32_t* __restrict__ ma, const int32_t* __restrict__ nb,
-                                       const int32_t* __restrict__ rowmax, const int32_t* __restrict__ colmax,
-                                       int64_t m, int64_t n, float pp_accu, int prec, int32_t* __restrict__ mu_exp,
-                                       int32_t* __restrict__ nu_exp) {
+__global__ void accurate_budget_kernel(const int32_t* __restrict__ base, const int32_t* __restrict__ cmax_in,
+                                       int64_t lines, float pp_accu, int prec, int32_t* __restrict__ exp_out) {
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= m + n) return;
-    const int32_t base = t < m ? ma[t] : nb[t - m];
-    const int32_t cmax = t < m ? rowmax[t] : colmax[t - m];
+    if (t >= lines) return;
+    const int32_t b0 = base[t];
+    const int32_t cmax = cmax_in[t];
     int32_t out = 0;
-    if (base != INT32_MIN) {
+    if (b0 != INT32_MIN) {
         int e = 0;
         if (cmax > 0) {
             e = static_cast<int>(
@@ -267,12 +231,9 @@ __global__ void accurate_budget_kernel(const int32_t* __restrict__ ma, const int
             e = e < cap ? e : cap;
         }
         const int cl = exponent_clamp(prec);
-        out = clampi(base + e, -cl, cl);
+        out = clampi(b0 + e, -cl, cl);
     }
-    if (t < m)
-        mu_exp[t] = out;
-    else
-        nu_exp[t - m] = out;
+    exp_out[t] = out;
 }
 
 }  // namespace
@@ -287,49 +248,43 @@ int row_stats_splits(int64_t m, int64_t k) {
     return static_cast<int>(splits);
 }
 
-void launch_row_stats(const void* a, int is_f32, int64_t m, int64_t k, int64_t lda, const LineStats& st,
-                      cudaStream_t s) {
-    const int64_t kps = (k + st.splits - 1) / st.splits;
-    dim3 grid(static_cast<unsigned>((m + kRowTile - 1) / kRowTile), static_cast<unsigned>(st.splits));
-    row_stats_kernel<<<grid, kRowTile * kColGroups, 0, s>>>(a, is_f32, m, k, lda, kps, st.amax, st.asum, st.nonfinite);
+void launch_row_stats(const void* a, int is_f32, int64_t m, int64_t k, int64_t lda, int splits, double* pmax,
+                      double* psum, int32_t* nonfinite, cudaStream_t s) {
+    const int64_t kps = (k + splits - 1) / splits;
+    dim3 grid(static_cast<unsigned>((m + kRowTile - 1) / kRowTile), static_cast<unsigned>(splits));
+    row_stats_kernel<<<grid, kRowTile * kColGroups, 0, s>>>(a, is_f32, m, k, lda, kps, pmax, psum, nonfinite);
 }
 
-void launch_col_stats(const void* b, int is_f32, int64_t k, int64_t n, int64_t ldb, const LineStats& st,
-                      cudaStream_t s) {
-    col_stats_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, s>>>(b, is_f32, k, n, ldb, st.bmax, st.bsum, st.nonfinite);
+void launch_col_stats(const void* b, int is_f32, int64_t k, int64_t n, int64_t ldb, double* pmax, double* psum,
+                      int32_t* nonfinite, cudaStream_t s) {
+    col_stats_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, s>>>(b, is_f32, k, n, ldb, pmax, psum, nonfinite);
 }
 
-void launch_fast_finalize(const LineStats& st, int64_t m, int64_t n, int64_t k, const DevConsts& c, int32_t* mu_exp,
-                          int32_t* nu_exp, int32_t* flag_count, int32_t* flag_rows, int32_t* flag_cols,
+void launch_fast_finalize(const double* pmax, const double* psum, int splits, int64_t lines, int64_t k,
+                          const DevConsts& c, int32_t* exp_out, int32_t* flag_count, int32_t* flag_list,
                           cudaStream_t s) {
-    cudaMemsetAsync(flag_count, 0, 2 * sizeof(int32_t), s);
-    const int64_t lines = m + n;
+    cudaMemsetAsync(flag_count, 0, sizeof(int32_t), s);
     fast_finalize_kernel<<<static_cast<unsigned>((lines + 255) / 256), 256, 0, s>>>(
-        st.amax, st.asum, st.splits, st.bmax, st.bsum, m, n, k, c.pp_fast, c.precision, mu_exp, nu_exp, flag_count,
-        flag_rows, flag_cols);
+        pmax, psum, splits, lines, k, c.pp_fast, c.precision, exp_out, flag_count, flag_list);
 }
 
-void launch_fast_exact(const void* a, const void* b, int is_f32, int64_t m, int64_t n, int64_t k, int64_t lda,
-                       int64_t ldb, const DevConsts& c, const int32_t* flag_count, const int32_t* flag_rows,
-                       const int32_t* flag_cols, int32_t* mu_exp, int32_t* nu_exp, cudaStream_t s) {
+void launch_fast_exact(const void* base, int is_f32, int64_t line_step, int64_t elem_step, int64_t k,
+                       const DevConsts& c, const int32_t* flag_count, const int32_t* flag_list, int32_t* exp_out,
+                       cudaStream_t s) {
     // The flagged count lives on the device; a fixed grid strides over it, so
     // the common case (nothing flagged) costs one tiny launch and no host sync.
-    fast_exact_kernel<<<148, 256, 0, s>>>(a, b, is_f32, m, n, k, lda, ldb, c.pp_fast, c.precision, flag_count,
-                                          flag_rows, flag_cols, mu_exp, nu_exp);
+    fast_exact_kernel<<<148, 256, 0, s>>>(base, is_f32, line_step, elem_step, k, c.pp_fast, c.precision, flag_count,
+                                          flag_list, exp_out);
 }
 
-void launch_accurate_base(const LineStats& st, int64_t m, int64_t n, int32_t* ma, int32_t* nb, cudaStream_t s) {
-    const int64_t lines = m + n;
-    accurate_base_kernel<<<static_cast<unsigned>((lines + 255) / 256), 256, 0, s>>>(st.amax, st.splits, st.bmax, m,
-                                                                                    n, ma, nb);
+void launch_accurate_base(const double* pmax, int splits, int64_t lines, int32_t* out, cudaStream_t s) {
+    accurate_base_kernel<<<static_cast<unsigned>((lines + 255) / 256), 256, 0, s>>>(pmax, splits, lines, out);
 }
 
-void launch_accurate_budget(const int32_t* ma, const int32_t* nb, const int32_t* rowmax, const int32_t* colmax,
-                            int64_t m, int64_t n, const DevConsts& c, int32_t* mu_exp, int32_t* nu_exp,
-                            cudaStream_t s) {
-    const int64_t lines = m + n;
-    accurate_budget_kernel<<<static_cast<unsigned>((lines + 255) / 256), 256, 0, s>>>(
-        ma, nb, rowmax, colmax, m, n, c.pp_accu, c.precision, mu_exp, nu_exp);
+void launch_accurate_budget(const int32_t* base, const int32_t* cmax, int64_t lines, const DevConsts& c,
+                            int32_t* exp_out, cudaStream_t s) {
+    accurate_budget_kernel<<<static_cast<unsigned>((lines + 255) / 256), 256, 0, s>>>(base, cmax, lines, c.pp_accu,
+                                                                                      c.precision, exp_out);
 }
 
 }  // namespace ozk

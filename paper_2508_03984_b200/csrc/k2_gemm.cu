@@ -416,12 +416,12 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // 3-D map over planes[n_mod][rows][ld] bytes, box {128 B of K, box_rows, 1}
-bool make_plane_map(CUtensorMap* map, const int8_t* base, int64_t k, int64_t rows, int64_t ld, int n_mod,
-                    int box_rows) {
+bool make_plane_map(CUtensorMap* map, const int8_t* base, int64_t k, int64_t rows, int64_t ld, int64_t plane_stride,
+                    int n_mod, int box_rows) {
     auto enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(n_mod)};
-    cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(ld * rows)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(plane_stride)};
     cuuint32_t box[3] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows), 1};
     cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
@@ -434,8 +434,8 @@ template <int CG, int KIND>
 int launch_impl(const K2Launch& L, cudaStream_t s) {
     using C = Cfg<CG>;
     CUtensorMap ma, mb;
-    if (!make_plane_map(&ma, L.a_planes, L.k, L.m, L.ld, L.n_mod, C::kBM) ||
-        !make_plane_map(&mb, L.b_planes, L.k, L.n, L.ld, L.n_mod, C::kBRows)) {
+    if (!make_plane_map(&ma, L.a_planes, L.k, L.m, L.ld, L.a_stride, L.n_mod, C::kBM) ||
+        !make_plane_map(&mb, L.b_planes, L.k, L.n, L.ld, L.b_stride, L.n_mod, C::kBRows)) {
         set_error("cuTensorMapEncodeTiled failed");
         return OZK_CUDA_ERROR;
     }
@@ -449,7 +449,7 @@ int launch_impl(const K2Launch& L, cudaStream_t s) {
     P.num_kb = static_cast<int>((L.k + kBK - 1) / kBK);
     P.out = L.out;
     P.ldo = L.ldo;
-    P.plane_out = L.ldo * L.n;
+    P.plane_out = L.out_stride;
     P.rowmax = L.rowmax;
     P.colmax = L.colmax;
     for (int i = 0; i < L.n_mod && L.c; ++i) {

@@ -27,21 +27,28 @@ __global__ void __launch_bounds__(128)
     double c1[4] = {0.0, 0.0, 0.0, 0.0}, c2[4] = {0.0, 0.0, 0.0, 0.0};
     const uint8_t* src = u + j * ldu + i0;
     const bool fp64_tables = c.precision == OZK_FP64;
+    const int n_mod = c.n;
+    // all plane loads first (predicated, compile-time indices: registers), so
+    // a thread has its N loads in flight at once instead of one per FP chain step
+    uint32_t w[OZK_MAX_MODULI];
+#pragma unroll
+    for (int t = 0; t < OZK_MAX_MODULI; ++t)
+        w[t] = t < n_mod ? __ldg(reinterpret_cast<const uint32_t*>(src + t * plane_stride)) : 0u;
 #pragma unroll
     for (int t = 0; t < OZK_MAX_MODULI; ++t) {  // compile-time bound: constants become immediates
-        if (t >= c.n) break;
-        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(src + t * plane_stride));
-        const double s1 = c.s1[t], s2 = c.s2[t];
+        if (t < n_mod) {
+            const double s1 = c.s1[t], s2 = c.s2[t];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            // u -> double without a conversion instruction: 2^52 + u, minus 2^52
-            const double v = __dsub_rn(__hiloint2double(0x43300000, (w >> (8 * q)) & 0xffu), 0x1.0p52);
-            // FP64 tables: s1*u is exact and so is the running sum (beta_i
-            // construction), so the fused form equals the reference's
-            // mul-then-add bit for bit. FP32 tables carry the full-width s1
-            // (crt_tables.cpp:160-163): keep the two roundings there.
-            c1[q] = fp64_tables ? __fma_rn(s1, v, c1[q]) : __dadd_rn(c1[q], __dmul_rn(s1, v));
-            c2[q] = __dadd_rn(c2[q], __dmul_rn(s2, v));
+            for (int q = 0; q < 4; ++q) {
+                // u -> double without a conversion instruction: 2^52 + u, minus 2^52
+                const double v = __dsub_rn(__hiloint2double(0x43300000, (w[t] >> (8 * q)) & 0xffu), 0x1.0p52);
+                // FP64 tables: s1*u is exact and so is the running sum (beta_i
+                // construction), so the fused form equals the reference's
+                // mul-then-add bit for bit. FP32 tables carry the full-width s1
+                // (crt_tables.cpp:160-163): keep the two roundings there.
+                c1[q] = fp64_tables ? __fma_rn(s1, v, c1[q]) : __dadd_rn(c1[q], __dmul_rn(s1, v));
+                c2[q] = __dadd_rn(c2[q], __dmul_rn(s2, v));
+            }
         }
     }
     const int ne = nu_exp[j];
@@ -67,11 +74,10 @@ __global__ void __launch_bounds__(128)
 
 }  // namespace
 
-void launch_reconstruct(const uint8_t* u, int64_t ldu, int64_t m, int64_t n, const int32_t* mu_exp,
+void launch_reconstruct(const uint8_t* u, int64_t ldu, int64_t stride, int64_t m, int64_t n, const int32_t* mu_exp,
                         const int32_t* nu_exp, const DevConsts& c, double alpha, double beta, void* C, int64_t ldc,
                         int c_is_f32, cudaStream_t s) {
     dim3 grid(static_cast<unsigned>(n), static_cast<unsigned>((m + 511) / 512));
-    const int64_t stride = ldu * n;
     const bool plain = alpha == 1.0 && beta == 0.0;
     if (c_is_f32) {
         if (plain)

@@ -38,48 +38,45 @@ inline int64_t plane_ld(int64_t k) { return (k + 15) / 16 * 16; }
 inline int64_t u_ld(int64_t m) { return (m + 15) / 16 * 16; }
 
 // ---- K1 launchers (k1_scale.cu / k1_residue.cu) ----------------------------
-// Partial reductions per line (row of A / column of B): max |x| and sum x^2.
-struct LineStats {
-    double* amax;  // [splits][m]
-    double* asum;  // [splits][m]
-    double* bmax;  // [n]
-    double* bsum;  // [n]
-    int splits;
-    int32_t* nonfinite;  // set to 1 if any input entry is NaN/Inf
-};
+// Per-line reductions (rows of A split over k into `splits` partials laid out
+// [split][m]; columns of B one warp each): max |x| and sum x^2, plus the
+// non-finite flag of emulator.cpp:19-22.
 int row_stats_splits(int64_t m, int64_t k);
-void launch_row_stats(const void* a, int a_is_f32, int64_t m, int64_t k, int64_t lda, const LineStats& st,
-                      cudaStream_t s);
-void launch_col_stats(const void* b, int b_is_f32, int64_t k, int64_t n, int64_t ldb, const LineStats& st,
-                      cudaStream_t s);
-// fast mode: exponents + near-boundary flags -> exact sequential recompute
-void launch_fast_finalize(const LineStats& st, int64_t m, int64_t n, int64_t k, const DevConsts& c, int32_t* mu_exp,
-                          int32_t* nu_exp, int32_t* flag_count, int32_t* flag_rows, int32_t* flag_cols,
+void launch_row_stats(const void* a, int is_f32, int64_t m, int64_t k, int64_t lda, int splits, double* pmax,
+                      double* psum, int32_t* nonfinite, cudaStream_t s);
+void launch_col_stats(const void* b, int is_f32, int64_t k, int64_t n, int64_t ldb, double* pmax, double* psum,
+                      int32_t* nonfinite, cudaStream_t s);
+// fast mode: exponents + near-boundary flags -> exact sequential recompute.
+// Element h of line l is at base[l*line_step + h*elem_step].
+void launch_fast_finalize(const double* pmax, const double* psum, int splits, int64_t lines, int64_t k,
+                          const DevConsts& c, int32_t* exp_out, int32_t* flag_count, int32_t* flag_list,
                           cudaStream_t s);
-void launch_fast_exact(const void* a, const void* b, int is_f32, int64_t m, int64_t n, int64_t k, int64_t lda,
-                       int64_t ldb, const DevConsts& c, const int32_t* flag_count, const int32_t* flag_rows,
-                       const int32_t* flag_cols, int32_t* mu_exp, int32_t* nu_exp, cudaStream_t s);
-// accurate mode: mu' / nu' exponents (5 - ilogb max), zero lines marked with INT32_MIN
-void launch_accurate_base(const LineStats& st, int64_t m, int64_t n, int32_t* ma, int32_t* nb, cudaStream_t s);
-void launch_accurate_budget(const int32_t* ma, const int32_t* nb, const int32_t* rowmax, const int32_t* colmax,
-                            int64_t m, int64_t n, const DevConsts& c, int32_t* mu_exp, int32_t* nu_exp,
-                            cudaStream_t s);
+void launch_fast_exact(const void* base, int is_f32, int64_t line_step, int64_t elem_step, int64_t k,
+                       const DevConsts& c, const int32_t* flag_count, const int32_t* flag_list, int32_t* exp_out,
+                       cudaStream_t s);
+// accurate mode: mu'/nu' exponents (5 - ilogb max; INT32_MIN = zero line) and
+// the budget from the bound-GEMM maxima
+void launch_accurate_base(const double* pmax, int splits, int64_t lines, int32_t* out, cudaStream_t s);
+void launch_accurate_budget(const int32_t* base, const int32_t* cmax, int64_t lines, const DevConsts& c,
+                            int32_t* exp_out, cudaStream_t s);
 
 // Plane writers. kind 0: residues of trunc(x * 2^exp) (N planes);
 // kind 1: Abar/Bbar = ceil(|x| * 2^exp) (1 plane; exp INT32_MIN = zero line).
 void launch_a_planes(const void* a, int is_f32, int64_t m, int64_t k, int64_t lda, const int32_t* row_exp,
                      const DevConsts& c, int kind, int8_t* planes, int64_t ld, cudaStream_t s);
 void launch_b_planes(const void* b, int is_f32, int64_t k, int64_t n, int64_t ldb, const int32_t* col_exp,
-                     const DevConsts& c, int kind, int8_t* planes, int64_t ld, cudaStream_t s);
+                     const DevConsts& c, int kind, int8_t* planes, int64_t ld, int64_t plane_stride, cudaStream_t s);
 // FP64 -> FP32 rounding of an input (emulator.cpp:84-91), column-major with ld
 void launch_round_to_f32(const double* x, int64_t rows, int64_t cols, int64_t ld, float* out, cudaStream_t s);
 
 // ---- K2 (k2_gemm.cu) -------------------------------------------------------
 enum K2Kind { K2_I32 = 0, K2_U8 = 1, K2_MAX = 2 };
 struct K2Launch {
-    const int8_t* a_planes;  // [n_mod][m][ld]
-    const int8_t* b_planes;  // [n_mod][n][ld]
+    const int8_t* a_planes;  // [n_mod] planes of m rows x ld bytes, plane stride a_stride
+    const int8_t* b_planes;  // [n_mod] planes of n rows x ld bytes, plane stride b_stride
     int64_t m, n, k, ld;
+    int64_t a_stride, b_stride;  // bytes between planes
+    int64_t out_stride;          // elements between output planes (I32 / U8)
     int n_mod;
     int kind;
     void* out;  // I32 / U8: [n_mod][n][ldo]
@@ -92,7 +89,7 @@ struct K2Launch {
 int launch_k2(const K2Launch& L, cudaStream_t s);
 
 // ---- K3 (k3_reconstruct.cu) -----------------------------------------------
-void launch_reconstruct(const uint8_t* u, int64_t ldu, int64_t m, int64_t n, const int32_t* mu_exp,
+void launch_reconstruct(const uint8_t* u, int64_t ldu, int64_t plane_stride, int64_t m, int64_t n, const int32_t* mu_exp,
                         const int32_t* nu_exp, const DevConsts& c, double alpha, double beta, void* C, int64_t ldc,
                         int c_is_f32, cudaStream_t s);
 
