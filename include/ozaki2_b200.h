@@ -124,11 +124,13 @@ int ozk_sgemm(ozk_handle h, int n_moduli, int mode, int64_t m, int64_t n, int64_
  *      (scale_fast / scale_accurate, scaling.hpp:28-36). */
 int ozk_stage_scale(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
                     const void* B, int64_t ldb, int32_t* mu_exp, int32_t* nu_exp);
-/* leading dimension (bytes) of one residue-plane row for inner size k */
-int64_t ozk_plane_ld(int64_t k);
-/* K1b: truncate_scale + to_residue_slices (residue.hpp:31-62). Planes are
- * K-major for the tensor cores: a_planes[N][m][ld], b_planes[N][n][ld] with
- * ld = ozk_plane_ld(k); plane i holds rmod(trunc(scaled x), p_i). */
+/* column pitch (bytes) of a residue plane whose columns hold `rows` entries */
+int64_t ozk_plane_ld(int64_t rows);
+/* K1b: truncate_scale + to_residue_slices (residue.hpp:31-62). Planes keep
+ * the reference's column-major slice layout (residue.cpp:24-42) with a
+ * 16-byte-padded leading dimension: a_planes[N][k][ozk_plane_ld(m)] (read
+ * MN-major by the GEMM), b_planes[N][n][ozk_plane_ld(k)] (read K-major);
+ * plane i holds rmod(trunc(scaled x), p_i). */
 int ozk_stage_residues(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, const void* A,
                        int64_t lda, const void* B, int64_t ldb, const int32_t* mu_exp, const int32_t* nu_exp,
                        int8_t* a_planes, int8_t* b_planes);

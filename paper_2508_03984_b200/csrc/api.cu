@@ -191,7 +191,7 @@ struct Job {
     ozk_constants c;
     DevConsts dc;
     int mode;
-    int64_t m, n, k, ld, ldu;
+    int64_t m, n, k, ld, lda_p, ldu;  // ld: B plane pitch (k), lda_p: A plane pitch (m)
     const void* a;  // device operands as the kernels read them
     const void* b;
     int64_t lda, ldb;
@@ -213,6 +213,7 @@ int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c,
     J.n = n;
     J.k = k;
     J.ld = plane_ld(k);
+    J.lda_p = plane_ld(m);
     J.ldu = u_ld(m);
     const int N = c.n_moduli;
     J.splits = row_stats_splits(m, k);
@@ -220,11 +221,11 @@ int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c,
     OZK_TRY(ensure(h->stats, sizeof(double) * (2 * J.splits * m + 2 * n)));
     OZK_TRY(ensure(h->ints, sizeof(int32_t) * 4 * (m + n)));
     if (need_products) {
-        OZK_TRY(ensure(h->planes_a, static_cast<size_t>(N * m * J.ld)));
+        OZK_TRY(ensure(h->planes_a, static_cast<size_t>(N * k * J.lda_p)));
         OZK_TRY(ensure(h->planes_b, static_cast<size_t>(N * n * J.ld)));
         OZK_TRY(ensure(h->u, static_cast<size_t>(N * n * J.ldu)));
     } else if (cfg->mode == OZK_ACCURATE) {  // the bound operands Abar/Bbar
-        OZK_TRY(ensure(h->planes_a, static_cast<size_t>(m * J.ld)));
+        OZK_TRY(ensure(h->planes_a, static_cast<size_t>(k * J.lda_p)));
         OZK_TRY(ensure(h->planes_b, static_cast<size_t>(n * J.ld)));
     }
     J.flags = static_cast<int32_t*>(h->flags.p);
@@ -299,7 +300,7 @@ int stage_rows(ozk_context* h, Job& J) {
         return check_launch(h, 2);
     }
     launch_accurate_base(J.amax, J.splits, J.m, J.ma, h->stream);
-    launch_a_planes(J.a, J.in_f32, J.m, J.k, J.lda, J.ma, J.dc, 1, J.pa, J.ld, h->stream);
+    launch_a_planes(J.a, J.in_f32, J.m, J.k, J.lda, J.ma, J.dc, 1, J.pa, J.lda_p, J.k * J.lda_p, h->stream);
     OZK_CUDA(cudaMemsetAsync(J.rowmax, 0, sizeof(int32_t) * J.m, h->stream));
     return check_launch(h, 2);
 }
@@ -328,7 +329,8 @@ int stage_cols(ozk_context* h, Job& J, int64_t j0, int64_t nj) {
     L.n = nj;
     L.k = J.k;
     L.ld = J.ld;
-    L.a_stride = J.m * J.ld;
+    L.lda = J.lda_p;
+    L.a_stride = J.k * J.lda_p;
     L.b_stride = J.n * J.ld;
     L.n_mod = 1;
     L.kind = K2_MAX;
@@ -348,7 +350,7 @@ int stage_budget(ozk_context* h, Job& J) {
 }
 
 int stage_row_residues(ozk_context* h, Job& J, const int32_t* mu, int8_t* pa) {
-    launch_a_planes(J.a, J.in_f32, J.m, J.k, J.lda, mu, J.dc, 0, pa, J.ld, h->stream);
+    launch_a_planes(J.a, J.in_f32, J.m, J.k, J.lda, mu, J.dc, 0, pa, J.lda_p, J.k * J.lda_p, h->stream);
     return check_launch(h, 1);
 }
 
@@ -368,6 +370,7 @@ int stage_products(ozk_context* h, Job& J, int64_t j0, int64_t nj, const int8_t*
     L.n = nj;
     L.k = J.k;
     L.ld = J.ld;
+    L.lda = J.lda_p;
     L.a_stride = pa_stride;
     L.b_stride = pb_stride;
     L.n_mod = J.c.n_moduli;
@@ -402,7 +405,7 @@ int compute_block(ozk_context* h, Job& J, int64_t j0, int64_t nj, double alpha, 
     }
     {
         StageTimer t(h, OZK_PROFILE_PRODUCTS);
-        OZK_TRY(stage_products(h, J, j0, nj, J.pa, J.m * J.ld, J.pb, J.n * J.ld, OZK_PRODUCTS_U8, J.u, J.ldu,
+        OZK_TRY(stage_products(h, J, j0, nj, J.pa, J.k * J.lda_p, J.pb, J.n * J.ld, OZK_PRODUCTS_U8, J.u, J.ldu,
                                J.n * J.ldu));
     }
     StageTimer t(h, OZK_PROFILE_RECONSTRUCT);
@@ -760,7 +763,8 @@ int ozk_stage_products(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n
     J.n = n;
     J.k = k;
     J.ld = plane_ld(k);
-    OZK_TRY(stage_products(h, J, 0, n, a_planes, m * J.ld, b_planes, n * J.ld, kind, out, ldo, ldo * n));
+    J.lda_p = plane_ld(m);
+    OZK_TRY(stage_products(h, J, 0, n, a_planes, k * J.lda_p, b_planes, n * J.ld, kind, out, ldo, ldo * n));
     OZK_CUDA(cudaStreamSynchronize(h->stream));
     return OZK_OK;
 }

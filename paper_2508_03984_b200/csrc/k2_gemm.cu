@@ -178,17 +178,23 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// Shared-memory matrix descriptor: K-major, 128B swizzle, 8-row core groups
-// 1024 B apart (SBO), Blackwell descriptor version 1.
-__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
-    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(1) << 16) |
+// Shared-memory matrix descriptors (128B swizzle, Blackwell version 1). Both
+// stage tiles are 128 rows of 128 B written by TMA, rows XOR-swizzled in
+// groups of 8 (1024 B apart = SBO):
+//  * B, K-major: a row is one n index with 128 k bytes; a k step of 32 moves
+//    the start address 32 B inside the swizzle atom;
+//  * A, MN-major: a row is one k index with 128 m bytes (one atom wide, so
+//    LBO — the next-atom stride along M — is never used); a k step of 32 moves
+//    32 rows = 4 atoms = 4096 B.
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_bytes) {
+    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16) |
            (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
            (static_cast<uint64_t>(2) << 61);
 }
-// Instruction descriptor: s8 x s8 -> s32, K-major A and B, no saturate.
+// Instruction descriptor: s8 x s8 -> s32, A MN-major (bit 15), B K-major, no saturate.
 template <int CG>
 __host__ __device__ constexpr uint32_t idesc_i8() {
-    return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(Cfg<CG>::kTileN >> 3) << 17) |
+    return (2u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (static_cast<uint32_t>(Cfg<CG>::kTileN >> 3) << 17) |
            (static_cast<uint32_t>(Cfg<CG>::kTileM >> 4) << 24);
 }
 
@@ -289,10 +295,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t dB = smem_u32(sB + stage * C::kStageB);
                     if constexpr (CG == 2) {
                         const uint32_t lb = full0_leader + 8u * stage;
-                        tma_load_3d_2sm(dA, &tmA, lb, kb * kBK, m0, mod);
+                        tma_load_3d_2sm(dA, &tmA, lb, m0, kb * kBK, mod);
                         tma_load_3d_2sm(dB, &tmB, lb, kb * kBK, n0, mod);
                     } else {
-                        tma_load_3d(dA, &tmA, fb, kb * kBK, m0, mod);
+                        tma_load_3d(dA, &tmA, fb, m0, kb * kBK, mod);
                         tma_load_3d(dB, &tmB, fb, kb * kBK, n0, mod);
                     }
                     if (++stage == C::kStages) {
@@ -323,8 +329,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t b0 = smem_u32(sB + stage * C::kStageB);
 #pragma unroll
                         for (int kk = 0; kk < kBK / 32; ++kk)
-                            mma_i8<CG>(d_tmem, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idesc,
-                                       (kb | kk) != 0);
+                            mma_i8<CG>(d_tmem, sdesc_sw128(a0 + kk * 32 * kBK, 16384), sdesc_sw128(b0 + kk * 32, 16),
+                                       idesc, (kb | kk) != 0);
                         mma_commit<CG>(smem_u32(empty + stage));
                     }
                     __syncwarp();
@@ -415,14 +421,16 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-// 3-D map over planes[n_mod][rows][ld] bytes, box {128 B of K, box_rows, 1}
-bool make_plane_map(CUtensorMap* map, const int8_t* base, int64_t k, int64_t rows, int64_t ld, int64_t plane_stride,
-                    int n_mod, int box_rows) {
+// 3-D map over n_mod column-major planes (inner extent `inner` bytes within a
+// column of `ld` bytes, `cols` columns, plane_stride bytes apart); box
+// {128 inner bytes, box_cols columns, 1}
+bool make_plane_map(CUtensorMap* map, const int8_t* base, int64_t inner, int64_t cols, int64_t ld, int64_t plane_stride,
+                    int n_mod, int box_cols) {
     auto enc = get_encode();
     if (!enc) return false;
-    cuuint64_t dims[3] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(n_mod)};
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(n_mod)};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(plane_stride)};
-    cuuint32_t box[3] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows), 1};
+    cuuint32_t box[3] = {128u, static_cast<cuuint32_t>(box_cols), 1};
     cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -434,7 +442,8 @@ template <int CG, int KIND>
 int launch_impl(const K2Launch& L, cudaStream_t s) {
     using C = Cfg<CG>;
     CUtensorMap ma, mb;
-    if (!make_plane_map(&ma, L.a_planes, L.k, L.m, L.ld, L.a_stride, L.n_mod, C::kBM) ||
+    // A: MN-major (m inner, k columns, box 128 m x 128 k); B: K-major (k inner, n columns)
+    if (!make_plane_map(&ma, L.a_planes, L.m, L.k, L.lda, L.a_stride, L.n_mod, kBK) ||
         !make_plane_map(&mb, L.b_planes, L.k, L.n, L.ld, L.b_stride, L.n_mod, C::kBRows)) {
         set_error("cuTensorMapEncodeTiled failed");
         return OZK_CUDA_ERROR;

@@ -31,8 +31,8 @@ struct DevConsts {
 
 DevConsts to_dev(const ozk_constants& c);
 
-// Inner-dimension row pitch of the K-major int8 planes: a multiple of 16 bytes
-// (TMA global strides must be 16-byte multiples).
+// Column pitch of the int8 planes: a multiple of 16 bytes (TMA global strides
+// must be 16-byte multiples). A planes use plane_ld(m), B planes plane_ld(k).
 inline int64_t plane_ld(int64_t k) { return (k + 15) / 16 * 16; }
 // Leading dimension of the uint8 U planes (16-byte aligned columns).
 inline int64_t u_ld(int64_t m) { return (m + 15) / 16 * 16; }
@@ -63,7 +63,7 @@ void launch_accurate_budget(const int32_t* base, const int32_t* cmax, int64_t li
 // Plane writers. kind 0: residues of trunc(x * 2^exp) (N planes);
 // kind 1: Abar/Bbar = ceil(|x| * 2^exp) (1 plane; exp INT32_MIN = zero line).
 void launch_a_planes(const void* a, int is_f32, int64_t m, int64_t k, int64_t lda, const int32_t* row_exp,
-                     const DevConsts& c, int kind, int8_t* planes, int64_t ld, cudaStream_t s);
+                     const DevConsts& c, int kind, int8_t* planes, int64_t ld, int64_t plane_stride, cudaStream_t s);
 void launch_b_planes(const void* b, int is_f32, int64_t k, int64_t n, int64_t ldb, const int32_t* col_exp,
                      const DevConsts& c, int kind, int8_t* planes, int64_t ld, int64_t plane_stride, cudaStream_t s);
 // FP64 -> FP32 rounding of an input (emulator.cpp:84-91), column-major with ld
@@ -72,9 +72,9 @@ void launch_round_to_f32(const double* x, int64_t rows, int64_t cols, int64_t ld
 // ---- K2 (k2_gemm.cu) -------------------------------------------------------
 enum K2Kind { K2_I32 = 0, K2_U8 = 1, K2_MAX = 2 };
 struct K2Launch {
-    const int8_t* a_planes;  // [n_mod] planes of m rows x ld bytes, plane stride a_stride
-    const int8_t* b_planes;  // [n_mod] planes of n rows x ld bytes, plane stride b_stride
-    int64_t m, n, k, ld;
+    const int8_t* a_planes;  // [n_mod] planes of k columns x lda bytes (MN-major), plane stride a_stride
+    const int8_t* b_planes;  // [n_mod] planes of n columns x ld bytes (K-major), plane stride b_stride
+    int64_t m, n, k, ld, lda;
     int64_t a_stride, b_stride;  // bytes between planes
     int64_t out_stride;          // elements between output planes (I32 / U8)
     int n_mod;

@@ -26,13 +26,13 @@ def _bits(x):
     return np.ascontiguousarray(x).view(np.int64 if x.dtype == np.float64 else np.int32)
 
 
-def _planes_kmajor(mats, ld):
-    """list of (rows x k) int8 matrices -> [N][rows][ld] K-major device buffer"""
+def _planes_colmajor(mats, ld):
+    """list of (rows x cols) int8 matrices -> [N][cols][ld] column-major device planes"""
     n_mod = len(mats)
-    rows, k = mats[0].shape
-    buf = np.zeros((n_mod, rows, ld), np.int8)
+    rows, cols = mats[0].shape
+    buf = np.zeros((n_mod, cols, ld), np.int8)
     for i, m in enumerate(mats):
-        buf[i, :, :k] = m
+        buf[i, :, :rows] = m.T
     return torch.from_numpy(buf).cuda()
 
 
@@ -47,9 +47,8 @@ def test_products_int32_and_u8(ctx, oracle, m, n, k):
     consts = oracle.constants(n_mod)
     A = [rng.integers(-128, 128, size=(m, k), dtype=np.int8) for _ in range(n_mod)]
     B = [rng.integers(-128, 128, size=(k, n), dtype=np.int8) for _ in range(n_mod)]
-    ld = ctx.plane_ld(k)
-    pa = _planes_kmajor(A, ld)
-    pb = _planes_kmajor([b.T for b in B], ld)
+    pa = _planes_colmajor(A, ctx.plane_ld(m))
+    pb = _planes_colmajor(B, ctx.plane_ld(k))
     out = torch.zeros((n_mod, n, m), dtype=torch.int32, device="cuda")
     ctx.stage_products(cfg, m, n, k, pa, pb, _lib.OZK_PRODUCTS_I32, out, m)
     u = torch.zeros((n_mod, n, m), dtype=torch.uint8, device="cuda")
@@ -68,9 +67,8 @@ def test_products_wraparound_k_2_17(ctx, oracle):
     """SPEC.md:239 / :493: k = 2^17 all -128 -> 2^31 wraps to INT32_MIN; mod 256 = 0."""
     m, n, k = 4, 4, 1 << 17
     cfg = EmuConfig(n_moduli=2)
-    ld = ctx.plane_ld(k)
-    pa = torch.full((2, m, ld), -128, dtype=torch.int8, device="cuda")
-    pb = torch.full((2, n, ld), -128, dtype=torch.int8, device="cuda")
+    pa = torch.full((2, k, ctx.plane_ld(m)), -128, dtype=torch.int8, device="cuda")
+    pb = torch.full((2, n, ctx.plane_ld(k)), -128, dtype=torch.int8, device="cuda")
     out = torch.zeros((2, n, m), dtype=torch.int32, device="cuda")
     ctx.stage_products(cfg, m, n, k, pa, pb, _lib.OZK_PRODUCTS_I32, out, m)
     assert (out == -(2 ** 31)).all()
@@ -111,14 +109,13 @@ def test_residue_planes(ctx, oracle, prec, N):
     b = gen_matrix(k, n, 2.0, 22, dt)
     cfg = EmuConfig(n_moduli=N, mode=ScaleMode.Accurate, precision=Precision(prec))
     mu, nu = oracle.scale(a, b, N, 1, prec)
-    ld = ctx.plane_ld(k)
-    pa = torch.zeros((N, m, ld), dtype=torch.int8, device="cuda")
-    pb = torch.zeros((N, n, ld), dtype=torch.int8, device="cuda")
+    pa = torch.zeros((N, k, ctx.plane_ld(m)), dtype=torch.int8, device="cuda")
+    pb = torch.zeros((N, n, ctx.plane_ld(k)), dtype=torch.int8, device="cuda")
     ctx.stage_residues(_dev_colmajor(a), _dev_colmajor(b), cfg, torch.from_numpy(mu).cuda(),
                        torch.from_numpy(nu).cuda(), pa, pb)
     wa = oracle.residues(oracle.truncate(a, mu, 0, prec), N, prec)  # (N, m, k)
     wb = oracle.residues(oracle.truncate(b, nu, 1, prec), N, prec)  # (N, k, n)
-    np.testing.assert_array_equal(pa.cpu().numpy()[:, :, :k], wa)
+    np.testing.assert_array_equal(pa.cpu().numpy()[:, :, :m].transpose(0, 2, 1), wa)
     np.testing.assert_array_equal(pb.cpu().numpy()[:, :, :k], wb.transpose(0, 2, 1))
 
 
@@ -216,14 +213,13 @@ def test_residue_planes_large_magnitudes(ctx, oracle, prec, N, lo, hi):
     mu = rng.integers(lo, hi, size=m).astype(np.int32)
     nu = rng.integers(lo, hi, size=n).astype(np.int32)
     cfg = EmuConfig(n_moduli=N, mode=ScaleMode.Fast, precision=Precision(prec))
-    ld = ctx.plane_ld(k)
-    pa = torch.zeros((N, m, ld), dtype=torch.int8, device="cuda")
-    pb = torch.zeros((N, n, ld), dtype=torch.int8, device="cuda")
+    pa = torch.zeros((N, k, ctx.plane_ld(m)), dtype=torch.int8, device="cuda")
+    pb = torch.zeros((N, n, ctx.plane_ld(k)), dtype=torch.int8, device="cuda")
     ctx.stage_residues(_dev_colmajor(a), _dev_colmajor(b), cfg, torch.from_numpy(mu).cuda(),
                        torch.from_numpy(nu).cuda(), pa, pb)
     wa = oracle.residues(oracle.truncate(a, mu, 0, prec), N, prec)
     wb = oracle.residues(oracle.truncate(b, nu, 1, prec), N, prec)
-    np.testing.assert_array_equal(pa.cpu().numpy()[:, :, :k], wa)
+    np.testing.assert_array_equal(pa.cpu().numpy()[:, :, :m].transpose(0, 2, 1), wa)
     np.testing.assert_array_equal(pb.cpu().numpy()[:, :, :k], wb.transpose(0, 2, 1))
 
 
