@@ -61,6 +61,10 @@ struct K2Params {
     int* colmax;
     int p[OZK_MAX_MODULI];
     int pinv[OZK_MAX_MODULI];
+    int group;             // tile rows per raster group
+    int hints;             // 1: L2 evict_last on operand loads, streaming U stores
+    int sync_slack;        // >0: a cluster starts tile lt only after every cluster finished lt - slack
+    unsigned int* done;    // completed (cluster, tile) count for sync_slack
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -114,6 +118,35 @@ __device__ __forceinline__ void tma_load_3d_2sm(uint32_t dst, const CUtensorMap*
         "%4, %5}], [%2];" ::"r"(dst),
         "l"(map), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_hint(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                                 int c2, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
+        "%4, %5}], [%2], %6;" ::"r"(dst),
+        "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_2sm_hint(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                     int c1, int c2, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
+        "l"(map), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_stream_u8(uint8_t* p, uint32_t v) {
+    asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
@@ -200,11 +233,10 @@ __host__ __device__ constexpr uint32_t idesc_i8() {
 
 // work item t -> (modulus, tile row, tile column), grouped raster of 8 tile
 // rows per modulus so the co-resident tiles share A/B panels in L2
-__device__ __forceinline__ void decode_tile(int t, int tiles_m, int tiles_n, int& mod, int& tm, int& tn) {
+__device__ __forceinline__ void decode_tile(int t, int tiles_m, int tiles_n, int G, int& mod, int& tm, int& tn) {
     const int per_mod = tiles_m * tiles_n;
     mod = t / per_mod;
     const int r = t - mod * per_mod;
-    constexpr int G = 8;
     const int group = r / (G * tiles_n);
     const int first = group * G;
     const int gsize = tiles_m - first < G ? tiles_m - first : G;
@@ -282,9 +314,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             const uint32_t full0_leader = CG == 2 ? mapa(smem_u32(full), 0) : smem_u32(full);
-            for (int t = cluster_id; t < total; t += nclusters) {
+            const uint64_t pol = policy_evict_last();
+            int lt = 0;
+            for (int t = cluster_id; t < total; t += nclusters, ++lt) {
+                if (P.sync_slack > 0 && leader && lt >= P.sync_slack) {
+                    // lockstep: every cluster must have finished its tile lt - slack
+                    const unsigned int need = static_cast<unsigned int>(
+                        min(total, (lt - P.sync_slack + 1) * nclusters));
+                    while (ld_acquire(P.done) < need) __nanosleep(256);
+                }
                 int mod, tm, tn;
-                decode_tile(t, P.tiles_m, P.tiles_n, mod, tm, tn);
+                decode_tile(t, P.tiles_m, P.tiles_n, P.group, mod, tm, tn);
                 const int m0 = tm * C::kTileM + static_cast<int>(rank) * C::kBM;
                 const int n0 = tn * C::kTileN + static_cast<int>(rank) * C::kBRows;
                 for (int kb = 0; kb < P.num_kb; ++kb) {
@@ -295,11 +335,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t dB = smem_u32(sB + stage * C::kStageB);
                     if constexpr (CG == 2) {
                         const uint32_t lb = full0_leader + 8u * stage;
-                        tma_load_3d_2sm(dA, &tmA, lb, m0, kb * kBK, mod);
-                        tma_load_3d_2sm(dB, &tmB, lb, kb * kBK, n0, mod);
+                        if (P.hints) {
+                            tma_load_3d_2sm_hint(dA, &tmA, lb, m0, kb * kBK, mod, pol);
+                            tma_load_3d_2sm_hint(dB, &tmB, lb, kb * kBK, n0, mod, pol);
+                        } else {
+                            tma_load_3d_2sm(dA, &tmA, lb, m0, kb * kBK, mod);
+                            tma_load_3d_2sm(dB, &tmB, lb, kb * kBK, n0, mod);
+                        }
                     } else {
-                        tma_load_3d(dA, &tmA, fb, m0, kb * kBK, mod);
-                        tma_load_3d(dB, &tmB, fb, kb * kBK, n0, mod);
+                        if (P.hints) {
+                            tma_load_3d_hint(dA, &tmA, fb, m0, kb * kBK, mod, pol);
+                            tma_load_3d_hint(dB, &tmB, fb, kb * kBK, n0, mod, pol);
+                        } else {
+                            tma_load_3d(dA, &tmA, fb, m0, kb * kBK, mod);
+                            tma_load_3d(dB, &tmB, fb, kb * kBK, n0, mod);
+                        }
                     }
                     if (++stage == C::kStages) {
                         stage = 0;
@@ -339,7 +389,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                         phase ^= 1;
                     }
                 }
-                if (lane == 0) mma_commit<CG>(smem_u32(tfull + acc));
+                if (lane == 0) {
+                    mma_commit<CG>(smem_u32(tfull + acc));
+                    if (P.sync_slack > 0) {
+                        // all MMAs of this tile are issued and its operands consumed in
+                        // order behind the ring, so the tile's loads are done
+                        __threadfence();
+                        atomicAdd(P.done, 1u);
+                    }
+                }
                 __syncwarp();
             }
         }
@@ -352,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int acc = lt & 1;
             const uint32_t acc_phase = (lt >> 1) & 1;
             int mod, tm, tn;
-            decode_tile(t, P.tiles_m, P.tiles_n, mod, tm, tn);
+            decode_tile(t, P.tiles_m, P.tiles_n, P.group, mod, tm, tn);
             mbar_wait(smem_u32(tfull + acc), acc_phase);
             tc_fence_after();
             const int row = tm * C::kTileM + static_cast<int>(rank) * C::kBM + q * 32 + lane;
@@ -366,11 +424,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint8_t* dst = static_cast<uint8_t*>(P.out) + static_cast<long long>(mod) * P.plane_out + row;
                     const int pm = P.p[mod], pinv = P.pinv[mod];
                     if (row_ok) {
+                        if (P.hints) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (col0 + j < P.n)
-                                dst[static_cast<long long>(col0 + j) * P.ldo] =
-                                    static_cast<uint8_t>(mod_u8(static_cast<int32_t>(v[j]), pm, pinv));
+                            for (int j = 0; j < 32; ++j)
+                                if (col0 + j < P.n)
+                                    st_stream_u8(dst + static_cast<long long>(col0 + j) * P.ldo,
+                                                 mod_u8(static_cast<int32_t>(v[j]), pm, pinv));
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (col0 + j < P.n)
+                                    dst[static_cast<long long>(col0 + j) * P.ldo] =
+                                        static_cast<uint8_t>(mod_u8(static_cast<int32_t>(v[j]), pm, pinv));
+                        }
                     }
                 } else if constexpr (KIND == K2_I32) {
                     int32_t* dst = static_cast<int32_t*>(P.out) + static_cast<long long>(mod) * P.plane_out + row;
@@ -409,6 +475,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------- host helpers
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -464,6 +535,19 @@ int launch_impl(const K2Launch& L, cudaStream_t s) {
     for (int i = 0; i < L.n_mod && L.c; ++i) {
         P.p[i] = L.c->p[i];
         P.pinv[i] = L.c->pinv_mulhi[i];
+    }
+    P.group = env_int("OZK_K2_GROUP", 8);
+    P.hints = env_int("OZK_K2_HINTS", 0);
+    P.sync_slack = env_int("OZK_K2_SYNC", 0);
+    P.done = nullptr;
+    if (P.sync_slack > 0) {
+        static unsigned int* counter = nullptr;
+        if (!counter && cudaMalloc(&counter, sizeof(unsigned int)) != cudaSuccess) {
+            set_error("residue_gemm: counter allocation failed");
+            return OZK_CUDA_ERROR;
+        }
+        cudaMemsetAsync(counter, 0, sizeof(unsigned int), s);
+        P.done = counter;
     }
     const long long total = static_cast<long long>(L.n_mod) * P.tiles_m * P.tiles_n;
     long long clusters = L.num_sms / CG;
