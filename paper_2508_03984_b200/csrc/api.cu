@@ -177,10 +177,14 @@ int validate(const ozk_config* cfg, const ozk_constants& c, int64_t m, int64_t n
         set_error("gemm_emulated: unknown scaling mode");
         return OZK_CONFIG_ERROR;
     }
-    if (k > OZK_ENGINE_MAX_K) {
-        // TODO(next round): chunked k > 2^17 (emulator.cpp:57-73); the per-modulus
-        // U_i do not depend on the blocking, so this is a K2 chunk loop.
-        set_error("k > 2^17 is not supported yet");
+    if (cfg->mode == OZK_ACCURATE && k > (int64_t(1) << 19)) {
+        // the bound product Abar*Bbar (entries <= 64*64*k) accumulates in one
+        // int32 TMEM tile; beyond 2^19 it would need an int64 C-bar
+        set_error("accurate mode supports k <= 2^19 (bound-product accumulator range)");
+        return OZK_INPUT_ERROR;
+    }
+    if (k > (int64_t(1) << 31) - 1) {
+        set_error("k exceeds 2^31");
         return OZK_INPUT_ERROR;
     }
     return OZK_OK;
@@ -197,7 +201,7 @@ struct Job {
     int64_t lda, ldb;
     int in_f32;
     int32_t *mu, *nu, *ma, *nb, *rowmax, *colmax, *flag_rows, *flag_cols;
-    int32_t* flags;  // [0] non-finite, [1] flagged rows, [2] flagged columns
+    int32_t* flags;  // [0] non-finite, [1] flagged rows, [2] flagged columns, [4] K2 lockstep counter
     double *amax, *asum, *bmax, *bsum;
     int splits;
     int8_t *pa, *pb;
@@ -338,6 +342,7 @@ int stage_cols(ozk_context* h, Job& J, int64_t j0, int64_t nj) {
     L.colmax = J.colmax + j0;
     L.c = &J.dc;
     L.num_sms = h->num_sms;
+    L.sync_counter = reinterpret_cast<unsigned int*>(J.flags + 4);
     OZK_TRY(launch_k2(L, h->stream));
     return check_launch(h, 1);
 }
@@ -381,6 +386,7 @@ int stage_products(ozk_context* h, Job& J, int64_t j0, int64_t nj, const int8_t*
     L.out_stride = out_stride;
     L.c = &J.dc;
     L.num_sms = h->num_sms;
+    L.sync_counter = reinterpret_cast<unsigned int*>(J.flags + 4);
     OZK_TRY(launch_k2(L, h->stream));
     return check_launch(h, 1);
 }
@@ -751,12 +757,14 @@ int ozk_stage_products(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n
         set_error("ozk_stage_products: bad dimensions");
         return OZK_INPUT_ERROR;
     }
-    if (k > OZK_ENGINE_MAX_K) {
+    if (k > OZK_ENGINE_MAX_K && kind == OZK_PRODUCTS_I32) {  // int8_engine.cpp:44 (U8 runs blocked)
         set_error("int8_gemm: k exceeds 2^17, use blocked_int8_gemm");
         return OZK_INPUT_ERROR;
     }
     OZK_CUDA(cudaSetDevice(h->device));
+    OZK_TRY(ensure(h->flags, 64));
     Job J{};
+    J.flags = static_cast<int32_t*>(h->flags.p);
     J.c = c;
     J.dc = to_dev(c);
     J.m = m;

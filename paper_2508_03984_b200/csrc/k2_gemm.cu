@@ -33,6 +33,7 @@ namespace ozk {
 namespace {
 
 constexpr int kBK = 128;  // bytes (= int8 elements) of K per stage: one 128B swizzle atom
+constexpr int64_t kChunkK = OZK_ENGINE_MAX_K;  // longest exact int32 accumulation
 constexpr int kAccCols = 256;
 constexpr int kThreads = 256;
 constexpr int kEpiWarp0 = 4;
@@ -420,22 +421,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t v[32];
                 tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kAccCols + cb * 32, v);
                 const int col0 = tn * C::kTileN + cb * 32;
-                if constexpr (KIND == K2_U8) {
+                if constexpr (KIND == K2_U8 || KIND == K2_U8ACC) {
                     uint8_t* dst = static_cast<uint8_t*>(P.out) + static_cast<long long>(mod) * P.plane_out + row;
                     const int pm = P.p[mod], pinv = P.pinv[mod];
                     if (row_ok) {
-                        if (P.hints) {
 #pragma unroll
-                            for (int j = 0; j < 32; ++j)
-                                if (col0 + j < P.n)
-                                    st_stream_u8(dst + static_cast<long long>(col0 + j) * P.ldo,
-                                                 mod_u8(static_cast<int32_t>(v[j]), pm, pinv));
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j)
-                                if (col0 + j < P.n)
-                                    dst[static_cast<long long>(col0 + j) * P.ldo] =
-                                        static_cast<uint8_t>(mod_u8(static_cast<int32_t>(v[j]), pm, pinv));
+                        for (int j = 0; j < 32; ++j) {
+                            if (col0 + j < P.n) {
+                                uint8_t* q = dst + static_cast<long long>(col0 + j) * P.ldo;
+                                uint32_t u = mod_u8(static_cast<int32_t>(v[j]), pm, pinv);
+                                if constexpr (KIND == K2_U8ACC) {
+                                    // later k chunk (emulator.cpp:57-73): sum of per-block
+                                    // residues, reduced again; u + old < 2p
+                                    u += *q;
+                                    u = u >= static_cast<uint32_t>(pm) ? u - pm : u;
+                                }
+                                if (P.hints)
+                                    st_stream_u8(q, u);
+                                else
+                                    *q = static_cast<uint8_t>(u);
+                            }
                         }
                     }
                 } else if constexpr (KIND == K2_I32) {
@@ -538,17 +543,14 @@ int launch_impl(const K2Launch& L, cudaStream_t s) {
     }
     P.group = env_int("OZK_K2_GROUP", 8);
     P.hints = env_int("OZK_K2_HINTS", 0);
-    P.sync_slack = env_int("OZK_K2_SYNC", 0);
-    P.done = nullptr;
-    if (P.sync_slack > 0) {
-        static unsigned int* counter = nullptr;
-        if (!counter && cudaMalloc(&counter, sizeof(unsigned int)) != cudaSuccess) {
-            set_error("residue_gemm: counter allocation failed");
-            return OZK_CUDA_ERROR;
-        }
-        cudaMemsetAsync(counter, 0, sizeof(unsigned int), s);
-        P.done = counter;
-    }
+    // Lockstep (default on): co-resident clusters that share A/B panels stay
+    // within one tile of each other, so the panels they all stream are still in
+    // L2 when the trailing cluster reads them. Measured at 16384^3, N=14: DRAM
+    // reads 214 GB -> 57 GB per launch, and the power freed lifts the capped SM
+    // clock 1.15 -> 1.48 GHz (profiles/). The counter is per handle.
+    P.sync_slack = L.sync_counter ? env_int("OZK_K2_SYNC", 1) : 0;
+    P.done = L.sync_counter;
+    if (P.sync_slack > 0) cudaMemsetAsync(P.done, 0, sizeof(unsigned int), s);
     const long long total = static_cast<long long>(L.n_mod) * P.tiles_m * P.tiles_n;
     long long clusters = L.num_sms / CG;
     if (clusters > total) clusters = total;
@@ -587,6 +589,8 @@ int launch_kind(const K2Launch& L, cudaStream_t s) {
             return launch_impl<CG, K2_I32>(L, s);
         case K2_U8:
             return launch_impl<CG, K2_U8>(L, s);
+        case K2_U8ACC:
+            return launch_impl<CG, K2_U8ACC>(L, s);
         default:
             return launch_impl<CG, K2_MAX>(L, s);
     }
@@ -608,7 +612,23 @@ int launch_k2(const K2Launch& L, cudaStream_t s) {
         set_error("residue_gemm: dimension exceeds 2^31");
         return OZK_INPUT_ERROR;
     }
-    return k2_cta_group() == 1 ? launch_kind<1>(L, s) : launch_kind<2>(L, s);
+    auto one = [&](const K2Launch& X) { return k2_cta_group() == 1 ? launch_kind<1>(X, s) : launch_kind<2>(X, s); };
+    // One int32 accumulation stays exact for k <= 2^17 (only the benign
+    // k = 2^17 wrap, int8_engine.hpp:19-22); U8 products over a longer k run in
+    // chunks of 2^17, each chunk's residues added into U and reduced again —
+    // the reference's blocked path (emulator.cpp:57-73), whose value does not
+    // depend on where the blocks fall.
+    if (L.kind != K2_U8 || L.k <= kChunkK) return one(L);
+    for (int64_t k0 = 0; k0 < L.k; k0 += kChunkK) {
+        K2Launch X = L;
+        X.k = L.k - k0 < kChunkK ? L.k - k0 : kChunkK;
+        X.a_planes = L.a_planes + k0 * L.lda;  // MN-major: k columns
+        X.b_planes = L.b_planes + k0;          // K-major: offset inside each column
+        X.kind = k0 == 0 ? K2_U8 : K2_U8ACC;
+        const int st = one(X);
+        if (st != OZK_OK) return st;
+    }
+    return OZK_OK;
 }
 
 }  // namespace ozk

@@ -70,7 +70,7 @@ void launch_b_planes(const void* b, int is_f32, int64_t k, int64_t n, int64_t ld
 void launch_round_to_f32(const double* x, int64_t rows, int64_t cols, int64_t ld, float* out, cudaStream_t s);
 
 // ---- K2 (k2_gemm.cu) -------------------------------------------------------
-enum K2Kind { K2_I32 = 0, K2_U8 = 1, K2_MAX = 2 };
+enum K2Kind { K2_I32 = 0, K2_U8 = 1, K2_MAX = 2, K2_U8ACC = 3 };
 struct K2Launch {
     const int8_t* a_planes;  // [n_mod] planes of k columns x lda bytes (MN-major), plane stride a_stride
     const int8_t* b_planes;  // [n_mod] planes of n columns x ld bytes (K-major), plane stride b_stride
@@ -85,6 +85,7 @@ struct K2Launch {
     int32_t* colmax;
     const DevConsts* c;
     int num_sms;
+    unsigned int* sync_counter;  // per-handle device word for the inter-cluster lockstep (nullptr: off)
 };
 int launch_k2(const K2Launch& L, cudaStream_t s);
 

@@ -294,3 +294,26 @@ def test_host_pipeline_alpha_beta_multiblock(ctx, oracle):
     out = np.asfortranarray(c0.copy())
     ctx.gemm_host(a, b, EmuConfig(n_moduli=12), alpha=-1.5, beta=0.25, c=out)
     np.testing.assert_array_equal(_bits(out), _bits(-1.5 * base + 0.25 * c0))
+
+
+@pytest.mark.parametrize("k,mode", [((1 << 17) + 1000, ScaleMode.Fast), (300000, ScaleMode.Fast),
+                                    (200000, ScaleMode.Accurate), (1 << 17, ScaleMode.Accurate)])
+def test_long_k_blocked_path(oracle, k, mode):
+    """k > 2^17: the reference blocks the inner dimension (emulator.cpp:57-73);
+    the GPU chunks K2 by 2^17 and re-reduces the residues. Bit-exact either way."""
+    m, n = 9, 7
+    a = gen_matrix(m, k, 0.5, 61)
+    b = gen_matrix(k, n, 0.5, 62)
+    for bk in (1 << 17, 50000):
+        got = gemm_emulated(a, b, EmuConfig(n_moduli=14, mode=mode, block_k=bk)).c
+        want = oracle.gemm(a, b, 14, int(mode), block_k=bk)
+        np.testing.assert_array_equal(_bits(got), _bits(want))
+
+
+def test_accurate_k_limit():
+    from paper_2508_03984_b200 import InputError
+
+    a = np.zeros((2, (1 << 19) + 1), order="F")
+    b = np.zeros(((1 << 19) + 1, 2), order="F")
+    with pytest.raises(InputError):
+        gemm_emulated(a, b, EmuConfig(n_moduli=8, mode=ScaleMode.Accurate))
