@@ -119,6 +119,23 @@ int ozk_dgemm(ozk_handle h, int n_moduli, int mode, int64_t m, int64_t n, int64_
 int ozk_sgemm(ozk_handle h, int n_moduli, int mode, int64_t m, int64_t n, int64_t k, float alpha, const float* A,
               int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc);
 
+/* ---- column-sharded GEMM (multi-GPU) --------------------------
+ * This process computes C[:, shard] = alpha * A * B[:, shard] + beta * C[:, shard]
+ * with the full A (the same on every process). nu is column-local in both
+ * modes and fast-mode mu depends on A only; accurate-mode mu depends on the
+ * row maxima of the bound product Abar*Bbar over ALL columns
+ * (scaling.cpp:143-163). So:
+ *   ozk_shard_begin   K1a for A's rows and this shard's columns;
+ *   ozk_shard_rowmax  accurate mode: device pointer to the m int32 partial row
+ *                     maxima, which the caller MAX-all-reduces across the
+ *                     shards (NCCL) on the handle's stream before _end;
+ *   ozk_shard_end     the budget, K1b, K2 and K3 for the shard.
+ * The concatenated shards are bit-identical to the single-process result. */
+int ozk_shard_begin(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, const void* A,
+                    int64_t lda, const void* B, int64_t ldb);
+int32_t* ozk_shard_rowmax(ozk_handle h);
+int ozk_shard_end(ozk_handle h, double alpha, double beta, void* C, int64_t ldc);
+
 /* ---- stage-level exports (device pointers; parity / debug) -------------- */
 /* K1a: scale exponents mu_i = 2^mu_exp[i], nu_j = 2^nu_exp[j]
  *      (scale_fast / scale_accurate, scaling.hpp:28-36). */

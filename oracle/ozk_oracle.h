@@ -77,6 +77,11 @@ int ozo_gemm_f32(const float* a, const float* b, int64_t m, int64_t n, int64_t k
 int ozo_gemm_f64_consts(const double* a, const double* b, int64_t m, int64_t n, int64_t k, const ozo_constants* c,
                         int mode, int64_t block_k, double* out);
 
+/* pipeline with caller-given exponents (sharding checks) and the accurate budget */
+int ozo_gemm_f64_scaled(const double* a, const double* b, int64_t m, int64_t n, int64_t k, const ozo_constants* c,
+                        const int32_t* mu, const int32_t* nu, int64_t block_k, double* out);
+int ozo_accurate_exponent(int64_t cmax, int base, const ozo_constants* c);
+
 /* debug: the uint8 residue products U_i of the pipeline (N consecutive m x n slices) */
 int ozo_products_u8_f64(const double* a, const double* b, int64_t m, int64_t n, int64_t k, int n_moduli, int mode,
                         int64_t block_k, uint8_t* u);

@@ -28,6 +28,7 @@ EXPORTED_SYMBOLS = (
     "ozk_gemm", "ozk_gemm_host", "ozk_dgemm", "ozk_sgemm",
     "ozk_stage_scale", "ozk_plane_ld", "ozk_stage_residues", "ozk_stage_products", "ozk_stage_reconstruct",
     "ozk_kernel_launches", "ozk_profile", "ozk_profile_read",
+    "ozk_shard_begin", "ozk_shard_rowmax", "ozk_shard_end",
 )
 PROFILE_SLOTS = ("scale", "residues", "products", "reconstruct", "total")
 
@@ -119,6 +120,10 @@ def load() -> C.CDLL:
     L.ozk_kernel_launches.restype = i64
     L.ozk_kernel_launches.argtypes = [p]
     L.ozk_profile.argtypes = [p, i32]
+    L.ozk_shard_begin.argtypes = [p, C.POINTER(OzkConfig), i64, i64, i64, p, i64, p, i64]
+    L.ozk_shard_rowmax.restype = p
+    L.ozk_shard_rowmax.argtypes = [p]
+    L.ozk_shard_end.argtypes = [p, C.c_double, C.c_double, p, i64]
     L.ozk_profile_read.argtypes = [p, p, p, i32]
     _lib = L
     return L

@@ -67,6 +67,26 @@ DevConsts to_dev(const ozk_constants& c) {
 
 using namespace ozk;
 
+namespace {
+// One emulated GEMM: constants, operand views and the carved workspace.
+struct Job {
+    ozk_constants c;
+    DevConsts dc;
+    int mode;
+    int64_t m, n, k, ld, lda_p, ldu;  // ld: B plane pitch (k), lda_p: A plane pitch (m)
+    const void* a;  // device operands as the kernels read them
+    const void* b;
+    int64_t lda, ldb;
+    int in_f32;
+    int32_t *mu, *nu, *ma, *nb, *rowmax, *colmax, *flag_rows, *flag_cols;
+    int32_t* flags;  // [0] non-finite, [1] flagged rows, [2] flagged columns, [4] K2 lockstep counter
+    double *amax, *asum, *bmax, *bsum;
+    int splits;
+    int8_t *pa, *pb;
+    uint8_t* u;
+};
+}  // namespace
+
 struct ozk_context {
     int device = 0;
     int num_sms = 148;
@@ -80,6 +100,10 @@ struct ozk_context {
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     double stage_ms[OZK_PROFILE_SLOTS] = {};
     int64_t stage_calls[OZK_PROFILE_SLOTS] = {};
+    // the column shard between ozk_shard_begin and ozk_shard_end
+    bool shard_open = false;
+    ozk_config shard_cfg{};
+    Job shard{};  // plain pointers into this handle's workspace
 };
 
 namespace {
@@ -190,23 +214,6 @@ int validate(const ozk_config* cfg, const ozk_constants& c, int64_t m, int64_t n
     return OZK_OK;
 }
 
-// One emulated GEMM: constants, operand views and the carved workspace.
-struct Job {
-    ozk_constants c;
-    DevConsts dc;
-    int mode;
-    int64_t m, n, k, ld, lda_p, ldu;  // ld: B plane pitch (k), lda_p: A plane pitch (m)
-    const void* a;  // device operands as the kernels read them
-    const void* b;
-    int64_t lda, ldb;
-    int in_f32;
-    int32_t *mu, *nu, *ma, *nb, *rowmax, *colmax, *flag_rows, *flag_cols;
-    int32_t* flags;  // [0] non-finite, [1] flagged rows, [2] flagged columns, [4] K2 lockstep counter
-    double *amax, *asum, *bmax, *bsum;
-    int splits;
-    int8_t *pa, *pb;
-    uint8_t* u;
-};
 
 int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c, int64_t m, int64_t n, int64_t k,
           const void* A, int64_t lda, const void* B, int64_t ldb, bool need_products) {
@@ -711,6 +718,59 @@ int ozk_sgemm(ozk_handle h, int n_moduli, int mode, int64_t m, int64_t n, int64_
     ozk_config cfg = ozk_default_config(n_moduli, mode, OZK_FP32);
     cfg.c_type = OZK_R32F;
     return ozk_gemm(h, &cfg, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+}
+
+int ozk_shard_begin(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, const void* A,
+                    int64_t lda, const void* B, int64_t ldb) {
+    if (!h) return OZK_INPUT_ERROR;
+    ozk_constants c;
+    OZK_TRY(resolve(cfg, c));
+    OZK_TRY(validate(cfg, c, m, n, k, lda, ldb));
+    OZK_CUDA(cudaSetDevice(h->device));
+    Job& J = h->shard;
+    J = Job{};
+    OZK_TRY(setup(h, J, cfg, c, m, n, k, A, lda, B, ldb, true));
+    h->shard_cfg = *cfg;
+    h->shard_cfg.constants = nullptr;  // resolved into J.c
+    {
+        StageTimer t(h, OZK_PROFILE_SCALE);
+        const void* b_src = J.b;
+        OZK_TRY(round_a(h, J, cfg));
+        OZK_TRY(round_b(h, J, cfg, b_src, ldb, 0, n));
+        OZK_TRY(stage_rows(h, J));
+        OZK_TRY(stage_cols(h, J, 0, n));  // accurate: partial row maxima over this shard's columns
+    }
+    h->shard_open = true;
+    return OZK_OK;
+}
+
+int32_t* ozk_shard_rowmax(ozk_handle h) {
+    if (!h || !h->shard_open) return nullptr;
+    return h->shard.rowmax;
+}
+
+int ozk_shard_end(ozk_handle h, double alpha, double beta, void* C, int64_t ldc) {
+    if (!h || !h->shard_open) {
+        set_error("ozk_shard_end without ozk_shard_begin");
+        return OZK_INPUT_ERROR;
+    }
+    h->shard_open = false;
+    Job& J = h->shard;
+    if (ldc < J.m) {
+        set_error("gemm_emulated: ldc < m");
+        return OZK_INPUT_ERROR;
+    }
+    OZK_CUDA(cudaSetDevice(h->device));
+    if (J.mode == OZK_ACCURATE) {
+        StageTimer t(h, OZK_PROFILE_SCALE);
+        OZK_TRY(stage_budget(h, J));
+    }
+    {
+        StageTimer t(h, OZK_PROFILE_RESIDUES);
+        OZK_TRY(stage_row_residues(h, J, J.mu, J.pa));
+    }
+    OZK_TRY(compute_block(h, J, 0, J.n, alpha, beta, C, ldc, h->shard_cfg.c_type == OZK_R32F));
+    return finish_check(h, J, h->stream);
 }
 
 int ozk_stage_scale(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,

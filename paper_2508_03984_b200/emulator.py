@@ -165,6 +165,35 @@ class Context:
         _lib.check(self._lib.ozk_gemm(self.handle, C.byref(conf), m, n, k, float(alpha), A.data_ptr(), lda,
                                       B.data_ptr(), ldb, float(beta), C_out.data_ptr(), ldc))
 
+    # ---- column shard (multi-GPU, see distributed.py) -------------------------------
+    def shard_begin(self, A, B, cfg: EmuConfig) -> None:
+        m, k = A.shape
+        n = B.shape[1]
+        self._shard_m = m
+        self._shard_conf = _config(cfg, _dtype_code(A), _lib.OZK_R64F)
+        _lib.check(self._lib.ozk_shard_begin(self.handle, C.byref(self._shard_conf), m, n, k, A.data_ptr(),
+                                             _colmajor_ld(A), B.data_ptr(), _colmajor_ld(B)))
+
+    def shard_rowmax(self):
+        """the m int32 partial row maxima on the device, as a torch tensor (no copy)"""
+        import torch
+
+        ptr = self._lib.ozk_shard_rowmax(self.handle)
+        if not ptr:
+            raise InputError("no open shard")
+
+        class _Dev:
+            __cuda_array_interface__ = {"shape": (self._shard_m,), "typestr": "<i4", "data": (ptr, False),
+                                        "version": 3}
+
+        return torch.as_tensor(_Dev(), device=f"cuda:{self.device}")
+
+    def shard_end(self, C_out, alpha: float = 1.0, beta: float = 0.0) -> None:
+        if C_out.dtype.itemsize == 4:
+            raise InputError("shard output must be FP64 (set c_type through Context.gemm for FP32)")
+        _lib.check(self._lib.ozk_shard_end(self.handle, float(alpha), float(beta), C_out.data_ptr(),
+                                           _colmajor_ld(C_out)))
+
     # ---- stage exports (device tensors) --------------------------------------------
     def stage_scale(self, A, B, cfg: EmuConfig, mu_exp, nu_exp) -> None:
         m, k = A.shape

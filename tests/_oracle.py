@@ -111,6 +111,8 @@ class Oracle:
         for nm in ("ozo_gemm_f64", "ozo_gemm_f32", "ozo_products_u8_f64"):
             getattr(L, nm).argtypes = [_p, _p, _i64, _i64, _i64, C.c_int, C.c_int, _i64, _p]
         L.ozo_gemm_f64_consts.argtypes = [_p, _p, _i64, _i64, _i64, C.POINTER(Constants), C.c_int, _i64, _p]
+        L.ozo_gemm_f64_scaled.argtypes = [_p, _p, _i64, _i64, _i64, C.POINTER(Constants), _p, _p, _i64, _p]
+        L.ozo_accurate_exponent.argtypes = [C.c_int64, C.c_int, C.POINTER(Constants)]
 
     # -- constants -----------------------------------------------------------------
     def constants(self, n: int, prec: int = 0) -> Constants:
@@ -224,6 +226,20 @@ class Oracle:
         if st:
             raise ValueError(f"status {st}")
         return c
+
+    def gemm_scaled(self, a, b, n_moduli, mu_exp, nu_exp, block_k=1 << 17):
+        a, b = _f(a, np.float64), _f(b, np.float64)
+        m, k = a.shape
+        n = b.shape[1]
+        cs = self.constants(n_moduli)
+        mu = np.ascontiguousarray(mu_exp, np.int32)
+        nu = np.ascontiguousarray(nu_exp, np.int32)
+        c = np.zeros((m, n), np.float64, order="F")
+        self.lib.ozo_gemm_f64_scaled(_ptr(a), _ptr(b), m, n, k, C.byref(cs), _ptr(mu), _ptr(nu), block_k, _ptr(c))
+        return c
+
+    def accurate_exponent(self, cmax: int, base: int, n_moduli: int) -> int:
+        return self.lib.ozo_accurate_exponent(int(cmax), int(base), C.byref(self.constants(n_moduli)))
 
     def products_u8(self, a, b, n_moduli, mode, block_k=1 << 17):
         a, b = _f(a, np.float64), _f(b, np.float64)
