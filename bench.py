@@ -247,6 +247,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2508_03984_b200 import Context, EmuConfig, Precision, ScaleMode
+    from paper_2508_03984_b200.distributed import gemm_sharded
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -267,12 +268,11 @@ def main():
     A = gen_device(m, k, args.phi, 1, torch.float64, dev)
     B = gen_device(k, n, args.phi, 2 + rank, torch.float64, dev)  # this rank's column block
     C = torch.empty((n, m), dtype=torch.float64, device=dev).t()
-    A_root = A.t().contiguous() if world > 1 else None  # rank 0's A, broadcast each step
 
     def step():
         if world > 1:
-            dist.broadcast(A_root, src=0)
-            ctx.gemm(A_root.t(), B, cfg, C)
+            # column shard: A broadcast from rank 0 + (accurate) row-bound all-reduce
+            gemm_sharded(ctx, A, B, cfg, C)
         else:
             ctx.gemm(A, B, cfg, C)
 

@@ -91,20 +91,35 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
     for (int u = 0; u < kBPerThread; ++u)
         xlo[u] = static_cast<uint32_t>(__double2loint(__dadd_rn(static_cast<double>(x[u]), kMagic52)));
+    // the fast/literal choice is warp-uniform: branch once, outside the modulus loop
+    if (fast) {
 #pragma unroll 1
-    for (int t = 0; t < c.n; ++t) {
-        const uint32_t pt = s_p[t];
-        const double pinvt = s_pinv[t];
-        uint32_t v[kBPerThread];
+        for (int t = 0; t < c.n; ++t) {
+            const uint32_t pt = s_p[t];
+            const double pinvt = s_pinv[t];
+            uint2 word;
+            if (pt == 256) {  // p = 256: the residue is the low byte of x
+                word = make_uint2(pack_low_bytes(xlo[0], xlo[1], xlo[2], xlo[3]),
+                                  pack_low_bytes(xlo[4], xlo[5], xlo[6], xlo[7]));
+            } else {
+                const uint32_t neg_p = 0u - pt;
+                uint32_t v[kBPerThread];
 #pragma unroll
-        for (int u = 0; u < kBPerThread; ++u) {
-            if (fast && pt == 256)
-                v[u] = xlo[u];
-            else
-                v[u] = fast ? symmetric_residue(static_cast<double>(x[u]), xlo[u], pt, pinvt) : literal_byte(x[u], c, t);
+                for (int u = 0; u < kBPerThread; ++u)
+                    v[u] = symmetric_residue(static_cast<double>(x[u]), xlo[u], neg_p, pinvt);
+                word = make_uint2(pack_low_bytes(v[0], v[1], v[2], v[3]), pack_low_bytes(v[4], v[5], v[6], v[7]));
+            }
+            *reinterpret_cast<uint2*>(dst0 + t * plane_stride) = word;
         }
-        *reinterpret_cast<uint2*>(dst0 + t * plane_stride) =
-            make_uint2(pack_low_bytes(v[0], v[1], v[2], v[3]), pack_low_bytes(v[4], v[5], v[6], v[7]));
+    } else {
+#pragma unroll 1
+        for (int t = 0; t < c.n; ++t) {
+            uint32_t v[kBPerThread];
+#pragma unroll
+            for (int u = 0; u < kBPerThread; ++u) v[u] = literal_byte(x[u], c, t);
+            *reinterpret_cast<uint2*>(dst0 + t * plane_stride) =
+                make_uint2(pack_low_bytes(v[0], v[1], v[2], v[3]), pack_low_bytes(v[4], v[5], v[6], v[7]));
+        }
     }
 }
 

@@ -16,7 +16,19 @@
 namespace ozk {
 namespace {
 
-template <bool kF32Out, bool kPlain>
+// ldexp(x, e) as one multiply by 2^e when that is exact-and-correctly-rounded
+// (2^e normal, result normal); CUDA's general ldexp otherwise (subnormal or
+// overflowing results, huge |e|)
+__device__ __forceinline__ double scale_pow2(double x, int e) {
+    if (e >= -1022 && e <= 1023) {
+        const double r = __dmul_rn(x, pow2d(e));
+        if (fabs(r) >= 0x1.0p-1022 && fabs(r) <= 0x1.fffffffffffffp+1023) return r;
+        if (r == 0.0 && x == 0.0) return r;
+    }
+    return ldexp(x, e);
+}
+
+template <bool kF32Out, bool kPlain, bool kFp64Tables>
 __global__ void __launch_bounds__(128)
     reconstruct_kernel(const uint8_t* __restrict__ u, int64_t ldu, int64_t plane_stride, int64_t m, int64_t n,
                        const int32_t* __restrict__ mu_exp, const int32_t* __restrict__ nu_exp, const DevConsts c,
@@ -26,7 +38,6 @@ __global__ void __launch_bounds__(128)
     if (i0 >= m) return;
     double c1[4] = {0.0, 0.0, 0.0, 0.0}, c2[4] = {0.0, 0.0, 0.0, 0.0};
     const uint8_t* src = u + j * ldu + i0;
-    const bool fp64_tables = c.precision == OZK_FP64;
     const int n_mod = c.n;
     // all plane loads first (predicated, compile-time indices: registers), so
     // a thread has its N loads in flight at once instead of one per FP chain step
@@ -46,7 +57,7 @@ __global__ void __launch_bounds__(128)
                 // construction), so the fused form equals the reference's
                 // mul-then-add bit for bit. FP32 tables carry the full-width s1
                 // (crt_tables.cpp:160-163): keep the two roundings there.
-                c1[q] = fp64_tables ? __fma_rn(s1, v, c1[q]) : __dadd_rn(c1[q], __dmul_rn(s1, v));
+                c1[q] = kFp64Tables ? __fma_rn(s1, v, c1[q]) : __dadd_rn(c1[q], __dmul_rn(s1, v));
                 c2[q] = __dadd_rn(c2[q], __dmul_rn(s2, v));
             }
         }
@@ -58,7 +69,7 @@ __global__ void __launch_bounds__(128)
         if (i >= m) break;
         const double qv = rint(__dmul_rn(c.P_inv, c1[q]));
         const double cpp = __fma_rn(-c.P2, qv, __dadd_rn(__fma_rn(-c.P1, qv, c1[q]), c2[q]));
-        double r = ldexp(cpp, -(mu_exp[i] + ne));
+        double r = scale_pow2(cpp, -(mu_exp[i] + ne));
         if (!kPlain) {
             const double old = beta != 0.0 ? (kF32Out ? static_cast<double>(static_cast<float*>(C)[i + j * ldc])
                                                       : static_cast<double*>(C)[i + j * ldc])
@@ -72,6 +83,18 @@ __global__ void __launch_bounds__(128)
     }
 }
 
+template <bool kF32Out, bool kPlain>
+void launch_variant(dim3 grid, cudaStream_t s, const uint8_t* u, int64_t ldu, int64_t stride, int64_t m, int64_t n,
+                    const int32_t* mu_exp, const int32_t* nu_exp, const DevConsts& c, double alpha, double beta,
+                    void* C, int64_t ldc) {
+    if (c.precision == OZK_FP64)
+        reconstruct_kernel<kF32Out, kPlain, true>
+            <<<grid, 128, 0, s>>>(u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, C, ldc);
+    else
+        reconstruct_kernel<kF32Out, kPlain, false>
+            <<<grid, 128, 0, s>>>(u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, C, ldc);
+}
+
 }  // namespace
 
 void launch_reconstruct(const uint8_t* u, int64_t ldu, int64_t stride, int64_t m, int64_t n, const int32_t* mu_exp,
@@ -81,18 +104,14 @@ void launch_reconstruct(const uint8_t* u, int64_t ldu, int64_t stride, int64_t m
     const bool plain = alpha == 1.0 && beta == 0.0;
     if (c_is_f32) {
         if (plain)
-            reconstruct_kernel<true, true><<<grid, 128, 0, s>>>(u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta,
-                                                                C, ldc);
+            launch_variant<true, true>(grid, s, u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, C, ldc);
         else
-            reconstruct_kernel<true, false><<<grid, 128, 0, s>>>(u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha,
-                                                                 beta, C, ldc);
+            launch_variant<true, false>(grid, s, u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, C, ldc);
     } else {
         if (plain)
-            reconstruct_kernel<false, true><<<grid, 128, 0, s>>>(u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha,
-                                                                 beta, C, ldc);
+            launch_variant<false, true>(grid, s, u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, C, ldc);
         else
-            reconstruct_kernel<false, false><<<grid, 128, 0, s>>>(u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha,
-                                                                  beta, C, ldc);
+            launch_variant<false, false>(grid, s, u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, C, ldc);
     }
 }
 

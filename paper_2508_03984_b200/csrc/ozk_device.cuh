@@ -62,11 +62,11 @@ __device__ __forceinline__ bool symmetric_residue_domain(double x, int prec, int
     if (prec == OZK_FP64) return ax <= 0x1.0p50;
     return ax <= 0x1.0p21 || (n >= 5 && ax <= 0x1.0p43);
 }
-// x integer-valued, |x| <= 2^50; xlo = lo32(x + kMagic52). Returns r mod 2^32
-// (the int8 plane byte is its low byte).
-__device__ __forceinline__ uint32_t symmetric_residue(double x, uint32_t xlo, uint32_t p, double pinv64) {
+// x integer-valued, |x| <= 2^50; xlo = lo32(x + kMagic52); neg_p = -p mod 2^32.
+// Returns r mod 2^32 (the int8 plane byte is its low byte): one DFMA + one IMAD.
+__device__ __forceinline__ uint32_t symmetric_residue(double x, uint32_t xlo, uint32_t neg_p, double pinv64) {
     const uint32_t qlo = static_cast<uint32_t>(__double2loint(__fma_rn(x, pinv64, kMagic52)));
-    return xlo - qlo * p;
+    return xlo + qlo * neg_p;
 }
 // four residue words -> one packed word of their low bytes (3 PRMT)
 __device__ __forceinline__ uint32_t pack_low_bytes(uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
