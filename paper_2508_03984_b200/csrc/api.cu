@@ -60,6 +60,31 @@ DevConsts to_dev(const ozk_constants& c) {
     d.P_inv = c.P_inv;
     d.pp_fast = c.pp_fast;
     d.pp_accu = c.pp_accu;
+    // integer C1: common binary grid of the s1_i and a proof that every sum fits
+    int shift = 2000;
+    for (int i = 0; i < c.n_moduli; ++i) {
+        if (c.s1[i] == 0.0) continue;
+        int e = 0;
+        const double fr = std::frexp(c.s1[i], &e);  // s1 = fr * 2^e, fr in [0.5, 1)
+        long long mant = static_cast<long long>(std::ldexp(fr, 53));
+        int low = e - 53;
+        while (mant && !(mant & 1)) {
+            mant >>= 1;
+            ++low;
+        }
+        shift = low < shift ? low : shift;
+    }
+    bool ok = c.precision == OZK_FP64 && shift < 2000;
+    long double bound = 0;
+    for (int i = 0; i < c.n_moduli && ok; ++i) {
+        const long double hi = std::ldexp(static_cast<long double>(c.s1[i]), -shift);
+        ok = hi >= 0 && hi < 0x1p62L;
+        d.h1[i] = ok ? static_cast<unsigned long long>(hi) : 0ull;
+        bound += hi * (c.moduli[i] - 1);
+    }
+    d.c1_int = ok && bound < 0x1p53L;
+    d.c1_shift = ok ? shift : 0;
+    for (int i = 0; i < c.n_moduli; ++i) d.s2_m52[i] = -c.s2[i] * 0x1p52;
     return d;
 }
 

@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(128)
     const int64_t i0 = (static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x) * 4;
     if (i0 >= m) return;
     double c1[4] = {0.0, 0.0, 0.0, 0.0}, c2[4] = {0.0, 0.0, 0.0, 0.0};
+    unsigned long long c1i[4] = {0ull, 0ull, 0ull, 0ull};
     const uint8_t* src = u + j * ldu + i0;
     const int n_mod = c.n;
     // all plane loads first (predicated, compile-time indices: registers), so
@@ -48,19 +49,27 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
     for (int t = 0; t < OZK_MAX_MODULI; ++t) {  // compile-time bound: constants become immediates
         if (t < n_mod) {
-            const double s1 = c.s1[t], s2 = c.s2[t];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                // u -> double without a conversion instruction: 2^52 + u, minus 2^52
-                const double v = __dsub_rn(__hiloint2double(0x43300000, (w[t] >> (8 * q)) & 0xffu), 0x1.0p52);
-                // FP64 tables: s1*u is exact and so is the running sum (beta_i
-                // construction), so the fused form equals the reference's
-                // mul-then-add bit for bit. FP32 tables carry the full-width s1
-                // (crt_tables.cpp:160-163): keep the two roundings there.
-                c1[q] = kFp64Tables ? __fma_rn(s1, v, c1[q]) : __dadd_rn(c1[q], __dmul_rn(s1, v));
-                c2[q] = __dadd_rn(c2[q], __dmul_rn(s2, v));
+                const uint32_t ub = __byte_perm(w[t], 0u, 0x4440u | q);  // byte q, zero-extended
+                // V = 2^52 + u exactly; fma(s2, V, -s2 2^52) = fl(s2 u): the reference's
+                // rounded product (emulator.cpp:53), then its rounded sum
+                const double V = __hiloint2double(0x43300000, static_cast<int>(ub));
+                c2[q] = __dadd_rn(c2[q], __fma_rn(c.s2[t], V, c.s2_m52[t]));
+                if constexpr (kFp64Tables) {
+                    // exact integer form of c1 += s1 u (see DevConsts::c1_int)
+                    c1i[q] += c.h1[t] * ub;
+                } else {
+                    // FP32 tables carry the full-width s1 (crt_tables.cpp:160-163):
+                    // keep the reference's two roundings
+                    c1[q] = __dadd_rn(c1[q], __dmul_rn(c.s1[t], __dsub_rn(V, 0x1.0p52)));
+                }
             }
         }
+    }
+    if constexpr (kFp64Tables) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c1[q] = scale_pow2(static_cast<double>(static_cast<long long>(c1i[q])), c.c1_shift);
     }
     const int ne = nu_exp[j];
 #pragma unroll
@@ -87,7 +96,7 @@ template <bool kF32Out, bool kPlain>
 void launch_variant(dim3 grid, cudaStream_t s, const uint8_t* u, int64_t ldu, int64_t stride, int64_t m, int64_t n,
                     const int32_t* mu_exp, const int32_t* nu_exp, const DevConsts& c, double alpha, double beta,
                     void* C, int64_t ldc) {
-    if (c.precision == OZK_FP64)
+    if (c.c1_int)
         reconstruct_kernel<kF32Out, kPlain, true>
             <<<grid, 128, 0, s>>>(u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, C, ldc);
     else

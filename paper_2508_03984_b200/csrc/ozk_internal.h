@@ -27,6 +27,13 @@ struct DevConsts {
     double s2[OZK_MAX_MODULI];
     double P1, P2, P_inv;
     float pp_fast, pp_accu;
+    // K3's integer form of C1 = sum s1_i U_i: s1_i = h_i * 2^c1_shift with
+    // integer h_i, valid (c1_int = 1) when the exact sum always fits 53 bits,
+    // which is what makes the reference's FP64 sum exact (crt_tables.cpp:165-169)
+    int c1_int;
+    int c1_shift;
+    unsigned long long h1[OZK_MAX_MODULI];
+    double s2_m52[OZK_MAX_MODULI];  // -s2_i * 2^52 (for fl(s2*u) = fma(s2, 2^52 + u, -s2 * 2^52))
 };
 
 DevConsts to_dev(const ozk_constants& c);
