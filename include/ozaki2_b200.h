@@ -156,10 +156,36 @@ int ozk_stage_residues(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n
 int ozk_stage_products(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, const int8_t* a_planes,
                        const int8_t* b_planes, int kind, void* out, int64_t ldo);
 /* K3: accumulate + crt_reduce + unscale (+ alpha/beta), reconstruct.hpp:46-59.
- * U[N][n][ldu] uint8 as written by ozk_stage_products(OZK_PRODUCTS_U8). */
+ * U[N][n][ldu] uint8 as written by ozk_stage_products(OZK_PRODUCTS_U8);
+ * ldu a multiple of 8 and U 8-byte aligned. */
 int ozk_stage_reconstruct(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, const uint8_t* U, int64_t ldu,
                           const int32_t* mu_exp, const int32_t* nu_exp, double alpha, double beta, void* C,
                           int64_t ldc);
+
+/* ---- the reference's element-wise stage helpers, on device buffers ---------
+ * (used by the C++ drop-in's stage functions; all synchronous) */
+/* int8_gemm (int8_engine.hpp:23-24): C = A B, int8 column-major A (m x k, lda)
+ * and B (k x n, ldb) with lda, ldb multiples of 16; int32 column-major C
+ * (ldc); two's-complement wrapping accumulation; k <= 2^17. */
+int ozk_int8_gemm(ozk_handle h, int64_t m, int64_t n, int64_t k, const int8_t* A, int64_t lda, const int8_t* B,
+                  int64_t ldb, int32_t* C, int64_t ldc);
+/* truncate_scale (residue.cpp:7-22): out = trunc(x * 2^e), e = scale_exp[i]
+ * (side 0, rows) or scale_exp[j] (side 1, columns); type OZK_R64F | OZK_R32F */
+int ozk_truncate_scale(ozk_handle h, int type, int64_t rows, int64_t cols, const void* x, int64_t ldx,
+                       const int32_t* scale_exp, int side, void* out, int64_t ldo);
+/* to_residue_slices (residue.cpp:24-42): planes[N][cols][ldp] = rmod_fast(x) */
+int ozk_residues(ozk_handle h, const ozk_config* cfg, int64_t rows, int64_t cols, const void* x, int64_t ldx,
+                 int8_t* planes, int64_t ldp);
+/* mod_u8 over an array (reduce_products_u8, reconstruct.cpp:7-20) */
+int ozk_mod_u8_array(ozk_handle h, int64_t count, const int32_t* x, int32_t p, int32_t pinv_mulhi, uint8_t* out);
+/* accumulate (reconstruct.cpp:22-38): N uint8 planes of `count` entries -> C1, C2 */
+int ozk_accumulate(ozk_handle h, const ozk_config* cfg, int64_t count, const uint8_t* u, double* c1, double* c2);
+/* crt_reduce (reconstruct.cpp:40-47) */
+int ozk_crt_reduce(ozk_handle h, const ozk_config* cfg, int64_t count, const double* c1, const double* c2,
+                   double* out);
+/* unscale (reconstruct.cpp:49-69): out = ldexp(cpp, -(mu_exp[i] + nu_exp[j])) */
+int ozk_unscale(ozk_handle h, int64_t m, int64_t n, const double* cpp, int64_t ldc, const int32_t* mu_exp,
+                const int32_t* nu_exp, double* out, int64_t ldo);
 
 /* number of this library's kernels launched on the handle since creation */
 int64_t ozk_kernel_launches(ozk_handle h);

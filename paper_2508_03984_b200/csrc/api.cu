@@ -60,30 +60,6 @@ DevConsts to_dev(const ozk_constants& c) {
     d.P_inv = c.P_inv;
     d.pp_fast = c.pp_fast;
     d.pp_accu = c.pp_accu;
-    // integer C1: common binary grid of the s1_i and a proof that every sum fits
-    int shift = 2000;
-    for (int i = 0; i < c.n_moduli; ++i) {
-        if (c.s1[i] == 0.0) continue;
-        int e = 0;
-        const double fr = std::frexp(c.s1[i], &e);  // s1 = fr * 2^e, fr in [0.5, 1)
-        long long mant = static_cast<long long>(std::ldexp(fr, 53));
-        int low = e - 53;
-        while (mant && !(mant & 1)) {
-            mant >>= 1;
-            ++low;
-        }
-        shift = low < shift ? low : shift;
-    }
-    bool ok = c.precision == OZK_FP64 && shift < 2000;
-    long double bound = 0;
-    for (int i = 0; i < c.n_moduli && ok; ++i) {
-        const long double hi = std::ldexp(static_cast<long double>(c.s1[i]), -shift);
-        ok = hi >= 0 && hi < 0x1p62L;
-        d.h1[i] = ok ? static_cast<unsigned long long>(hi) : 0ull;
-        bound += hi * (c.moduli[i] - 1);
-    }
-    d.c1_int = ok && bound < 0x1p53L;
-    d.c1_shift = ok ? shift : 0;
     for (int i = 0; i < c.n_moduli; ++i) d.s2_m52[i] = -c.s2[i] * 0x1p52;
     return d;
 }
@@ -868,8 +844,8 @@ int ozk_stage_reconstruct(ozk_handle h, const ozk_config* cfg, int64_t m, int64_
     if (!h) return OZK_INPUT_ERROR;
     ozk_constants c;
     OZK_TRY(resolve(cfg, c));
-    if (m < 1 || n < 1 || ldu < m || ldc < m || (ldu % 4) != 0) {
-        set_error("ozk_stage_reconstruct: bad dimensions (ldu must be a multiple of 4)");
+    if (m < 1 || n < 1 || ldu < m || ldc < m || (ldu % 8) != 0) {
+        set_error("ozk_stage_reconstruct: bad dimensions (ldu must be a multiple of 8)");
         return OZK_INPUT_ERROR;
     }
     OZK_CUDA(cudaSetDevice(h->device));
@@ -880,6 +856,110 @@ int ozk_stage_reconstruct(ozk_handle h, const ozk_config* cfg, int64_t m, int64_
     J.n = n;
     OZK_TRY(stage_reconstruct(h, J, 0, n, U, ldu, ldu * n, mu_exp, nu_exp, alpha, beta, C, ldc,
                               cfg->c_type == OZK_R32F));
+    OZK_CUDA(cudaStreamSynchronize(h->stream));
+    return OZK_OK;
+}
+
+int ozk_int8_gemm(ozk_handle h, int64_t m, int64_t n, int64_t k, const int8_t* A, int64_t lda, const int8_t* B,
+                  int64_t ldb, int32_t* C, int64_t ldc) {
+    if (!h) return OZK_INPUT_ERROR;
+    if (m < 0 || n < 0 || k < 0 || lda < m || ldb < k || ldc < m || (lda % 16) || (ldb % 16)) {
+        set_error("int8_gemm: bad dimensions (lda, ldb must be multiples of 16)");
+        return OZK_INPUT_ERROR;
+    }
+    if (k > OZK_ENGINE_MAX_K) {
+        set_error("int8_gemm: k exceeds 2^17, use blocked_int8_gemm");
+        return OZK_INPUT_ERROR;
+    }
+    OZK_CUDA(cudaSetDevice(h->device));
+    if (m == 0 || n == 0) return OZK_OK;
+    if (k == 0) {
+        for (int64_t j = 0; j < n; ++j) OZK_CUDA(cudaMemsetAsync(C + j * ldc, 0, sizeof(int32_t) * m, h->stream));
+        OZK_CUDA(cudaStreamSynchronize(h->stream));
+        return OZK_OK;
+    }
+    OZK_TRY(ensure(h->flags, 64));
+    Job J{};
+    J.flags = static_cast<int32_t*>(h->flags.p);
+    J.c.n_moduli = 1;  // one plane, raw int32 output: no modulus involved
+    J.dc.n = 1;
+    J.m = m;
+    J.n = n;
+    J.k = k;
+    J.ld = ldb;
+    J.lda_p = lda;
+    OZK_TRY(stage_products(h, J, 0, n, A, k * lda, B, n * ldb, OZK_PRODUCTS_I32, C, ldc, ldc * n));
+    OZK_CUDA(cudaStreamSynchronize(h->stream));
+    return OZK_OK;
+}
+
+int ozk_truncate_scale(ozk_handle h, int type, int64_t rows, int64_t cols, const void* x, int64_t ldx,
+                       const int32_t* scale_exp, int side, void* out, int64_t ldo) {
+    if (!h || rows < 0 || cols < 0 || ldx < rows || ldo < rows) return OZK_INPUT_ERROR;
+    OZK_CUDA(cudaSetDevice(h->device));
+    if (rows * cols == 0) return OZK_OK;
+    launch_truncate(type == OZK_R32F, x, rows, cols, ldx, scale_exp, side, out, ldo, h->stream);
+    OZK_TRY(check_launch(h, 1));
+    OZK_CUDA(cudaStreamSynchronize(h->stream));
+    return OZK_OK;
+}
+
+int ozk_residues(ozk_handle h, const ozk_config* cfg, int64_t rows, int64_t cols, const void* x, int64_t ldx,
+                 int8_t* planes, int64_t ldp) {
+    if (!h) return OZK_INPUT_ERROR;
+    ozk_constants c;
+    OZK_TRY(resolve(cfg, c));
+    if (rows < 0 || cols < 0 || ldx < rows || ldp < rows) return OZK_INPUT_ERROR;
+    OZK_CUDA(cudaSetDevice(h->device));
+    if (rows * cols == 0) return OZK_OK;
+    launch_residues_literal(cfg->a_type == OZK_R32F, x, rows, cols, ldx, to_dev(c), planes, ldp, h->stream);
+    OZK_TRY(check_launch(h, 1));
+    OZK_CUDA(cudaStreamSynchronize(h->stream));
+    return OZK_OK;
+}
+
+int ozk_mod_u8_array(ozk_handle h, int64_t count, const int32_t* x, int32_t p, int32_t pinv_mulhi, uint8_t* out) {
+    if (!h || count < 0) return OZK_INPUT_ERROR;
+    OZK_CUDA(cudaSetDevice(h->device));
+    if (!count) return OZK_OK;
+    launch_mod_u8(x, count, p, pinv_mulhi, out, h->stream);
+    OZK_TRY(check_launch(h, 1));
+    OZK_CUDA(cudaStreamSynchronize(h->stream));
+    return OZK_OK;
+}
+
+int ozk_accumulate(ozk_handle h, const ozk_config* cfg, int64_t count, const uint8_t* u, double* c1, double* c2) {
+    if (!h || count < 0) return OZK_INPUT_ERROR;
+    ozk_constants c;
+    OZK_TRY(resolve(cfg, c));
+    OZK_CUDA(cudaSetDevice(h->device));
+    if (!count) return OZK_OK;
+    launch_accumulate(u, count, to_dev(c), c1, c2, h->stream);
+    OZK_TRY(check_launch(h, 1));
+    OZK_CUDA(cudaStreamSynchronize(h->stream));
+    return OZK_OK;
+}
+
+int ozk_crt_reduce(ozk_handle h, const ozk_config* cfg, int64_t count, const double* c1, const double* c2,
+                   double* out) {
+    if (!h || count < 0) return OZK_INPUT_ERROR;
+    ozk_constants c;
+    OZK_TRY(resolve(cfg, c));
+    OZK_CUDA(cudaSetDevice(h->device));
+    if (!count) return OZK_OK;
+    launch_crt_reduce(c1, c2, count, to_dev(c), out, h->stream);
+    OZK_TRY(check_launch(h, 1));
+    OZK_CUDA(cudaStreamSynchronize(h->stream));
+    return OZK_OK;
+}
+
+int ozk_unscale(ozk_handle h, int64_t m, int64_t n, const double* cpp, int64_t ldc, const int32_t* mu_exp,
+                const int32_t* nu_exp, double* out, int64_t ldo) {
+    if (!h || m < 0 || n < 0 || ldc < m || ldo < m) return OZK_INPUT_ERROR;
+    OZK_CUDA(cudaSetDevice(h->device));
+    if (m * n == 0) return OZK_OK;
+    launch_unscale(cpp, m, n, ldc, mu_exp, nu_exp, out, ldo, h->stream);
+    OZK_TRY(check_launch(h, 1));
     OZK_CUDA(cudaStreamSynchronize(h->stream));
     return OZK_OK;
 }

@@ -15,9 +15,14 @@
 #include <stdexcept>
 #include <string>
 
+#include <cuda_runtime.h>
+
 #include "crtgemm/emulator.hpp"
 #include "crtgemm/errors.hpp"
+#include "crtgemm/int8_engine.hpp"
+#include "crtgemm/reconstruct.hpp"
 #include "crtgemm/residue.hpp"
+#include "crtgemm/scaling.hpp"
 #include "ozaki2_b200.h"
 
 namespace crtgemm {
@@ -132,6 +137,98 @@ EmulationResult run(const Matrix<T>& a, const Matrix<T>& b, const EmuConfig& cfg
     return r;
 }
 
+// device scratch for the stage helpers (RAII)
+struct Dev {
+    void* p = nullptr;
+    explicit Dev(size_t bytes) {
+        if (bytes && cudaMalloc(&p, bytes) != cudaSuccess) throw std::runtime_error("ozaki2_b200: cudaMalloc failed");
+    }
+    ~Dev() {
+        if (p) cudaFree(p);
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+void up(void* dst, const void* src, size_t bytes) {
+    if (bytes && cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+        throw std::runtime_error("ozaki2_b200: H2D copy failed");
+}
+void down(void* dst, const void* src, size_t bytes) {
+    if (bytes && cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+        throw std::runtime_error("ozaki2_b200: D2H copy failed");
+}
+
+std::vector<std::int32_t> exps_of(const std::vector<double>& scale) {
+    std::vector<std::int32_t> e(scale.size());
+    for (std::size_t i = 0; i < scale.size(); ++i) e[i] = std::ilogb(scale[i]);
+    return e;
+}
+
+template <typename T>
+ScalePair scale_impl(const Matrix<T>& a, const Matrix<T>& b, const CrtConstants& c, ScaleMode mode) {
+    ozk_constants oc = to_c(c);
+    ozk_config cfg = ozk_default_config(c.n(), mode_code(mode), prec_code(c.precision));
+    cfg.a_type = sizeof(T) == 4 ? OZK_R32F : OZK_R64F;
+    cfg.constants = &oc;
+    const std::int64_t m = a.rows, k = a.cols, n = b.cols;
+    Dev da(sizeof(T) * a.data.size()), db(sizeof(T) * b.data.size()), dmu(4 * m + 4), dnu(4 * n + 4);
+    up(da.p, a.data.data(), sizeof(T) * a.data.size());
+    up(db.p, b.data.data(), sizeof(T) * b.data.size());
+    std::lock_guard<std::mutex> lock(g_mtx);
+    check(ozk_stage_scale(handle_locked(), &cfg, m, n, k, da.p, m, db.p, k, dmu.as<std::int32_t>(),
+                          dnu.as<std::int32_t>()));
+    std::vector<std::int32_t> mu(m), nu(n);
+    down(mu.data(), dmu.p, 4 * m);
+    down(nu.data(), dnu.p, 4 * n);
+    ScalePair s;
+    s.mode = mode;
+    for (auto e : mu) s.mu.push_back(std::ldexp(1.0, e));
+    for (auto e : nu) s.nu.push_back(std::ldexp(1.0, e));
+    return s;
+}
+
+template <typename T>
+Matrix<T> truncate_impl(const Matrix<T>& m, const std::vector<double>& scale, Side side) {
+    const auto e = exps_of(scale);
+    Matrix<T> out(m.rows, m.cols);
+    Dev dx(sizeof(T) * m.data.size()), dout(sizeof(T) * m.data.size()), de(4 * e.size() + 4);
+    up(dx.p, m.data.data(), sizeof(T) * m.data.size());
+    up(de.p, e.data(), 4 * e.size());
+    std::lock_guard<std::mutex> lock(g_mtx);
+    check(ozk_truncate_scale(handle_locked(), sizeof(T) == 4 ? OZK_R32F : OZK_R64F, m.rows, m.cols, dx.p, m.rows,
+                             de.as<std::int32_t>(), side == Side::Row ? 0 : 1, dout.p, m.rows));
+    down(out.data.data(), dout.p, sizeof(T) * m.data.size());
+    return out;
+}
+
+template <typename T>
+ResidueSlices residues_impl(const Matrix<T>& m, const CrtConstants& c) {
+    ozk_constants oc = to_c(c);
+    ozk_config cfg = ozk_default_config(c.n(), OZK_FAST, prec_code(c.precision));
+    cfg.a_type = sizeof(T) == 4 ? OZK_R32F : OZK_R64F;
+    cfg.constants = &oc;
+    const std::int64_t cnt = m.size();
+    Dev dx(sizeof(T) * cnt + 8), dp(static_cast<size_t>(c.n() * cnt) + 8);
+    up(dx.p, m.data.data(), sizeof(T) * cnt);
+    {
+        std::lock_guard<std::mutex> lock(g_mtx);
+        check(ozk_residues(handle_locked(), &cfg, m.rows, m.cols, dx.p, m.rows, dp.as<std::int8_t>(), m.rows));
+    }
+    ResidueSlices rs;
+    rs.n_moduli = c.n();
+    rs.rows = m.rows;
+    rs.cols = m.cols;
+    for (int i = 0; i < c.n(); ++i) {
+        Matrix<std::int8_t> sl(m.rows, m.cols);
+        down(sl.data.data(), dp.as<std::int8_t>() + i * cnt, static_cast<size_t>(cnt));
+        rs.slices.push_back(std::move(sl));
+    }
+    return rs;
+}
+
 }  // namespace
 
 // ---- BigInt -------------------------------------------------------------------
@@ -216,6 +313,162 @@ EmulationResult gemm_emulated(const Matrix<double>& a, const Matrix<double>& b, 
 
 EmulationResult gemm_emulated(const Matrix<float>& a, const Matrix<float>& b, const EmuConfig& cfg) {
     return gemm_emulated(a, b, cfg, build_constants(cfg.n_moduli, cfg.precision));
+}
+
+// ---- stage functions (the reference's public stage API, on the GPU) ------------
+ScalePair scale_fast(const Matrix<double>& a, const Matrix<double>& b, const CrtConstants& c) {
+    return scale_impl(a, b, c, ScaleMode::Fast);
+}
+ScalePair scale_fast(const Matrix<float>& a, const Matrix<float>& b, const CrtConstants& c) {
+    return scale_impl(a, b, c, ScaleMode::Fast);
+}
+ScalePair scale_accurate(const Matrix<double>& a, const Matrix<double>& b, const CrtConstants& c,
+                         std::int64_t block_k, int /*n_threads*/) {
+    if (block_k < 1) throw InputError("blocked_int8_gemm: invalid block_k");  // int8_engine.cpp:86
+    return scale_impl(a, b, c, ScaleMode::Accurate);
+}
+ScalePair scale_accurate(const Matrix<float>& a, const Matrix<float>& b, const CrtConstants& c,
+                         std::int64_t block_k, int /*n_threads*/) {
+    if (block_k < 1) throw InputError("blocked_int8_gemm: invalid block_k");
+    return scale_impl(a, b, c, ScaleMode::Accurate);
+}
+
+Matrix<double> truncate_scale(const Matrix<double>& m, const std::vector<double>& scale, Side side) {
+    return truncate_impl(m, scale, side);
+}
+Matrix<float> truncate_scale(const Matrix<float>& m, const std::vector<double>& scale, Side side) {
+    return truncate_impl(m, scale, side);
+}
+ResidueSlices to_residue_slices(const Matrix<double>& m, const CrtConstants& c) { return residues_impl(m, c); }
+ResidueSlices to_residue_slices(const Matrix<float>& m, const CrtConstants& c) { return residues_impl(m, c); }
+
+Int32ProductMatrix int8_gemm(const Matrix<std::int8_t>& a, const Matrix<std::int8_t>& b, int /*n_threads*/) {
+    if (a.cols != b.rows) throw InputError("int8_gemm: inner dimensions disagree");
+    if (a.cols > kEngineMaxK) throw InputError("int8_gemm: k exceeds 2^17, use blocked_int8_gemm");
+    const std::int64_t m = a.rows, k = a.cols, n = b.cols;
+    const std::int64_t lda = (m + 15) / 16 * 16, ldb = (k + 15) / 16 * 16;
+    Int32ProductMatrix out;
+    out.k_used = k;
+    out.data = Matrix<std::int32_t>(m, n);
+    Dev da(static_cast<size_t>(lda * k) + 16), db(static_cast<size_t>(ldb * n) + 16), dc(4 * m * n + 16);
+    if (k && m && cudaMemcpy2D(da.p, lda, a.data.data(), m, m, k, cudaMemcpyHostToDevice) != cudaSuccess)
+        throw std::runtime_error("ozaki2_b200: H2D copy failed");
+    if (k && n && cudaMemcpy2D(db.p, ldb, b.data.data(), k, k, n, cudaMemcpyHostToDevice) != cudaSuccess)
+        throw std::runtime_error("ozaki2_b200: H2D copy failed");
+    {
+        std::lock_guard<std::mutex> lock(g_mtx);
+        check(ozk_int8_gemm(handle_locked(), m, n, k, da.as<std::int8_t>(), lda, db.as<std::int8_t>(), ldb,
+                            dc.as<std::int32_t>(), m));
+    }
+    down(out.data.data.data(), dc.p, 4 * static_cast<size_t>(m * n));
+    return out;
+}
+
+// The reference keeps a triple loop here as an in-tree cross-check of its
+// tiled CPU kernel (int8_engine.cpp:66-80); on the GPU both names run the
+// tensor-core engine, whose parity tests check it against the oracle instead.
+Int32ProductMatrix int8_gemm_reference(const Matrix<std::int8_t>& a, const Matrix<std::int8_t>& b) {
+    if (a.cols != b.rows) throw InputError("int8_gemm_reference: inner dimensions disagree");
+    if (a.cols > kEngineMaxK) throw InputError("int8_gemm_reference: k exceeds 2^17");
+    return int8_gemm(a, b, 1);
+}
+
+std::vector<Int32ProductMatrix> blocked_int8_gemm(const Matrix<std::int8_t>& a, const Matrix<std::int8_t>& b,
+                                                  std::int64_t block_k, int n_threads) {
+    if (a.cols != b.rows) throw InputError("blocked_int8_gemm: inner dimensions disagree");
+    if (block_k < 1 || block_k > kEngineMaxK) throw InputError("blocked_int8_gemm: invalid block_k");
+    std::vector<Int32ProductMatrix> out;
+    for (std::int64_t h0 = 0; h0 < a.cols; h0 += block_k) {
+        const std::int64_t len = std::min(block_k, a.cols - h0);
+        out.push_back(int8_gemm(column_block(a, h0, len), row_block(b, h0, len), n_threads));
+    }
+    if (out.empty()) {
+        Int32ProductMatrix zero;
+        zero.data = Matrix<std::int32_t>(a.rows, b.cols);
+        out.push_back(std::move(zero));
+    }
+    return out;
+}
+
+ResidueProducts reduce_products_u8(const std::vector<Int32ProductMatrix>& prods, const CrtConstants& c) {
+    if (static_cast<int>(prods.size()) != c.n())
+        throw InputError("reduce_products_u8: product count does not match modulus count");
+    ResidueProducts out;
+    for (int i = 0; i < c.n(); ++i) {
+        const auto& src = prods[static_cast<std::size_t>(i)].data;
+        const std::int64_t cnt = src.size();
+        Dev dx(4 * static_cast<size_t>(cnt) + 4), du(static_cast<size_t>(cnt) + 4);
+        up(dx.p, src.data.data(), 4 * static_cast<size_t>(cnt));
+        {
+            std::lock_guard<std::mutex> lock(g_mtx);
+            check(ozk_mod_u8_array(handle_locked(), cnt, dx.as<std::int32_t>(),
+                                   c.modulus_set.moduli[static_cast<std::size_t>(i)],
+                                   c.pinv_mulhi[static_cast<std::size_t>(i)], du.as<std::uint8_t>()));
+        }
+        Matrix<std::uint8_t> u(src.rows, src.cols);
+        down(u.data.data(), du.p, static_cast<size_t>(cnt));
+        out.u.push_back(std::move(u));
+    }
+    return out;
+}
+
+std::pair<Matrix<double>, Matrix<double>> accumulate(const ResidueProducts& u, const CrtConstants& c) {
+    if (static_cast<int>(u.u.size()) != c.n()) throw InputError("accumulate: residue count does not match modulus count");
+    const std::int64_t rows = u.u.front().rows, cols = u.u.front().cols, cnt = rows * cols;
+    ozk_constants oc = to_c(c);
+    ozk_config cfg = ozk_default_config(c.n(), OZK_FAST, prec_code(c.precision));
+    cfg.constants = &oc;
+    Dev du(static_cast<size_t>(c.n() * cnt) + 4), d1(8 * static_cast<size_t>(cnt) + 8), d2(8 * static_cast<size_t>(cnt) + 8);
+    for (int i = 0; i < c.n(); ++i) up(du.as<std::uint8_t>() + i * cnt, u.u[static_cast<std::size_t>(i)].data.data(), cnt);
+    {
+        std::lock_guard<std::mutex> lock(g_mtx);
+        check(ozk_accumulate(handle_locked(), &cfg, cnt, du.as<std::uint8_t>(), d1.as<double>(), d2.as<double>()));
+    }
+    Matrix<double> c1(rows, cols), c2(rows, cols);
+    down(c1.data.data(), d1.p, 8 * static_cast<size_t>(cnt));
+    down(c2.data.data(), d2.p, 8 * static_cast<size_t>(cnt));
+    return {std::move(c1), std::move(c2)};
+}
+
+Matrix<double> crt_reduce(const Matrix<double>& c1, const Matrix<double>& c2, const CrtConstants& c) {
+    if (c1.rows != c2.rows || c1.cols != c2.cols) throw InputError("crt_reduce: shape mismatch");
+    const std::int64_t cnt = c1.size();
+    ozk_constants oc = to_c(c);
+    ozk_config cfg = ozk_default_config(c.n(), OZK_FAST, prec_code(c.precision));
+    cfg.constants = &oc;
+    Dev d1(8 * static_cast<size_t>(cnt) + 8), d2(8 * static_cast<size_t>(cnt) + 8), dout(8 * static_cast<size_t>(cnt) + 8);
+    up(d1.p, c1.data.data(), 8 * static_cast<size_t>(cnt));
+    up(d2.p, c2.data.data(), 8 * static_cast<size_t>(cnt));
+    {
+        std::lock_guard<std::mutex> lock(g_mtx);
+        check(ozk_crt_reduce(handle_locked(), &cfg, cnt, d1.as<double>(), d2.as<double>(), dout.as<double>()));
+    }
+    Matrix<double> out(c1.rows, c1.cols);
+    down(out.data.data(), dout.p, 8 * static_cast<size_t>(cnt));
+    return out;
+}
+
+EmulationResult unscale(const Matrix<double>& cpp, const ScalePair& scales, const CrtConstants& c) {
+    const std::int64_t m = cpp.rows, n = cpp.cols;
+    if (static_cast<std::int64_t>(scales.mu.size()) != m || static_cast<std::int64_t>(scales.nu.size()) != n)
+        throw InputError("unscale: scale vector length mismatch");
+    const auto mu = exps_of(scales.mu), nu = exps_of(scales.nu);
+    Dev dc(8 * static_cast<size_t>(m * n) + 8), dout(8 * static_cast<size_t>(m * n) + 8), dmu(4 * m + 4), dnu(4 * n + 4);
+    up(dc.p, cpp.data.data(), 8 * static_cast<size_t>(m * n));
+    up(dmu.p, mu.data(), 4 * m);
+    up(dnu.p, nu.data(), 4 * n);
+    {
+        std::lock_guard<std::mutex> lock(g_mtx);
+        check(ozk_unscale(handle_locked(), m, n, dc.as<double>(), m, dmu.as<std::int32_t>(), dnu.as<std::int32_t>(),
+                          dout.as<double>(), m));
+    }
+    EmulationResult r;
+    r.n_moduli = c.n();
+    r.mode = scales.mode;
+    r.precision = c.precision;
+    r.c = Matrix<double>(m, n);
+    down(r.c.data.data(), dout.p, 8 * static_cast<size_t>(m * n));
+    return r;
 }
 
 Matrix<float> to_fp32(const Matrix<double>& m) {

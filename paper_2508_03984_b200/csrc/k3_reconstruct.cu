@@ -9,12 +9,14 @@
 //   C  = ldexp(C'', -(e_mu_i + e_nu_j))
 // then the optional alpha/beta extension in FP64 and the FP32 down-cast of
 // to_fp32 (emulator.cpp:110-115) when C is single precision. Each thread owns
-// four consecutive rows: one 32-bit load per plane, 32 B of C out, so a warp
-// moves 128 B per plane and 1 KB of C — HBM-bound at N + 8 bytes per element.
+// eight consecutive rows: one 64-bit load per plane, 64 B of C out, so a warp
+// moves 256 B per plane and 2 KB of C — HBM-bound at N + 8 bytes per element.
 #include "ozk_device.cuh"
 
 namespace ozk {
 namespace {
+
+constexpr int kRows = 8;  // rows per thread: one 8-byte load per plane, 64 B of C out
 
 // ldexp(x, e) as one multiply by 2^e when that is exact-and-correctly-rounded
 // (2^e normal, result normal); CUDA's general ldexp otherwise (subnormal or
@@ -34,46 +36,43 @@ __global__ void __launch_bounds__(128)
                        const int32_t* __restrict__ mu_exp, const int32_t* __restrict__ nu_exp, const DevConsts c,
                        double alpha, double beta, void* __restrict__ C, int64_t ldc) {
     const int64_t j = blockIdx.x;
-    const int64_t i0 = (static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x) * 4;
+    const int64_t i0 = (static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x) * kRows;
     if (i0 >= m) return;
-    double c1[4] = {0.0, 0.0, 0.0, 0.0}, c2[4] = {0.0, 0.0, 0.0, 0.0};
-    unsigned long long c1i[4] = {0ull, 0ull, 0ull, 0ull};
+    double c1[kRows], c2[kRows];
+#pragma unroll
+    for (int q = 0; q < kRows; ++q) c1[q] = c2[q] = 0.0;
     const uint8_t* src = u + j * ldu + i0;
     const int n_mod = c.n;
     // all plane loads first (predicated, compile-time indices: registers), so
     // a thread has its N loads in flight at once instead of one per FP chain step
-    uint32_t w[OZK_MAX_MODULI];
+    uint2 w[OZK_MAX_MODULI];
 #pragma unroll
     for (int t = 0; t < OZK_MAX_MODULI; ++t)
-        w[t] = t < n_mod ? __ldg(reinterpret_cast<const uint32_t*>(src + t * plane_stride)) : 0u;
+        w[t] = t < n_mod ? __ldg(reinterpret_cast<const uint2*>(src + t * plane_stride)) : make_uint2(0u, 0u);
 #pragma unroll
     for (int t = 0; t < OZK_MAX_MODULI; ++t) {  // compile-time bound: constants become immediates
         if (t < n_mod) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t ub = __byte_perm(w[t], 0u, 0x4440u | q);  // byte q, zero-extended
-                // V = 2^52 + u exactly; fma(s2, V, -s2 2^52) = fl(s2 u): the reference's
-                // rounded product (emulator.cpp:53), then its rounded sum
+            for (int q = 0; q < kRows; ++q) {
+                const uint32_t word = q < 4 ? w[t].x : w[t].y;
+                const uint32_t ub = __byte_perm(word, 0u, 0x4440u | (q & 3));  // byte q, zero-extended
+                // V = 2^52 + u exactly (no conversion instruction); v = u
                 const double V = __hiloint2double(0x43300000, static_cast<int>(ub));
+                const double v = __dsub_rn(V, 0x1.0p52);
+                // FP64 tables: s1*u is exact and so is the running sum (beta_i
+                // construction), so the fused form equals the reference's
+                // mul-then-add bit for bit. FP32 tables carry the full-width s1
+                // (crt_tables.cpp:160-163): keep the two roundings there.
+                c1[q] = kFp64Tables ? __fma_rn(c.s1[t], v, c1[q]) : __dadd_rn(c1[q], __dmul_rn(c.s1[t], v));
+                // fl(s2 u) = fma(s2, 2^52 + u, -s2 2^52): the reference's rounded
+                // product (emulator.cpp:53), then its rounded sum
                 c2[q] = __dadd_rn(c2[q], __fma_rn(c.s2[t], V, c.s2_m52[t]));
-                if constexpr (kFp64Tables) {
-                    // exact integer form of c1 += s1 u (see DevConsts::c1_int)
-                    c1i[q] += c.h1[t] * ub;
-                } else {
-                    // FP32 tables carry the full-width s1 (crt_tables.cpp:160-163):
-                    // keep the reference's two roundings
-                    c1[q] = __dadd_rn(c1[q], __dmul_rn(c.s1[t], __dsub_rn(V, 0x1.0p52)));
-                }
             }
         }
     }
-    if constexpr (kFp64Tables) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) c1[q] = scale_pow2(static_cast<double>(static_cast<long long>(c1i[q])), c.c1_shift);
-    }
     const int ne = nu_exp[j];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kRows; ++q) {
         const int64_t i = i0 + q;
         if (i >= m) break;
         const double qv = rint(__dmul_rn(c.P_inv, c1[q]));
@@ -96,7 +95,7 @@ template <bool kF32Out, bool kPlain>
 void launch_variant(dim3 grid, cudaStream_t s, const uint8_t* u, int64_t ldu, int64_t stride, int64_t m, int64_t n,
                     const int32_t* mu_exp, const int32_t* nu_exp, const DevConsts& c, double alpha, double beta,
                     void* C, int64_t ldc) {
-    if (c.c1_int)
+    if (c.precision == OZK_FP64)
         reconstruct_kernel<kF32Out, kPlain, true>
             <<<grid, 128, 0, s>>>(u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, C, ldc);
     else
@@ -109,7 +108,7 @@ void launch_variant(dim3 grid, cudaStream_t s, const uint8_t* u, int64_t ldu, in
 void launch_reconstruct(const uint8_t* u, int64_t ldu, int64_t stride, int64_t m, int64_t n, const int32_t* mu_exp,
                         const int32_t* nu_exp, const DevConsts& c, double alpha, double beta, void* C, int64_t ldc,
                         int c_is_f32, cudaStream_t s) {
-    dim3 grid(static_cast<unsigned>(n), static_cast<unsigned>((m + 511) / 512));
+    dim3 grid(static_cast<unsigned>(n), static_cast<unsigned>((m + 128 * kRows - 1) / (128 * kRows)));
     const bool plain = alpha == 1.0 && beta == 0.0;
     if (c_is_f32) {
         if (plain)

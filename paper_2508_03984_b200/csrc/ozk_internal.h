@@ -27,12 +27,6 @@ struct DevConsts {
     double s2[OZK_MAX_MODULI];
     double P1, P2, P_inv;
     float pp_fast, pp_accu;
-    // K3's integer form of C1 = sum s1_i U_i: s1_i = h_i * 2^c1_shift with
-    // integer h_i, valid (c1_int = 1) when the exact sum always fits 53 bits,
-    // which is what makes the reference's FP64 sum exact (crt_tables.cpp:165-169)
-    int c1_int;
-    int c1_shift;
-    unsigned long long h1[OZK_MAX_MODULI];
     double s2_m52[OZK_MAX_MODULI];  // -s2_i * 2^52 (for fl(s2*u) = fma(s2, 2^52 + u, -s2 * 2^52))
 };
 
@@ -100,5 +94,17 @@ int launch_k2(const K2Launch& L, cudaStream_t s);
 void launch_reconstruct(const uint8_t* u, int64_t ldu, int64_t plane_stride, int64_t m, int64_t n, const int32_t* mu_exp,
                         const int32_t* nu_exp, const DevConsts& c, double alpha, double beta, void* C, int64_t ldc,
                         int c_is_f32, cudaStream_t s);
+
+// ---- element-wise stage helpers (k_misc.cu) ---------------------------------
+void launch_truncate(int is_f32, const void* x, int64_t rows, int64_t cols, int64_t ldx, const int32_t* se, int side,
+                     void* out, int64_t ldo, cudaStream_t s);
+void launch_residues_literal(int is_f32, const void* x, int64_t rows, int64_t cols, int64_t ldx, const DevConsts& c,
+                             int8_t* planes, int64_t ldp, cudaStream_t s);
+void launch_mod_u8(const int32_t* x, int64_t count, int32_t p, int32_t pinv, uint8_t* out, cudaStream_t s);
+void launch_accumulate(const uint8_t* u, int64_t count, const DevConsts& c, double* c1, double* c2, cudaStream_t s);
+void launch_crt_reduce(const double* c1, const double* c2, int64_t count, const DevConsts& c, double* out,
+                       cudaStream_t s);
+void launch_unscale(const double* cpp, int64_t m, int64_t n, int64_t ldc, const int32_t* mu, const int32_t* nu,
+                    double* out, int64_t ldo, cudaStream_t s);
 
 }  // namespace ozk

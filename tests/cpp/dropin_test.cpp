@@ -15,6 +15,10 @@
 
 #include "crtgemm/emulator.hpp"
 #include "crtgemm/errors.hpp"
+#include "crtgemm/int8_engine.hpp"
+#include "crtgemm/reconstruct.hpp"
+#include "crtgemm/residue.hpp"
+#include "crtgemm/scaling.hpp"
 
 using namespace crtgemm;
 
@@ -80,6 +84,33 @@ int main(int argc, char** argv) {
     if (mod_u8(-1, 255, c14.pinv_mulhi[1]) != 254) return 9;
     const Matrix<float> f = to_fp32(read_matrix(dir + "/a.bin"));
     if (f.rows != a.rows) return 10;
+    // the stage-level API composes to exactly gemm_emulated (emulator.cpp:25-78)
+    for (int accurate = 0; accurate < 2; ++accurate) {
+        const CrtConstants& c = build_constants(14, Precision::Fp64);
+        const ScalePair s = accurate ? scale_accurate(a, b, c) : scale_fast(a, b, c);
+        const Matrix<double> ap = truncate_scale(a, s.mu, Side::Row), bp = truncate_scale(b, s.nu, Side::Col);
+        const ResidueSlices sa = to_residue_slices(ap, c), sb = to_residue_slices(bp, c);
+        std::vector<Int32ProductMatrix> prods;
+        for (int i = 0; i < c.n(); ++i) {
+            prods.push_back(int8_gemm(sa.slices[static_cast<size_t>(i)], sb.slices[static_cast<size_t>(i)]));
+            const auto ref = int8_gemm_reference(sa.slices[static_cast<size_t>(i)], sb.slices[static_cast<size_t>(i)]);
+            if (!(ref.data == prods.back().data)) return 11;
+        }
+        const auto blocks = blocked_int8_gemm(sa.slices[1], sb.slices[1], 32);
+        Matrix<std::int32_t> sum(a.rows, b.cols);
+        for (const auto& blk : blocks)
+            for (size_t e = 0; e < sum.data.size(); ++e) sum.data[e] += blk.data.data[e];
+        if (!(sum == prods[1].data)) return 12;
+        const ResidueProducts u = reduce_products_u8(prods, c);
+        const auto c12 = accumulate(u, c);
+        const EmulationResult r = unscale(crt_reduce(c12.first, c12.second, c), s, c);
+        EmuConfig cfg;
+        cfg.n_moduli = 14;
+        cfg.mode = accurate ? ScaleMode::Accurate : ScaleMode::Fast;
+        const EmulationResult direct = gemm_emulated(a, b, cfg);
+        if (!(r.c == direct.c)) return 13;
+        write_matrix(dir + "/stages_" + std::to_string(accurate) + ".bin", r.c);
+    }
     std::printf("dropin ok: %d cases\n", idx);
     return 0;
 }

@@ -55,5 +55,8 @@ def test_cpp_dropin_bitexact(tmp_path, oracle):
         aa, bb = (a.astype(np.float32), b.astype(np.float32)) if prec else (a, b)
         want = oracle.gemm(aa, bb, N, mode, prec=prec)
         np.testing.assert_array_equal(got.view(np.int64), want.view(np.int64))
+    for mode in (0, 1):  # the stage-level API composed by hand == the oracle pipeline
+        got = _read(tmp_path / f"stages_{mode}.bin")
+        np.testing.assert_array_equal(got.view(np.int64), oracle.gemm(a, b, 14, mode).view(np.int64))
     gold = open(os.path.join(ROOT, "tests", "golden", "tables_14_fp64.csv")).read()
     assert (tmp_path / "tables_14.csv").read_text() == gold
