@@ -44,6 +44,13 @@ extern "C" {
 #define OZK_FAST 0
 #define OZK_ACCURATE 1
 
+/* ozk_config.flags. OZK_FLAG_FAST_EXPONENT_FIX: fast-mode scaling subtracts
+ * the row/column max exponent g = floor(log2 max|x|), which the reference
+ * omits (scaling.cpp:50-56 vs PAPER.md:313-314); without it the
+ * reference's fast mode breaks the CRT range for |x| >= 2 rows/columns. Off by
+ * default: results then equal the reference bit for bit. */
+#define OZK_FLAG_FAST_EXPONENT_FIX 1
+
 /* storage types of A/B/C buffers */
 #define OZK_R64F 0
 #define OZK_R32F 1
@@ -82,7 +89,7 @@ typedef struct {
     int32_t precision; /* OZK_FP64 | OZK_FP32 */
     int32_t a_type;    /* OZK_R64F | OZK_R32F (also B's type) */
     int32_t c_type;    /* OZK_R64F | OZK_R32F */
-    int32_t reserved;
+    int32_t flags;     /* OZK_FLAG_* (0 = the reference's behaviour) */
     int64_t block_k; /* validated in [1, 2^17] like the reference; results do not depend on it */
     const ozk_constants* constants;
 } ozk_config;

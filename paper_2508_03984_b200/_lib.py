@@ -18,6 +18,7 @@ OZK_FP64, OZK_FP32 = 0, 1
 OZK_FAST, OZK_ACCURATE = 0, 1
 OZK_R64F, OZK_R32F = 0, 1
 OZK_PRODUCTS_I32, OZK_PRODUCTS_U8 = 0, 1
+OZK_FLAG_FAST_EXPONENT_FIX = 1
 MAX_MODULI = 20
 ENGINE_MAX_K = 1 << 17
 
@@ -76,7 +77,7 @@ class OzkConfig(C.Structure):
         ("precision", C.c_int32),
         ("a_type", C.c_int32),
         ("c_type", C.c_int32),
-        ("reserved", C.c_int32),
+        ("flags", C.c_int32),
         ("block_k", C.c_int64),
         ("constants", C.POINTER(OzkConstants)),
     ]

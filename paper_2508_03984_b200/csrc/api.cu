@@ -220,6 +220,7 @@ int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c,
           const void* A, int64_t lda, const void* B, int64_t ldb, bool need_products) {
     J.c = c;
     J.dc = to_dev(c);
+    J.dc.fast_fix = (cfg->flags & OZK_FLAG_FAST_EXPONENT_FIX) ? 1 : 0;
     J.mode = cfg->mode;
     J.m = m;
     J.n = n;

@@ -153,8 +153,9 @@ __device__ __forceinline__ bool needs_exact(double y, double mx, int64_t k) {
 // One thread per line (a row of A or a column of a B block). Rows combine
 // `splits` k-partials laid out [split][lines].
 __global__ void fast_finalize_kernel(const double* __restrict__ pmax, const double* __restrict__ psum, int splits,
-                                     int64_t lines, int64_t k, float pp_fast, int prec, int32_t* __restrict__ exp_out,
-                                     int32_t* __restrict__ flag_count, int32_t* __restrict__ flag_list) {
+                                     int64_t lines, int64_t k, float pp_fast, int prec, int fix,
+                                     int32_t* __restrict__ exp_out, int32_t* __restrict__ flag_count,
+                                     int32_t* __restrict__ flag_list) {
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= lines) return;
     double mx = pmax[t], s = psum[t];
@@ -166,7 +167,7 @@ __global__ void fast_finalize_kernel(const double* __restrict__ pmax, const doub
     if (mx != 0.0) {
         const int g = ilogb(mx);
         const double y = fast_budget(ldexp(s, -2 * g), k, pp_fast);
-        e = fast_exponent_from_budget(y, g, prec);
+        e = fast_exponent_from_budget(y, g, prec, fix);
         if (needs_exact(y, mx, k)) flag_list[atomicAdd(flag_count, 1)] = static_cast<int32_t>(t);
     }
     exp_out[t] = e;
@@ -175,7 +176,7 @@ __global__ void fast_finalize_kernel(const double* __restrict__ pmax, const doub
 // One warp per flagged line: element h of line l sits at base[l*line_step + h*elem_step].
 // Reference order: s = 0; for h: nh = ldexp(x_h, -g); s += nh*nh (no FMA).
 __global__ void fast_exact_kernel(const void* __restrict__ base, int is_f32, int64_t line_step, int64_t elem_step,
-                                  int64_t k, float pp_fast, int prec, const int32_t* __restrict__ flag_count,
+                                  int64_t k, float pp_fast, int prec, int fix, const int32_t* __restrict__ flag_count,
                                   const int32_t* __restrict__ flag_list, int32_t* __restrict__ exp_out) {
     const int lane = threadIdx.x % 32;
     const int warps = gridDim.x * (blockDim.x / 32);
@@ -199,7 +200,7 @@ __global__ void fast_exact_kernel(const void* __restrict__ base, int is_f32, int
             const int cnt = k - h0 < 32 ? static_cast<int>(k - h0) : 32;
             for (int q = 0; q < cnt; ++q) s = __dadd_rn(s, __shfl_sync(0xffffffffu, sq, q));
         }
-        if (lane == 0) exp_out[line] = fast_exponent_from_budget(fast_budget(s, k, pp_fast), g, prec);
+        if (lane == 0) exp_out[line] = fast_exponent_from_budget(fast_budget(s, k, pp_fast), g, prec, fix);
     }
 }
 
@@ -265,7 +266,7 @@ void launch_fast_finalize(const double* pmax, const double* psum, int splits, in
                           cudaStream_t s) {
     cudaMemsetAsync(flag_count, 0, sizeof(int32_t), s);
     fast_finalize_kernel<<<static_cast<unsigned>((lines + 255) / 256), 256, 0, s>>>(
-        pmax, psum, splits, lines, k, c.pp_fast, c.precision, exp_out, flag_count, flag_list);
+        pmax, psum, splits, lines, k, c.pp_fast, c.precision, c.fast_fix, exp_out, flag_count, flag_list);
 }
 
 void launch_fast_exact(const void* base, int is_f32, int64_t line_step, int64_t elem_step, int64_t k,
@@ -273,8 +274,8 @@ void launch_fast_exact(const void* base, int is_f32, int64_t line_step, int64_t 
                        cudaStream_t s) {
     // The flagged count lives on the device; a fixed grid strides over it, so
     // the common case (nothing flagged) costs one tiny launch and no host sync.
-    fast_exact_kernel<<<148, 256, 0, s>>>(base, is_f32, line_step, elem_step, k, c.pp_fast, c.precision, flag_count,
-                                          flag_list, exp_out);
+    fast_exact_kernel<<<148, 256, 0, s>>>(base, is_f32, line_step, elem_step, k, c.pp_fast, c.precision, c.fast_fix,
+                                          flag_count, flag_list, exp_out);
 }
 
 void launch_accurate_base(const double* pmax, int splits, int64_t lines, int32_t* out, cudaStream_t s) {

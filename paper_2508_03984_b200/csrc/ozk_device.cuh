@@ -98,9 +98,9 @@ __device__ __forceinline__ double fast_budget(double s, int64_t k, float pp_fast
     return __dsub_rn(static_cast<double>(pp_fast), t);
 }
 // fast_exponent tail (scaling.cpp:52-55); the reference omits the "- g" term
-// and so do we.
-__device__ __forceinline__ int fast_exponent_from_budget(double y, int g, int prec) {
-    int e = static_cast<int>(floor(y));
+// and so do we, unless OZK_FLAG_FAST_EXPONENT_FIX asks for it.
+__device__ __forceinline__ int fast_exponent_from_budget(double y, int g, int prec, int fix = 0) {
+    int e = static_cast<int>(floor(y)) - (fix ? g : 0);
     const int cap = magnitude_cap(prec) - 1 - g;
     e = e < cap ? e : cap;
     const int cl = exponent_clamp(prec);

@@ -27,7 +27,8 @@ struct DevConsts {
     double s2[OZK_MAX_MODULI];
     double P1, P2, P_inv;
     float pp_fast, pp_accu;
-    double s2_m52[OZK_MAX_MODULI];  // -s2_i * 2^52 (for fl(s2*u) = fma(s2, 2^52 + u, -s2 * 2^52))
+    double s2_m52[OZK_MAX_MODULI];
+    int fast_fix;  // OZK_FLAG_FAST_EXPONENT_FIX  // -s2_i * 2^52 (for fl(s2*u) = fma(s2, 2^52 + u, -s2 * 2^52))
 };
 
 DevConsts to_dev(const ozk_constants& c);

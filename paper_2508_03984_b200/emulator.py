@@ -46,6 +46,9 @@ class EmuConfig:
     precision: Precision = Precision.Fp64
     block_k: int = kEngineMaxK
     threads: int = 1
+    # extension (not in the reference): subtract the max exponent in fast-mode
+    # scaling, the term scaling.cpp:50-56 omits. Off = reference bits.
+    fast_exponent_fix: bool = False
 
 
 @dataclasses.dataclass
@@ -95,6 +98,7 @@ def _config(cfg: EmuConfig, a_type: int, c_type: int, constants=None) -> _lib.Oz
     c.a_type = a_type
     c.c_type = c_type
     c.block_k = int(cfg.block_k)
+    c.flags = _lib.OZK_FLAG_FAST_EXPONENT_FIX if getattr(cfg, "fast_exponent_fix", False) else 0
     c.constants = C.pointer(constants) if constants is not None else None
     return c
 
