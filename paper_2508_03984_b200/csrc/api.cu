@@ -80,7 +80,7 @@ struct Job {
     int64_t lda, ldb;
     int in_f32;
     int32_t *mu, *nu, *ma, *nb, *rowmax, *colmax, *flag_rows, *flag_cols;
-    int32_t* flags;  // [0] non-finite, [1] flagged rows, [2] flagged columns, [4] K2 lockstep counter
+    int32_t* flags;  // [0] non-finite, [1] flagged rows, [2] flagged columns, [4..] K2 lockstep words (1 KB)
     double *amax, *asum, *bmax, *bsum;
     int splits;
     int8_t *pa, *pb;
@@ -230,7 +230,7 @@ int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c,
     J.ldu = u_ld(m);
     const int N = c.n_moduli;
     J.splits = row_stats_splits(m, k);
-    OZK_TRY(ensure(h->flags, 64));
+    OZK_TRY(ensure(h->flags, 2048));
     OZK_TRY(ensure(h->stats, sizeof(double) * (2 * J.splits * m + 2 * n)));
     OZK_TRY(ensure(h->ints, sizeof(int32_t) * 4 * (m + n)));
     if (need_products) {
@@ -264,7 +264,7 @@ int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c,
     J.lda = lda;
     J.ldb = ldb;
     J.in_f32 = cfg->a_type == OZK_R32F;
-    OZK_CUDA(cudaMemsetAsync(J.flags, 0, 64, h->stream));
+    OZK_CUDA(cudaMemsetAsync(J.flags, 0, 16, h->stream));
     return OZK_OK;
 }
 
@@ -824,7 +824,7 @@ int ozk_stage_products(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n
         return OZK_INPUT_ERROR;
     }
     OZK_CUDA(cudaSetDevice(h->device));
-    OZK_TRY(ensure(h->flags, 64));
+    OZK_TRY(ensure(h->flags, 2048));
     Job J{};
     J.flags = static_cast<int32_t*>(h->flags.p);
     J.c = c;
@@ -879,7 +879,7 @@ int ozk_int8_gemm(ozk_handle h, int64_t m, int64_t n, int64_t k, const int8_t* A
         OZK_CUDA(cudaStreamSynchronize(h->stream));
         return OZK_OK;
     }
-    OZK_TRY(ensure(h->flags, 64));
+    OZK_TRY(ensure(h->flags, 2048));
     Job J{};
     J.flags = static_cast<int32_t*>(h->flags.p);
     J.c.n_moduli = 1;  // one plane, raw int32 output: no modulus involved

@@ -64,8 +64,11 @@ struct K2Params {
     int pinv[OZK_MAX_MODULI];
     int group;             // tile rows per raster group
     int hints;             // 1: L2 evict_last on operand loads, streaming U stores
-    int sync_slack;        // >0: a cluster starts tile lt only after every cluster finished lt - slack
-    unsigned int* done;    // completed (cluster, tile) count for sync_slack
+    int sync_mode;         // 0 off; 1 tile lockstep (slack 1); 2 k-block lockstep
+    int sync_window;       // mode 2: max k-blocks ahead of the slowest cluster
+    int sync_every;        // mode 2: check every this many k-blocks
+    unsigned int* done;    // mode 1: completed (cluster, tile) count
+    unsigned int* progress;  // mode 2: issued k-blocks per cluster
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -143,6 +146,9 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 }
 __device__ __forceinline__ void st_stream_u8(uint8_t* p, uint32_t v) {
     asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release(unsigned int* p, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
     unsigned int v;
@@ -310,25 +316,44 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int cluster_id = blockIdx.x / CG, nclusters = gridDim.x / CG;
 
     if (warp == 0) {
-        if (lane == 0) {
-            // ---------------- TMA producer ----------------
-            int stage = 0;
-            uint32_t phase = 0;
-            const uint32_t full0_leader = CG == 2 ? mapa(smem_u32(full), 0) : smem_u32(full);
-            const uint64_t pol = policy_evict_last();
-            int lt = 0;
-            for (int t = cluster_id; t < total; t += nclusters, ++lt) {
-                if (P.sync_slack > 0 && leader && lt >= P.sync_slack) {
-                    // lockstep: every cluster must have finished its tile lt - slack
-                    const unsigned int need = static_cast<unsigned int>(
-                        min(total, (lt - P.sync_slack + 1) * nclusters));
-                    while (ld_acquire(P.done) < need) __nanosleep(256);
+        // ---------------- TMA producer ----------------
+        // lane 0 issues; the whole warp joins the k-block lockstep checks
+        int stage = 0;
+        uint32_t phase = 0;
+        const uint32_t full0_leader = CG == 2 ? mapa(smem_u32(full), 0) : smem_u32(full);
+        const uint64_t pol = policy_evict_last();
+        const bool kstep = P.sync_mode == 2 && leader;
+        int lt = 0;
+        for (int t = cluster_id; t < total; t += nclusters, ++lt) {
+            if (P.sync_mode == 1 && leader && lt >= 1 && lane == 0) {
+                // tile lockstep: every cluster must have finished its tile lt - 1
+                const unsigned int need = static_cast<unsigned int>(min(total, lt * nclusters));
+                while (ld_acquire(P.done) < need) __nanosleep(256);
+            }
+            __syncwarp();
+            int mod, tm, tn;
+            decode_tile(t, P.tiles_m, P.tiles_n, P.group, mod, tm, tn);
+            const int m0 = tm * C::kTileM + static_cast<int>(rank) * C::kBM;
+            const int n0 = tn * C::kTileN + static_cast<int>(rank) * C::kBRows;
+            for (int kb = 0; kb < P.num_kb; ++kb) {
+                if (kstep && (kb % P.sync_every) == 0) {
+                    // k-block lockstep: publish this cluster's issued k-blocks, then
+                    // stay within `window` k-blocks of the slowest cluster
+                    const unsigned int g = static_cast<unsigned int>(lt * P.num_kb + kb);
+                    if (lane == 0) st_release(P.progress + cluster_id, g);
+                    if (g > static_cast<unsigned int>(P.sync_window)) {
+                        const unsigned int target = g - static_cast<unsigned int>(P.sync_window);
+                        while (true) {
+                            unsigned int lo = 0xffffffffu;
+                            for (int cl = lane; cl < nclusters; cl += 32) lo = min(lo, ld_acquire(P.progress + cl));
+#pragma unroll
+                            for (int o = 16; o; o >>= 1) lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+                            if (lo >= target) break;
+                            __nanosleep(128);
+                        }
+                    }
                 }
-                int mod, tm, tn;
-                decode_tile(t, P.tiles_m, P.tiles_n, P.group, mod, tm, tn);
-                const int m0 = tm * C::kTileM + static_cast<int>(rank) * C::kBM;
-                const int n0 = tn * C::kTileN + static_cast<int>(rank) * C::kBRows;
-                for (int kb = 0; kb < P.num_kb; ++kb) {
+                if (lane == 0) {
                     mbar_wait(smem_u32(empty + stage), phase ^ 1);
                     const uint32_t fb = smem_u32(full + stage);
                     if (leader) mbar_arrive_expect_tx(fb, C::kTxBytes);
@@ -352,13 +377,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                             tma_load_3d(dB, &tmB, fb, kb * kBK, n0, mod);
                         }
                     }
-                    if (++stage == C::kStages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                }
+                if (++stage == C::kStages) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
+        if (kstep && lane == 0) st_release(P.progress + cluster_id, 0xffffffffu);  // done: never the minimum
     } else if (warp == 1) {
         if (leader) {
             // ---------------- MMA issuer ----------------
@@ -392,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 if (lane == 0) {
                     mma_commit<CG>(smem_u32(tfull + acc));
-                    if (P.sync_slack > 0) {
+                    if (P.sync_mode == 1) {
                         // all MMAs of this tile are issued and its operands consumed in
                         // order behind the ring, so the tile's loads are done
                         __threadfence();
@@ -548,9 +574,13 @@ int launch_impl(const K2Launch& L, cudaStream_t s) {
     // L2 when the trailing cluster reads them. Measured at 16384^3, N=14: DRAM
     // reads 214 GB -> 57 GB per launch, and the power freed lifts the capped SM
     // clock 1.15 -> 1.48 GHz (profiles/). The counter is per handle.
-    P.sync_slack = L.sync_counter ? env_int("OZK_K2_SYNC", 1) : 0;
+    P.sync_mode = L.sync_counter ? env_int("OZK_K2_SYNC", 1) : 0;
+    P.sync_window = env_int("OZK_K2_SYNC_WINDOW", 32);
+    P.sync_every = env_int("OZK_K2_SYNC_EVERY", 8);
+    if (P.sync_every < 1) P.sync_every = 1;
     P.done = L.sync_counter;
-    if (P.sync_slack > 0) cudaMemsetAsync(P.done, 0, sizeof(unsigned int), s);
+    P.progress = L.sync_counter ? L.sync_counter + 16 : nullptr;
+    if (P.sync_mode > 0) cudaMemsetAsync(P.done, 0, sizeof(unsigned int) * 16 * 16, s);
     const long long total = static_cast<long long>(L.n_mod) * P.tiles_m * P.tiles_n;
     long long clusters = L.num_sms / CG;
     if (clusters > total) clusters = total;
