@@ -326,9 +326,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         int lt = 0;
         for (int t = cluster_id; t < total; t += nclusters, ++lt) {
             if (P.sync_mode == 1 && leader && lt >= 1 && lane == 0) {
-                // tile lockstep: every cluster must have finished its tile lt - 1
+                // tile lockstep: every cluster's producer must have issued its tile
+                // lt - 1. Counting producers (not MMA completion) lets this cluster
+                // keep its ring full while it waits, so the MMA pipe does not drain.
                 const unsigned int need = static_cast<unsigned int>(min(total, lt * nclusters));
-                while (ld_acquire(P.done) < need) __nanosleep(256);
+                while (ld_acquire(P.done) < need) __nanosleep(128);
             }
             __syncwarp();
             int mod, tm, tn;
@@ -383,6 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     phase ^= 1;
                 }
             }
+            if (P.sync_mode == 1 && leader && lane == 0) atomicAdd(P.done, 1u);  // tile lt fully issued
         }
         if (kstep && lane == 0) st_release(P.progress + cluster_id, 0xffffffffu);  // done: never the minimum
     } else if (warp == 1) {
@@ -416,15 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         phase ^= 1;
                     }
                 }
-                if (lane == 0) {
-                    mma_commit<CG>(smem_u32(tfull + acc));
-                    if (P.sync_mode == 1) {
-                        // all MMAs of this tile are issued and its operands consumed in
-                        // order behind the ring, so the tile's loads are done
-                        __threadfence();
-                        atomicAdd(P.done, 1u);
-                    }
-                }
+                if (lane == 0) mma_commit<CG>(smem_u32(tfull + acc));
                 __syncwarp();
             }
         }

@@ -13,11 +13,9 @@ from paper_2508_03984_b200 import Context, EmuConfig  # noqa: E402
 from paper_2508_03984_b200 import _lib  # noqa: E402
 
 VARIANTS = [
-    {"OZK_K2_SYNC": "1"},
-    {"OZK_K2_SYNC": "2", "OZK_K2_SYNC_WINDOW": "16", "OZK_K2_SYNC_EVERY": "4"},
-    {"OZK_K2_SYNC": "2", "OZK_K2_SYNC_WINDOW": "32", "OZK_K2_SYNC_EVERY": "8"},
-    {"OZK_K2_SYNC": "2", "OZK_K2_SYNC_WINDOW": "64", "OZK_K2_SYNC_EVERY": "8"},
-    {"OZK_K2_SYNC": "2", "OZK_K2_SYNC_WINDOW": "128", "OZK_K2_SYNC_EVERY": "16"},
+    {"OZK_K2_SYNC": "1", "OZK_K2_GROUP": "8"},
+    {"OZK_K2_SYNC": "1", "OZK_K2_GROUP": "4"},
+    {"OZK_K2_SYNC": "1", "OZK_K2_GROUP": "12"},
     {"OZK_K2_SYNC": "0"},
 ]
 
