@@ -372,6 +372,19 @@ def main():
                 torch.cuda.synchronize()
                 sweep[f"{md.name.lower()}{N}"] = flop / (s0.elapsed_time(s1) / 2 * 1e-3) / 1e12
         extra["dgemm_sweep_tflops"] = sweep
+        # BLAS transposes (square problem: the stored operands are read as op(X) = X^T)
+        trans = {}
+        for ta, tb in ((False, False), (True, False), (False, True), (True, True)):
+            ctx.gemm(A, B, cfg, C, trans_a=ta, trans_b=tb)
+            torch.cuda.synchronize()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            for _ in range(2):
+                ctx.gemm(A, B, cfg, C, trans_a=ta, trans_b=tb)
+            s1.record(stream)
+            torch.cuda.synchronize()
+            trans["TN"[not ta] + "TN"[not tb]] = flop / (s0.elapsed_time(s1) / 2 * 1e-3) / 1e12
+        extra["transposes_tflops"] = trans
         # accuracy vs native FP64 on a sampled block (emulated vs torch fp64 vs exact-ish fp64 reference)
         extra["accuracy"] = accuracy_probe(ctx, A, B, cfg)
         out["extra"] = extra

@@ -50,6 +50,15 @@ extern "C" {
  * reference's fast mode breaks the CRT range for |x| >= 2 rows/columns. Off by
  * default: results then equal the reference bit for bit. */
 #define OZK_FLAG_FAST_EXPONENT_FIX 1
+/* BLAS transposes (extension; the reference takes op(X) = X only,
+ * emulator.hpp:23-32). C = alpha * op(A) * op(B) + beta * C with op(A) m x k,
+ * op(B) k x n. OZK_FLAG_TRANS_A: A is stored k x m (column-major, lda >= k) and
+ * op(A) = A^T; OZK_FLAG_TRANS_B: B is stored n x k (ldb >= n), op(B) = B^T.
+ * Results equal the reference's gemm_emulated(op(A), op(B)) bit for bit; no
+ * transpose is materialised (the GEMM reads either operand major). The stage
+ * API (ozk_stage_residues / ozk_stage_products) takes untransposed operands. */
+#define OZK_FLAG_TRANS_A 2
+#define OZK_FLAG_TRANS_B 4
 
 /* storage types of A/B/C buffers */
 #define OZK_R64F 0
@@ -125,6 +134,16 @@ int ozk_dgemm(ozk_handle h, int n_moduli, int mode, int64_t m, int64_t n, int64_
               int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
 int ozk_sgemm(ozk_handle h, int n_moduli, int mode, int64_t m, int64_t n, int64_t k, float alpha, const float* A,
               int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc);
+/* cublasDgemm-shaped: transa/transb 'N' or 'T' ('C' == 'T' for real data) */
+int ozk_dgemm_ex(ozk_handle h, int n_moduli, int mode, char transa, char transb, int64_t m, int64_t n, int64_t k,
+                 double alpha, const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+                 int64_t ldc);
+/* Strided batch (cublasGemmStridedBatched shape): problem b uses A + b*stride_a,
+ * B + b*stride_b, C + b*stride_c (elements); each equals ozk_gemm on that
+ * slice. Batch entries run back to back on the handle's stream. */
+int ozk_gemm_strided_batched(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, double alpha,
+                             const void* A, int64_t lda, int64_t stride_a, const void* B, int64_t ldb,
+                             int64_t stride_b, double beta, void* C, int64_t ldc, int64_t stride_c, int64_t batch);
 
 /* ---- column-sharded GEMM (multi-GPU) --------------------------
  * This process computes C[:, shard] = alpha * A * B[:, shard] + beta * C[:, shard]

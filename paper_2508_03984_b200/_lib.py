@@ -19,6 +19,8 @@ OZK_FAST, OZK_ACCURATE = 0, 1
 OZK_R64F, OZK_R32F = 0, 1
 OZK_PRODUCTS_I32, OZK_PRODUCTS_U8 = 0, 1
 OZK_FLAG_FAST_EXPONENT_FIX = 1
+OZK_FLAG_TRANS_A = 2
+OZK_FLAG_TRANS_B = 4
 MAX_MODULI = 20
 ENGINE_MAX_K = 1 << 17
 
@@ -26,7 +28,7 @@ ENGINE_MAX_K = 1 << 17
 EXPORTED_SYMBOLS = (
     "ozk_create", "ozk_destroy", "ozk_set_stream", "ozk_last_error", "ozk_version", "ozk_default_config",
     "ozk_select_moduli", "ozk_mod_inverse", "ozk_build_constants", "ozk_dump_tables_csv",
-    "ozk_gemm", "ozk_gemm_host", "ozk_dgemm", "ozk_sgemm",
+    "ozk_gemm", "ozk_gemm_host", "ozk_dgemm", "ozk_sgemm", "ozk_dgemm_ex", "ozk_gemm_strided_batched",
     "ozk_stage_scale", "ozk_plane_ld", "ozk_stage_residues", "ozk_stage_products", "ozk_stage_reconstruct",
     "ozk_kernel_launches", "ozk_profile", "ozk_profile_read",
     "ozk_shard_begin", "ozk_shard_rowmax", "ozk_shard_end",
@@ -113,6 +115,10 @@ def load() -> C.CDLL:
     L.ozk_gemm_host.argtypes = gemm_args
     L.ozk_dgemm.argtypes = [p, i32, i32, i64, i64, i64, C.c_double, p, i64, p, i64, C.c_double, p, i64]
     L.ozk_sgemm.argtypes = [p, i32, i32, i64, i64, i64, C.c_float, p, i64, p, i64, C.c_float, p, i64]
+    L.ozk_dgemm_ex.argtypes = [p, i32, i32, C.c_char, C.c_char, i64, i64, i64, C.c_double, p, i64, p, i64,
+                               C.c_double, p, i64]
+    L.ozk_gemm_strided_batched.argtypes = [p, C.POINTER(OzkConfig), i64, i64, i64, C.c_double, p, i64, i64, p, i64, i64,
+                                           C.c_double, p, i64, i64, i64]
     L.ozk_stage_scale.argtypes = [p, C.POINTER(OzkConfig), i64, i64, i64, p, i64, p, i64, p, p]
     L.ozk_plane_ld.restype = i64
     L.ozk_plane_ld.argtypes = [i64]

@@ -74,7 +74,13 @@ struct Job {
     ozk_constants c;
     DevConsts dc;
     int mode;
-    int64_t m, n, k, ld, lda_p, ldu;  // ld: B plane pitch (k), lda_p: A plane pitch (m)
+    int64_t m, n, k, ldu;
+    // op(A) / op(B) storage: ta -> A is k x m, tb -> B is n x k (column-major, BLAS 'T').
+    // Planes follow the storage, so no transpose is ever materialised:
+    //   A: !ta MN-major [N][k][lda_p = ld(m)],  ta K-major [N][m][lda_p = ld(k)]
+    //   B: !tb K-major  [N][n][ld = ld(k)],     tb MN-major [N][k][ld = ld(n)]
+    bool ta, tb;
+    int64_t ld, lda_p, pa_stride, pb_stride;
     const void* a;  // device operands as the kernels read them
     const void* b;
     int64_t lda, ldb;
@@ -82,7 +88,7 @@ struct Job {
     int32_t *mu, *nu, *ma, *nb, *rowmax, *colmax, *flag_rows, *flag_cols;
     int32_t* flags;  // [0] non-finite, [1] flagged rows, [2] flagged columns, [4..] K2 lockstep words (1 KB)
     double *amax, *asum, *bmax, *bsum;
-    int splits;
+    int splits, splits_b;  // k-partials of the row-stat reductions of op(A) (!ta) / op(B) (tb)
     int8_t *pa, *pb;
     uint8_t* u;
 };
@@ -194,7 +200,8 @@ int validate(const ozk_config* cfg, const ozk_constants& c, int64_t m, int64_t n
         set_error("gemm_emulated: block_k must be in [1, 2^17]");
         return OZK_CONFIG_ERROR;
     }
-    if (lda < m || ldb < k) {
+    const bool ta = (cfg->flags & OZK_FLAG_TRANS_A) != 0, tb = (cfg->flags & OZK_FLAG_TRANS_B) != 0;
+    if (lda < (ta ? k : m) || ldb < (tb ? n : k)) {
         set_error("gemm_emulated: leading dimension smaller than the matrix");
         return OZK_INPUT_ERROR;
     }
@@ -225,28 +232,33 @@ int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c,
     J.m = m;
     J.n = n;
     J.k = k;
-    J.ld = plane_ld(k);
-    J.lda_p = plane_ld(m);
+    J.ta = (cfg->flags & OZK_FLAG_TRANS_A) != 0;
+    J.tb = (cfg->flags & OZK_FLAG_TRANS_B) != 0;
+    J.lda_p = J.ta ? plane_ld(k) : plane_ld(m);
+    J.pa_stride = J.ta ? m * J.lda_p : k * J.lda_p;
+    J.ld = J.tb ? plane_ld(n) : plane_ld(k);
+    J.pb_stride = J.tb ? k * J.ld : n * J.ld;
     J.ldu = u_ld(m);
     const int N = c.n_moduli;
-    J.splits = row_stats_splits(m, k);
+    J.splits = J.ta ? 1 : row_stats_splits(m, k);
+    J.splits_b = J.tb ? row_stats_splits(n, k) : 1;
     OZK_TRY(ensure(h->flags, 2048));
-    OZK_TRY(ensure(h->stats, sizeof(double) * (2 * J.splits * m + 2 * n)));
+    OZK_TRY(ensure(h->stats, sizeof(double) * (2 * J.splits * m + 2 * J.splits_b * n)));
     OZK_TRY(ensure(h->ints, sizeof(int32_t) * 4 * (m + n)));
     if (need_products) {
-        OZK_TRY(ensure(h->planes_a, static_cast<size_t>(N * k * J.lda_p)));
-        OZK_TRY(ensure(h->planes_b, static_cast<size_t>(N * n * J.ld)));
+        OZK_TRY(ensure(h->planes_a, static_cast<size_t>(N * J.pa_stride)));
+        OZK_TRY(ensure(h->planes_b, static_cast<size_t>(N * J.pb_stride)));
         OZK_TRY(ensure(h->u, static_cast<size_t>(N * n * J.ldu)));
     } else if (cfg->mode == OZK_ACCURATE) {  // the bound operands Abar/Bbar
-        OZK_TRY(ensure(h->planes_a, static_cast<size_t>(k * J.lda_p)));
-        OZK_TRY(ensure(h->planes_b, static_cast<size_t>(n * J.ld)));
+        OZK_TRY(ensure(h->planes_a, static_cast<size_t>(J.pa_stride)));
+        OZK_TRY(ensure(h->planes_b, static_cast<size_t>(J.pb_stride)));
     }
     J.flags = static_cast<int32_t*>(h->flags.p);
     double* d = static_cast<double*>(h->stats.p);
     J.amax = d;
     J.asum = d + J.splits * m;
     J.bmax = d + 2 * J.splits * m;
-    J.bsum = J.bmax + n;
+    J.bsum = J.bmax + J.splits_b * n;
     int32_t* p = static_cast<int32_t*>(h->ints.p);
     J.mu = p;
     J.nu = J.mu + m;
@@ -277,43 +289,82 @@ bool rounds_inputs(const Job& J, const ozk_config* cfg) {
 int round_a(ozk_context* h, Job& J, const ozk_config* cfg) {
     if (!rounds_inputs(J, cfg)) return OZK_OK;
     OZK_TRY(ensure(h->f32a, sizeof(float) * J.m * J.k));
-    launch_round_to_f32(static_cast<const double*>(J.a), J.m, J.k, J.lda, static_cast<float*>(h->f32a.p), h->stream);
+    const int64_t rows = J.ta ? J.k : J.m, cols = J.ta ? J.m : J.k;
+    launch_round_to_f32(static_cast<const double*>(J.a), rows, cols, J.lda, static_cast<float*>(h->f32a.p), rows,
+                        h->stream);
     J.a = h->f32a.p;
-    J.lda = J.m;
+    J.lda = rows;
     J.in_f32 = 1;
     return check_launch(h, 1);
 }
 
-// B is rounded block by block into a k x n FP32 staging buffer; src keeps the
-// caller's FP64 view for the later blocks
+// B is rounded block by block into a k x n (tb: n x k) FP32 staging buffer;
+// src keeps the caller's FP64 view for the later blocks
 int round_b(ozk_context* h, Job& J, const ozk_config* cfg, const void* src, int64_t src_ld, int64_t j0, int64_t nj) {
     if (!rounds_inputs(J, cfg)) return OZK_OK;
     OZK_TRY(ensure(h->f32b, sizeof(float) * J.k * J.n));
-    launch_round_to_f32(static_cast<const double*>(src) + j0 * src_ld, J.k, nj, src_ld,
-                        static_cast<float*>(h->f32b.p) + j0 * J.k, h->stream);
+    float* dst = static_cast<float*>(h->f32b.p);
+    if (J.tb)
+        launch_round_to_f32(static_cast<const double*>(src) + j0, nj, J.k, src_ld, dst + j0, J.n, h->stream);
+    else
+        launch_round_to_f32(static_cast<const double*>(src) + j0 * src_ld, J.k, nj, src_ld, dst + j0 * J.k, J.k,
+                            h->stream);
     J.b = h->f32b.p;
-    J.ldb = J.k;
+    J.ldb = J.tb ? J.n : J.k;
     J.in_f32 = 1;
     return check_launch(h, 1);
 }
 
+// first element of op(B)'s column j0 (tb: row j0 of the stored n x k B)
 const void* b_block(const Job& J, int64_t j0) {
-    return J.in_f32 ? static_cast<const void*>(static_cast<const float*>(J.b) + j0 * J.ldb)
-                    : static_cast<const void*>(static_cast<const double*>(J.b) + j0 * J.ldb);
+    const int64_t off = J.tb ? j0 : j0 * J.ldb;
+    return J.in_f32 ? static_cast<const void*>(static_cast<const float*>(J.b) + off)
+                    : static_cast<const void*>(static_cast<const double*>(J.b) + off);
+}
+
+// byte offset of op(B)'s column j0 inside a B plane
+int64_t b_plane_off(const Job& J, int64_t j0) { return J.tb ? j0 : j0 * J.ld; }
+
+// op(A)'s rows: row stats over A's rows, or column stats over the stored k x m A^T
+void a_line_stats(ozk_context* h, Job& J) {
+    if (J.ta)
+        launch_col_stats(J.a, J.in_f32, J.k, J.m, J.lda, J.amax, J.asum, J.flags, h->stream);
+    else
+        launch_row_stats(J.a, J.in_f32, J.m, J.k, J.lda, J.splits, J.amax, J.asum, J.flags, h->stream);
+}
+
+// residues (kind 0) or the bound plane (kind 1) of op(A), in the layout K2 reads
+void a_planes(ozk_context* h, Job& J, const int32_t* mu, int kind, int8_t* pa, int64_t stride) {
+    if (J.ta)  // K-major: column i of the stored A^T is row i of op(A), scaled by mu[i]
+        launch_b_planes(J.a, J.in_f32, J.k, J.m, J.lda, mu, J.dc, kind, pa, J.lda_p, stride, h->stream);
+    else
+        launch_a_planes(J.a, J.in_f32, J.m, J.k, J.lda, mu, J.dc, kind, pa, J.lda_p, stride, h->stream);
+}
+
+// op(B) columns [j0, j0+nj): planes at b_plane_off(j0)
+void b_planes(ozk_context* h, Job& J, int64_t j0, int64_t nj, const int32_t* nu, int kind, int8_t* pb,
+              int64_t stride) {
+    if (J.tb)  // MN-major: row j of the stored B^T is column j of op(B), scaled by nu[j]
+        launch_a_planes(b_block(J, j0), J.in_f32, nj, J.k, J.ldb, nu + j0, J.dc, kind, pb + b_plane_off(J, j0), J.ld,
+                        stride, h->stream);
+    else
+        launch_b_planes(b_block(J, j0), J.in_f32, J.k, nj, J.ldb, nu + j0, J.dc, kind, pb + b_plane_off(J, j0), J.ld,
+                        stride, h->stream);
 }
 
 // ---- stages ----------------------------------------------------------------------
 // rows of A: stats, and fast-mode mu (or accurate-mode mu' + the Abar plane)
 int stage_rows(ozk_context* h, Job& J) {
-    launch_row_stats(J.a, J.in_f32, J.m, J.k, J.lda, J.splits, J.amax, J.asum, J.flags, h->stream);
+    a_line_stats(h, J);
     OZK_TRY(check_launch(h, 1));
     if (J.mode == OZK_FAST) {
         launch_fast_finalize(J.amax, J.asum, J.splits, J.m, J.k, J.dc, J.mu, J.flags + 1, J.flag_rows, h->stream);
-        launch_fast_exact(J.a, J.in_f32, 1, J.lda, J.k, J.dc, J.flags + 1, J.flag_rows, J.mu, h->stream);
+        launch_fast_exact(J.a, J.in_f32, J.ta ? J.lda : 1, J.ta ? 1 : J.lda, J.k, J.dc, J.flags + 1, J.flag_rows,
+                          J.mu, h->stream);
         return check_launch(h, 2);
     }
     launch_accurate_base(J.amax, J.splits, J.m, J.ma, h->stream);
-    launch_a_planes(J.a, J.in_f32, J.m, J.k, J.lda, J.ma, J.dc, 1, J.pa, J.lda_p, J.k * J.lda_p, h->stream);
+    a_planes(h, J, J.ma, 1, J.pa, J.pa_stride);
     OZK_CUDA(cudaMemsetAsync(J.rowmax, 0, sizeof(int32_t) * J.m, h->stream));
     return check_launch(h, 2);
 }
@@ -322,17 +373,23 @@ int stage_rows(ozk_context* h, Job& J) {
 // Bbar block and the bound GEMM Abar * Bbar_block (row maxima accumulate)
 int stage_cols(ozk_context* h, Job& J, int64_t j0, int64_t nj) {
     const void* bj = b_block(J, j0);
-    launch_col_stats(bj, J.in_f32, J.k, nj, J.ldb, J.bmax + j0, J.bsum + j0, J.flags, h->stream);
+    // this block's [split][nj] partials
+    double* bmax = J.bmax + J.splits_b * j0;
+    double* bsum = J.bsum + J.splits_b * j0;
+    if (J.tb)
+        launch_row_stats(bj, J.in_f32, nj, J.k, J.ldb, J.splits_b, bmax, bsum, J.flags, h->stream);
+    else
+        launch_col_stats(bj, J.in_f32, J.k, nj, J.ldb, bmax, bsum, J.flags, h->stream);
     OZK_TRY(check_launch(h, 1));
     if (J.mode == OZK_FAST) {
-        launch_fast_finalize(J.bmax + j0, J.bsum + j0, 1, nj, J.k, J.dc, J.nu + j0, J.flags + 2, J.flag_cols,
-                             h->stream);
-        launch_fast_exact(bj, J.in_f32, J.ldb, 1, J.k, J.dc, J.flags + 2, J.flag_cols, J.nu + j0, h->stream);
+        launch_fast_finalize(bmax, bsum, J.splits_b, nj, J.k, J.dc, J.nu + j0, J.flags + 2, J.flag_cols, h->stream);
+        launch_fast_exact(bj, J.in_f32, J.tb ? 1 : J.ldb, J.tb ? J.ldb : 1, J.k, J.dc, J.flags + 2, J.flag_cols,
+                          J.nu + j0, h->stream);
         return check_launch(h, 2);
     }
-    launch_accurate_base(J.bmax + j0, 1, nj, J.nb + j0, h->stream);
-    int8_t* bbar = J.pb + j0 * J.ld;
-    launch_b_planes(bj, J.in_f32, J.k, nj, J.ldb, J.nb + j0, J.dc, 1, bbar, J.ld, J.n * J.ld, h->stream);
+    launch_accurate_base(bmax, J.splits_b, nj, J.nb + j0, h->stream);
+    int8_t* bbar = J.pb + b_plane_off(J, j0);
+    b_planes(h, J, j0, nj, J.nb, 1, J.pb, J.pb_stride);
     OZK_CUDA(cudaMemsetAsync(J.colmax + j0, 0, sizeof(int32_t) * nj, h->stream));
     OZK_TRY(check_launch(h, 2));
     K2Launch L{};
@@ -343,8 +400,10 @@ int stage_cols(ozk_context* h, Job& J, int64_t j0, int64_t nj) {
     L.k = J.k;
     L.ld = J.ld;
     L.lda = J.lda_p;
-    L.a_stride = J.k * J.lda_p;
-    L.b_stride = J.n * J.ld;
+    L.a_mn = !J.ta;
+    L.b_mn = J.tb;
+    L.a_stride = J.pa_stride;
+    L.b_stride = J.pb_stride;
     L.n_mod = 1;
     L.kind = K2_MAX;
     L.rowmax = J.rowmax;
@@ -364,14 +423,13 @@ int stage_budget(ozk_context* h, Job& J) {
 }
 
 int stage_row_residues(ozk_context* h, Job& J, const int32_t* mu, int8_t* pa) {
-    launch_a_planes(J.a, J.in_f32, J.m, J.k, J.lda, mu, J.dc, 0, pa, J.lda_p, J.k * J.lda_p, h->stream);
+    a_planes(h, J, mu, 0, pa, J.pa_stride);
     return check_launch(h, 1);
 }
 
 int stage_col_residues(ozk_context* h, Job& J, int64_t j0, int64_t nj, const int32_t* nu, int8_t* pb,
                        int64_t pb_stride) {
-    launch_b_planes(b_block(J, j0), J.in_f32, J.k, nj, J.ldb, nu + j0, J.dc, 0, pb + j0 * J.ld, J.ld, pb_stride,
-                    h->stream);
+    b_planes(h, J, j0, nj, nu, 0, pb, pb_stride);
     return check_launch(h, 1);
 }
 
@@ -379,12 +437,14 @@ int stage_products(ozk_context* h, Job& J, int64_t j0, int64_t nj, const int8_t*
                    const int8_t* pb, int64_t pb_stride, int kind, void* out, int64_t ldo, int64_t out_stride) {
     K2Launch L{};
     L.a_planes = pa;
-    L.b_planes = pb + j0 * J.ld;
+    L.b_planes = pb + b_plane_off(J, j0);
     L.m = J.m;
     L.n = nj;
     L.k = J.k;
     L.ld = J.ld;
     L.lda = J.lda_p;
+    L.a_mn = !J.ta;
+    L.b_mn = J.tb;
     L.a_stride = pa_stride;
     L.b_stride = pb_stride;
     L.n_mod = J.c.n_moduli;
@@ -416,11 +476,11 @@ int compute_block(ozk_context* h, Job& J, int64_t j0, int64_t nj, double alpha, 
                   int c_f32) {
     {
         StageTimer t(h, OZK_PROFILE_RESIDUES);
-        OZK_TRY(stage_col_residues(h, J, j0, nj, J.nu, J.pb, J.n * J.ld));
+        OZK_TRY(stage_col_residues(h, J, j0, nj, J.nu, J.pb, J.pb_stride));
     }
     {
         StageTimer t(h, OZK_PROFILE_PRODUCTS);
-        OZK_TRY(stage_products(h, J, j0, nj, J.pa, J.k * J.lda_p, J.pb, J.n * J.ld, OZK_PRODUCTS_U8, J.u, J.ldu,
+        OZK_TRY(stage_products(h, J, j0, nj, J.pa, J.pa_stride, J.pb, J.pb_stride, OZK_PRODUCTS_U8, J.u, J.ldu,
                                J.n * J.ldu));
     }
     StageTimer t(h, OZK_PROFILE_RECONSTRUCT);
@@ -498,8 +558,10 @@ int gemm_host(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int
     if (!h->h2d) OZK_CUDA(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
     if (!h->d2h) OZK_CUDA(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
     const size_t es = cfg->a_type == OZK_R32F ? 4 : 8, cs = cfg->c_type == OZK_R32F ? 4 : 8;
-    OZK_TRY(ensure(h->host_a, es * lda * k));
-    OZK_TRY(ensure(h->host_b, es * ldb * n));
+    const bool ta = (cfg->flags & OZK_FLAG_TRANS_A) != 0, tb = (cfg->flags & OZK_FLAG_TRANS_B) != 0;
+    const size_t a_bytes = es * lda * (ta ? m : k);
+    OZK_TRY(ensure(h->host_a, a_bytes));
+    OZK_TRY(ensure(h->host_b, es * ldb * (tb ? k : n)));
     OZK_TRY(ensure(h->host_c, cs * ldc * n));
     Job J{};
     OZK_TRY(setup(h, J, cfg, c, m, n, k, h->host_a.p, lda, h->host_b.p, ldb, true));
@@ -526,14 +588,19 @@ int gemm_host(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int
     OZK_CUDA(cudaEventRecord(evStart, h->stream));
     OZK_CUDA(cudaStreamWaitEvent(h->h2d, evStart, 0));
     OZK_CUDA(cudaStreamWaitEvent(h->d2h, evStart, 0));
-    OZK_CUDA(cudaMemcpyAsync(h->host_a.p, A, es * lda * k, cudaMemcpyHostToDevice, h->h2d));
+    OZK_CUDA(cudaMemcpyAsync(h->host_a.p, A, a_bytes, cudaMemcpyHostToDevice, h->h2d));
     OZK_CUDA(cudaEventRecord(evA, h->h2d));
     for (int b = 0; b < nblk; ++b) {
         int64_t j0, nj;
         block(b, j0, nj);
-        OZK_CUDA(cudaMemcpyAsync(static_cast<char*>(h->host_b.p) + es * ldb * j0,
-                                 static_cast<const char*>(B) + es * ldb * j0, es * ldb * nj, cudaMemcpyHostToDevice,
-                                 h->h2d));
+        if (tb)  // op(B) columns = rows j0.. of the stored n x k B: a pitched copy
+            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(h->host_b.p) + es * j0, es * ldb,
+                                       static_cast<const char*>(B) + es * j0, es * ldb, es * nj, k,
+                                       cudaMemcpyHostToDevice, h->h2d));
+        else
+            OZK_CUDA(cudaMemcpyAsync(static_cast<char*>(h->host_b.p) + es * ldb * j0,
+                                     static_cast<const char*>(B) + es * ldb * j0, es * ldb * nj,
+                                     cudaMemcpyHostToDevice, h->h2d));
         if (beta != 0.0)
             OZK_CUDA(cudaMemcpyAsync(static_cast<char*>(h->host_c.p) + cs * ldc * j0,
                                      static_cast<const char*>(C) + cs * ldc * j0, cs * ldc * nj,
@@ -722,6 +789,43 @@ int ozk_sgemm(ozk_handle h, int n_moduli, int mode, int64_t m, int64_t n, int64_
     return ozk_gemm(h, &cfg, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 
+int ozk_dgemm_ex(ozk_handle h, int n_moduli, int mode, char transa, char transb, int64_t m, int64_t n, int64_t k,
+                 double alpha, const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+                 int64_t ldc) {
+    auto flag = [](char t, int bit, int32_t& f) {
+        if (t == 'N' || t == 'n') return true;
+        if (t == 'T' || t == 't' || t == 'C' || t == 'c') {
+            f |= bit;
+            return true;
+        }
+        return false;
+    };
+    ozk_config cfg = ozk_default_config(n_moduli, mode, OZK_FP64);
+    if (!flag(transa, OZK_FLAG_TRANS_A, cfg.flags) || !flag(transb, OZK_FLAG_TRANS_B, cfg.flags)) {
+        set_error("ozk_dgemm_ex: trans must be 'N' or 'T'");
+        return OZK_CONFIG_ERROR;
+    }
+    return ozk_gemm(h, &cfg, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+}
+
+int ozk_gemm_strided_batched(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, double alpha,
+                             const void* A, int64_t lda, int64_t stride_a, const void* B, int64_t ldb,
+                             int64_t stride_b, double beta, void* C, int64_t ldc, int64_t stride_c, int64_t batch) {
+    if (!h) return OZK_INPUT_ERROR;
+    if (batch < 0) {
+        set_error("ozk_gemm_strided_batched: negative batch");
+        return OZK_INPUT_ERROR;
+    }
+    ozk_constants c;
+    OZK_TRY(resolve(cfg, c));  // the table is built once for the batch
+    const size_t ea = cfg->a_type == OZK_R32F ? 4 : 8, ec = cfg->c_type == OZK_R32F ? 4 : 8;
+    for (int64_t b = 0; b < batch; ++b)
+        OZK_TRY(gemm_device(h, cfg, c, m, n, k, alpha, static_cast<const char*>(A) + ea * stride_a * b, lda,
+                            static_cast<const char*>(B) + ea * stride_b * b, ldb, beta,
+                            static_cast<char*>(C) + ec * stride_c * b, ldc));
+    return OZK_OK;
+}
+
 int ozk_shard_begin(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, const void* A,
                     int64_t lda, const void* B, int64_t ldb) {
     if (!h) return OZK_INPUT_ERROR;
@@ -799,13 +903,17 @@ int ozk_stage_residues(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n
     OZK_TRY(resolve(cfg, c));
     OZK_TRY(validate(cfg, c, m, n, k, lda, ldb));
     OZK_CUDA(cudaSetDevice(h->device));
+    if (cfg->flags & (OZK_FLAG_TRANS_A | OZK_FLAG_TRANS_B)) {
+        set_error("ozk_stage_residues: the stage API takes untransposed operands");
+        return OZK_CONFIG_ERROR;
+    }
     Job J{};
     OZK_TRY(setup(h, J, cfg, c, m, n, k, A, lda, B, ldb, false));
     const void* b_src = J.b;
     OZK_TRY(round_a(h, J, cfg));
     OZK_TRY(round_b(h, J, cfg, b_src, ldb, 0, n));
     OZK_TRY(stage_row_residues(h, J, mu_exp, a_planes));
-    OZK_TRY(stage_col_residues(h, J, 0, n, nu_exp, b_planes, n * J.ld));
+    OZK_TRY(stage_col_residues(h, J, 0, n, nu_exp, b_planes, J.pb_stride));
     OZK_CUDA(cudaStreamSynchronize(h->stream));
     return OZK_OK;
 }

@@ -45,7 +45,7 @@ __device__ __forceinline__ uint32_t literal_byte(T x, const DevConsts& c, int t)
 template <typename T, int KIND, bool ROW_EXP>
 __global__ void __launch_bounds__(128)
     planes_kernel(const T* __restrict__ b, int64_t k, int64_t n, int64_t ldb, const int32_t* __restrict__ exps,
-                  const DevConsts c, int8_t* __restrict__ planes, int64_t ld, int64_t plane_stride) {
+                  const DevConsts c, int8_t* __restrict__ planes, int64_t ld, int64_t plane_stride, int64_t extent) {
     __shared__ double s_pinv[OZK_MAX_MODULI];
     __shared__ uint32_t s_p[OZK_MAX_MODULI];
     if (threadIdx.x < OZK_MAX_MODULI) {
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(128)
     }
     const int64_t j = blockIdx.x;
     const int64_t i0 = (static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x) * kBPerThread;
-    const bool active = i0 < ld;
+    const bool active = i0 < extent;  // rows up to plane_ld(rows): the zero padding K2's 16-byte rows need
     const int e = ROW_EXP ? 0 : exps[j];
     const T* col = b + j * ldb;
     T x[kBPerThread];
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(128)
     }
     fast = __all_sync(0xffffffffu, fast);
     __syncthreads();  // s_p / s_pinv
-    // ld is a multiple of 16, so a thread's 8 bytes are either all in [0, ld) or all past it
+    // extent is a multiple of 16, so a thread's 8 bytes are either all in [0, extent) or all past it
     if (!active) return;
     int8_t* dst0 = planes + j * ld + i0;
     if constexpr (KIND == 1) {
@@ -124,25 +124,29 @@ __global__ void __launch_bounds__(128)
 }
 
 __global__ void round_to_f32_kernel(const double* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,
-                                    float* __restrict__ out) {
+                                    float* __restrict__ out, int64_t ldo) {
     const int64_t total = rows * cols;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t i = e % rows, j = e / rows;
-        out[e] = __double2float_rn(x[i + j * ld]);
+        out[i + j * ldo] = __double2float_rn(x[i + j * ld]);
     }
 }
 
 template <int KIND, bool ROW_EXP>
 void planes_dispatch(const void* x, int is_f32, int64_t rows, int64_t cols, int64_t ldx, const int32_t* exps,
                      const DevConsts& c, int8_t* planes, int64_t ld, int64_t stride, cudaStream_t s) {
-    dim3 grid(static_cast<unsigned>(cols), static_cast<unsigned>((ld + 128 * kBPerThread - 1) / (128 * kBPerThread)));
+    // only rows [0, plane_ld(rows)) are written: a column block of an MN-major
+    // plane (ld > rows) must not touch its neighbours
+    const int64_t extent = plane_ld(rows);
+    dim3 grid(static_cast<unsigned>(cols),
+              static_cast<unsigned>((extent + 128 * kBPerThread - 1) / (128 * kBPerThread)));
     if (is_f32)
         planes_kernel<float, KIND, ROW_EXP><<<grid, 128, 0, s>>>(static_cast<const float*>(x), rows, cols, ldx, exps,
-                                                                 c, planes, ld, stride);
+                                                                 c, planes, ld, stride, extent);
     else
         planes_kernel<double, KIND, ROW_EXP><<<grid, 128, 0, s>>>(static_cast<const double*>(x), rows, cols, ldx,
-                                                                  exps, c, planes, ld, stride);
+                                                                  exps, c, planes, ld, stride, extent);
 }
 
 }  // namespace
@@ -165,8 +169,9 @@ void launch_b_planes(const void* b, int is_f32, int64_t k, int64_t n, int64_t ld
         planes_dispatch<1, false>(b, is_f32, k, n, ldb, col_exp, c, planes, ld, plane_stride, s);
 }
 
-void launch_round_to_f32(const double* x, int64_t rows, int64_t cols, int64_t ld, float* out, cudaStream_t s) {
-    round_to_f32_kernel<<<148 * 8, 256, 0, s>>>(x, rows, cols, ld, out);
+void launch_round_to_f32(const double* x, int64_t rows, int64_t cols, int64_t ld, float* out, int64_t ldo,
+                         cudaStream_t s) {
+    round_to_f32_kernel<<<148 * 8, 256, 0, s>>>(x, rows, cols, ld, out, ldo);
 }
 
 }  // namespace ozk

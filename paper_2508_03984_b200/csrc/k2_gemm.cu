@@ -231,11 +231,12 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_byt
            (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
            (static_cast<uint64_t>(2) << 61);
 }
-// Instruction descriptor: s8 x s8 -> s32, A MN-major (bit 15), B K-major, no saturate.
-template <int CG>
+// Instruction descriptor: s8 x s8 -> s32, operand majors (bit 15 A, bit 16 B;
+// 1 = MN-major), no saturate.
+template <int CG, bool A_MN, bool B_MN>
 __host__ __device__ constexpr uint32_t idesc_i8() {
-    return (2u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (static_cast<uint32_t>(Cfg<CG>::kTileN >> 3) << 17) |
-           (static_cast<uint32_t>(Cfg<CG>::kTileM >> 4) << 24);
+    return (2u << 4) | (1u << 7) | (1u << 10) | (A_MN ? (1u << 15) : 0u) | (B_MN ? (1u << 16) : 0u) |
+           (static_cast<uint32_t>(Cfg<CG>::kTileN >> 3) << 17) | (static_cast<uint32_t>(Cfg<CG>::kTileM >> 4) << 24);
 }
 
 // work item t -> (modulus, tile row, tile column), grouped raster of 8 tile
@@ -269,7 +270,10 @@ __device__ __forceinline__ int32_t column_max_scatter(uint32_t (&v)[32], int lan
     return static_cast<int32_t>(v[0]);
 }
 
-template <int CG, int KIND>
+// A_MN / B_MN: operand stored MN-major (A: column-major A; B: column-major B^T)
+// or K-major (A: column-major A^T; B: column-major B). Both majors are native
+// tcgen05 int8 operand forms, so the BLAS transposes cost nothing here.
+template <int CG, int KIND, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     residue_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const K2Params P) {
@@ -361,23 +365,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (leader) mbar_arrive_expect_tx(fb, C::kTxBytes);
                     const uint32_t dA = smem_u32(sA + stage * C::kStageA);
                     const uint32_t dB = smem_u32(sB + stage * C::kStageB);
+                    // coordinates: MN-major maps are (mn, k), K-major maps (k, mn)
+                    const int ac0 = A_MN ? m0 : kb * kBK, ac1 = A_MN ? kb * kBK : m0;
+                    const int bc0 = B_MN ? n0 : kb * kBK, bc1 = B_MN ? kb * kBK : n0;
+                    constexpr int kBBoxes = (B_MN && C::kBRows > 128) ? C::kBRows / 128 : 1;
                     if constexpr (CG == 2) {
                         const uint32_t lb = full0_leader + 8u * stage;
                         if (P.hints) {
-                            tma_load_3d_2sm_hint(dA, &tmA, lb, m0, kb * kBK, mod, pol);
-                            tma_load_3d_2sm_hint(dB, &tmB, lb, kb * kBK, n0, mod, pol);
+                            tma_load_3d_2sm_hint(dA, &tmA, lb, ac0, ac1, mod, pol);
+                            tma_load_3d_2sm_hint(dB, &tmB, lb, bc0, bc1, mod, pol);
                         } else {
-                            tma_load_3d_2sm(dA, &tmA, lb, m0, kb * kBK, mod);
-                            tma_load_3d_2sm(dB, &tmB, lb, kb * kBK, n0, mod);
+                            tma_load_3d_2sm(dA, &tmA, lb, ac0, ac1, mod);
+                            tma_load_3d_2sm(dB, &tmB, lb, bc0, bc1, mod);
                         }
                     } else {
-                        if (P.hints) {
-                            tma_load_3d_hint(dA, &tmA, fb, m0, kb * kBK, mod, pol);
-                            tma_load_3d_hint(dB, &tmB, fb, kb * kBK, n0, mod, pol);
-                        } else {
-                            tma_load_3d(dA, &tmA, fb, m0, kb * kBK, mod);
-                            tma_load_3d(dB, &tmB, fb, kb * kBK, n0, mod);
-                        }
+                        tma_load_3d(dA, &tmA, fb, ac0, ac1, mod);
+#pragma unroll
+                        for (int bx = 0; bx < kBBoxes; ++bx)  // MN atoms 16 KB apart (the descriptor's LBO)
+                            tma_load_3d(dB + bx * 16384, &tmB, fb, bc0 + bx * 128, bc1, mod);
                     }
                 }
                 if (++stage == C::kStages) {
@@ -391,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         if (leader) {
             // ---------------- MMA issuer ----------------
-            constexpr uint32_t idesc = idesc_i8<CG>();
+            constexpr uint32_t idesc = idesc_i8<CG, A_MN, B_MN>();
             int stage = 0;
             uint32_t phase = 0;
             int lt = 0;
@@ -408,9 +413,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t a0 = smem_u32(sA + stage * C::kStageA);
                         const uint32_t b0 = smem_u32(sB + stage * C::kStageB);
 #pragma unroll
-                        for (int kk = 0; kk < kBK / 32; ++kk)
-                            mma_i8<CG>(d_tmem, sdesc_sw128(a0 + kk * 32 * kBK, 16384), sdesc_sw128(b0 + kk * 32, 16),
-                                       idesc, (kb | kk) != 0);
+                        for (int kk = 0; kk < kBK / 32; ++kk) {
+                            // MN-major: a 32-k step is 32 rows = 4 swizzle atoms (4096 B);
+                            // atoms along MN are 16 KB apart (LBO). K-major: 32 B inside the atom.
+                            const uint64_t da = A_MN ? sdesc_sw128(a0 + kk * 32 * kBK, 16384)
+                                                     : sdesc_sw128(a0 + kk * 32, 16);
+                            const uint64_t db = B_MN ? sdesc_sw128(b0 + kk * 32 * kBK, 16384)
+                                                     : sdesc_sw128(b0 + kk * 32, 16);
+                            mma_i8<CG>(d_tmem, da, db, idesc, (kb | kk) != 0);
+                        }
                         mma_commit<CG>(smem_u32(empty + stage));
                     }
                     __syncwarp();
@@ -535,13 +546,18 @@ bool make_plane_map(CUtensorMap* map, const int8_t* base, int64_t inner, int64_t
     return r == CUDA_SUCCESS;
 }
 
-template <int CG, int KIND>
+template <int CG, int KIND, bool A_MN, bool B_MN>
 int launch_impl(const K2Launch& L, cudaStream_t s) {
     using C = Cfg<CG>;
     CUtensorMap ma, mb;
-    // A: MN-major (m inner, k columns, box 128 m x 128 k); B: K-major (k inner, n columns)
-    if (!make_plane_map(&ma, L.a_planes, L.m, L.k, L.lda, L.a_stride, L.n_mod, kBK) ||
-        !make_plane_map(&mb, L.b_planes, L.k, L.n, L.ld, L.b_stride, L.n_mod, C::kBRows)) {
+    // MN-major planes: mn inner, k columns, box 128 mn x 128 k; K-major planes:
+    // k inner, mn columns, box 128 k x (128 | 256) mn. L.lda / L.ld are the
+    // column pitches of the A / B planes in whichever major they are stored.
+    const bool ok_a = A_MN ? make_plane_map(&ma, L.a_planes, L.m, L.k, L.lda, L.a_stride, L.n_mod, kBK)
+                           : make_plane_map(&ma, L.a_planes, L.k, L.m, L.lda, L.a_stride, L.n_mod, C::kBM);
+    const bool ok_b = B_MN ? make_plane_map(&mb, L.b_planes, L.n, L.k, L.ld, L.b_stride, L.n_mod, kBK)
+                           : make_plane_map(&mb, L.b_planes, L.k, L.n, L.ld, L.b_stride, L.n_mod, C::kBRows);
+    if (!ok_a || !ok_b) {
         set_error("cuTensorMapEncodeTiled failed");
         return OZK_CUDA_ERROR;
     }
@@ -581,7 +597,7 @@ int launch_impl(const K2Launch& L, cudaStream_t s) {
     if (clusters > total) clusters = total;
     if (clusters < 1) clusters = 1;
 
-    auto kern = residue_gemm_kernel<CG, KIND>;
+    auto kern = residue_gemm_kernel<CG, KIND, A_MN, B_MN>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
@@ -607,18 +623,24 @@ int launch_impl(const K2Launch& L, cudaStream_t s) {
     return OZK_OK;
 }
 
-template <int CG>
+template <int CG, bool A_MN, bool B_MN>
 int launch_kind(const K2Launch& L, cudaStream_t s) {
     switch (L.kind) {
         case K2_I32:
-            return launch_impl<CG, K2_I32>(L, s);
+            return launch_impl<CG, K2_I32, A_MN, B_MN>(L, s);
         case K2_U8:
-            return launch_impl<CG, K2_U8>(L, s);
+            return launch_impl<CG, K2_U8, A_MN, B_MN>(L, s);
         case K2_U8ACC:
-            return launch_impl<CG, K2_U8ACC>(L, s);
+            return launch_impl<CG, K2_U8ACC, A_MN, B_MN>(L, s);
         default:
-            return launch_impl<CG, K2_MAX>(L, s);
+            return launch_impl<CG, K2_MAX, A_MN, B_MN>(L, s);
     }
+}
+
+template <int CG>
+int launch_layout(const K2Launch& L, cudaStream_t s) {
+    if (L.a_mn) return L.b_mn ? launch_kind<CG, true, true>(L, s) : launch_kind<CG, true, false>(L, s);
+    return L.b_mn ? launch_kind<CG, false, true>(L, s) : launch_kind<CG, false, false>(L, s);
 }
 
 }  // namespace
@@ -637,7 +659,7 @@ int launch_k2(const K2Launch& L, cudaStream_t s) {
         set_error("residue_gemm: dimension exceeds 2^31");
         return OZK_INPUT_ERROR;
     }
-    auto one = [&](const K2Launch& X) { return k2_cta_group() == 1 ? launch_kind<1>(X, s) : launch_kind<2>(X, s); };
+    auto one = [&](const K2Launch& X) { return k2_cta_group() == 1 ? launch_layout<1>(X, s) : launch_layout<2>(X, s); };
     // One int32 accumulation stays exact for k <= 2^17 (only the benign
     // k = 2^17 wrap, int8_engine.hpp:19-22); U8 products over a longer k run in
     // chunks of 2^17, each chunk's residues added into U and reduced again —
@@ -647,8 +669,8 @@ int launch_k2(const K2Launch& L, cudaStream_t s) {
     for (int64_t k0 = 0; k0 < L.k; k0 += kChunkK) {
         K2Launch X = L;
         X.k = L.k - k0 < kChunkK ? L.k - k0 : kChunkK;
-        X.a_planes = L.a_planes + k0 * L.lda;  // MN-major: k columns
-        X.b_planes = L.b_planes + k0;          // K-major: offset inside each column
+        X.a_planes = L.a_planes + (L.a_mn ? k0 * L.lda : k0);  // MN-major: k columns; K-major: inside a column
+        X.b_planes = L.b_planes + (L.b_mn ? k0 * L.ld : k0);
         X.kind = k0 == 0 ? K2_U8 : K2_U8ACC;
         const int st = one(X);
         if (st != OZK_OK) return st;

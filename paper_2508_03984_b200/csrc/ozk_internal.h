@@ -69,14 +69,19 @@ void launch_a_planes(const void* a, int is_f32, int64_t m, int64_t k, int64_t ld
 void launch_b_planes(const void* b, int is_f32, int64_t k, int64_t n, int64_t ldb, const int32_t* col_exp,
                      const DevConsts& c, int kind, int8_t* planes, int64_t ld, int64_t plane_stride, cudaStream_t s);
 // FP64 -> FP32 rounding of an input (emulator.cpp:84-91), column-major with ld
-void launch_round_to_f32(const double* x, int64_t rows, int64_t cols, int64_t ld, float* out, cudaStream_t s);
+void launch_round_to_f32(const double* x, int64_t rows, int64_t cols, int64_t ld, float* out, int64_t ldo,
+                         cudaStream_t s);
 
 // ---- K2 (k2_gemm.cu) -------------------------------------------------------
 enum K2Kind { K2_I32 = 0, K2_U8 = 1, K2_MAX = 2, K2_U8ACC = 3 };
 struct K2Launch {
-    const int8_t* a_planes;  // [n_mod] planes of k columns x lda bytes (MN-major), plane stride a_stride
-    const int8_t* b_planes;  // [n_mod] planes of n columns x ld bytes (K-major), plane stride b_stride
+    // planes are column-major byte matrices with column pitch lda / ld:
+    //   A MN-major (a_mn): k columns of m;  A K-major: m columns of k
+    //   B K-major:          n columns of k;  B MN-major (b_mn): k columns of n
+    const int8_t* a_planes;  // n_mod planes, plane stride a_stride
+    const int8_t* b_planes;  // n_mod planes, plane stride b_stride
     int64_t m, n, k, ld, lda;
+    bool a_mn = true, b_mn = false;
     int64_t a_stride, b_stride;  // bytes between planes
     int64_t out_stride;          // elements between output planes (I32 / U8)
     int n_mod;

@@ -90,7 +90,8 @@ def dump_tables_csv(c: _lib.OzkConstants) -> str:
     return buf.value.decode()
 
 
-def _config(cfg: EmuConfig, a_type: int, c_type: int, constants=None) -> _lib.OzkConfig:
+def _config(cfg: EmuConfig, a_type: int, c_type: int, constants=None, trans_a: bool = False,
+            trans_b: bool = False) -> _lib.OzkConfig:
     c = _lib.OzkConfig()
     c.n_moduli = int(cfg.n_moduli)
     c.mode = int(cfg.mode)
@@ -99,6 +100,7 @@ def _config(cfg: EmuConfig, a_type: int, c_type: int, constants=None) -> _lib.Oz
     c.c_type = c_type
     c.block_k = int(cfg.block_k)
     c.flags = _lib.OZK_FLAG_FAST_EXPONENT_FIX if getattr(cfg, "fast_exponent_fix", False) else 0
+    c.flags |= (_lib.OZK_FLAG_TRANS_A if trans_a else 0) | (_lib.OZK_FLAG_TRANS_B if trans_b else 0)
     c.constants = C.pointer(constants) if constants is not None else None
     return c
 
@@ -144,30 +146,51 @@ class Context:
 
     # ---- host (reference-facing) GEMM ----------------------------------------------
     def gemm_host(self, a: np.ndarray, b: np.ndarray, cfg: EmuConfig, alpha: float = 1.0, beta: float = 0.0,
-                  c: np.ndarray | None = None, c_dtype=np.float64, constants=None) -> np.ndarray:
-        _validate_threads(a, b, cfg)
+                  c: np.ndarray | None = None, c_dtype=np.float64, constants=None, trans_a: bool = False,
+                  trans_b: bool = False) -> np.ndarray:
+        """C = alpha op(a) op(b) + beta c with op(x) = x.T when trans_x (a/b are
+        passed as stored, e.g. a is k x m for trans_a; nothing is transposed)."""
+        _validate_threads(a.T if trans_a else a, b.T if trans_b else b, cfg)
         dt = np.float32 if a.dtype == np.float32 else np.float64
         a = np.asfortranarray(a, dtype=dt)
         b = np.asfortranarray(b, dtype=dt)
-        m, k = a.shape
-        n = b.shape[1]
+        m, k = (a.shape[1], a.shape[0]) if trans_a else a.shape
+        n = b.shape[0] if trans_b else b.shape[1]
         out = np.zeros((m, n), dtype=c_dtype, order="F") if c is None else c
         if not (out.flags.f_contiguous and out.shape == (m, n)):
             raise InputError("c must be an m x n Fortran-ordered array")
         conf = _config(cfg, _lib.OZK_R32F if dt == np.float32 else _lib.OZK_R64F,
-                       _lib.OZK_R32F if out.dtype == np.float32 else _lib.OZK_R64F, constants)
-        _lib.check(self._lib.ozk_gemm_host(self.handle, C.byref(conf), m, n, k, float(alpha), a.ctypes.data, m,
-                                           b.ctypes.data, k, float(beta), out.ctypes.data, m))
+                       _lib.OZK_R32F if out.dtype == np.float32 else _lib.OZK_R64F, constants, trans_a, trans_b)
+        _lib.check(self._lib.ozk_gemm_host(self.handle, C.byref(conf), m, n, k, float(alpha), a.ctypes.data,
+                                           a.shape[0], b.ctypes.data, b.shape[0], float(beta), out.ctypes.data, m))
         return out
 
     # ---- device GEMM (torch CUDA tensors, column-major) ------------------------------
-    def gemm(self, A, B, cfg: EmuConfig, C_out, alpha: float = 1.0, beta: float = 0.0, constants=None) -> None:
-        m, k = A.shape
-        n = B.shape[1]
+    def gemm(self, A, B, cfg: EmuConfig, C_out, alpha: float = 1.0, beta: float = 0.0, constants=None,
+             trans_a: bool = False, trans_b: bool = False) -> None:
+        """C_out = alpha op(A) op(B) + beta C_out; A, B as stored (column-major),
+        op(X) = X^T when trans_x (BLAS 'T')."""
+        m, k = (A.shape[1], A.shape[0]) if trans_a else A.shape
+        n = B.shape[0] if trans_b else B.shape[1]
         lda, ldb, ldc = _colmajor_ld(A), _colmajor_ld(B), _colmajor_ld(C_out)
-        conf = _config(cfg, _dtype_code(A), _dtype_code(C_out), constants)
+        conf = _config(cfg, _dtype_code(A), _dtype_code(C_out), constants, trans_a, trans_b)
         _lib.check(self._lib.ozk_gemm(self.handle, C.byref(conf), m, n, k, float(alpha), A.data_ptr(), lda,
                                       B.data_ptr(), ldb, float(beta), C_out.data_ptr(), ldc))
+
+    def gemm_strided_batched(self, A, B, cfg: EmuConfig, C_out, alpha: float = 1.0, beta: float = 0.0,
+                             trans_a: bool = False, trans_b: bool = False) -> None:
+        """batched gemm over (batch, rows, cols) tensors whose slices are column-major
+        (stride (s, 1, ld)), cublasGemmStridedBatched-style."""
+        batch = A.shape[0]
+        if B.shape[0] != batch or C_out.shape[0] != batch:
+            raise InputError("batch sizes disagree")
+        m, k = (A.shape[2], A.shape[1]) if trans_a else A.shape[1:]
+        n = B.shape[1] if trans_b else B.shape[2]
+        lda, ldb, ldc = _colmajor_ld(A[0]), _colmajor_ld(B[0]), _colmajor_ld(C_out[0])
+        conf = _config(cfg, _dtype_code(A), _dtype_code(C_out), None, trans_a, trans_b)
+        _lib.check(self._lib.ozk_gemm_strided_batched(
+            self.handle, C.byref(conf), m, n, k, float(alpha), A.data_ptr(), lda, A.stride(0), B.data_ptr(), ldb,
+            B.stride(0), float(beta), C_out.data_ptr(), ldc, C_out.stride(0), batch))
 
     # ---- column shard (multi-GPU, see distributed.py) -------------------------------
     def shard_begin(self, A, B, cfg: EmuConfig) -> None:
