@@ -695,6 +695,35 @@ int ozo_gemm_f64_scaled(const double* a, const double* b, int64_t m, int64_t n, 
     return 0;
 }
 
+/* FP32 twin of ozo_gemm_f64_scaled (emulator.cpp:82-93 after scaling) */
+int ozo_gemm_f32_scaled(const float* a, const float* b, int64_t m, int64_t n, int64_t k, const ozo_constants* c,
+                        const int32_t* mu, const int32_t* nu, int64_t block_k, double* out) {
+    float* ap = (float*)malloc((size_t)(m * k) * sizeof(float));
+    float* bp = (float*)malloc((size_t)(k * n) * sizeof(float));
+    ozo_truncate_f32(a, m, k, mu, 0, ap);
+    ozo_truncate_f32(b, k, n, nu, 1, bp);
+    int8_t* sa = (int8_t*)malloc((size_t)(c->n_moduli * m * k));
+    int8_t* sb = (int8_t*)malloc((size_t)(c->n_moduli * k * n));
+    ozo_residues_f32(ap, m * k, c, sa);
+    ozo_residues_f32(bp, k * n, c, sb);
+    uint8_t* u = (uint8_t*)malloc((size_t)(c->n_moduli * m * n));
+    for (int i = 0; i < c->n_moduli; ++i)
+        products_u8(sa + i * m * k, sb + i * k * n, m, n, k, block_k, c->moduli[i], c->pinv_mulhi[i], u + i * m * n);
+    double* c1 = (double*)malloc((size_t)(m * n) * sizeof(double));
+    double* c2 = (double*)malloc((size_t)(m * n) * sizeof(double));
+    ozo_accumulate(u, m * n, c, c1, c2);
+    for (int64_t e = 0; e < m * n; ++e) c1[e] = ozo_crt_reduce_element(c1[e], c2[e], c);
+    ozo_unscale(c1, m, n, mu, nu, out);
+    free(ap);
+    free(bp);
+    free(sa);
+    free(sb);
+    free(u);
+    free(c1);
+    free(c2);
+    return 0;
+}
+
 /* accurate-mode exponent of one line from its bound maximum (scaling.cpp:153-161);
  * base = 5 - ilogb(max|x|), the caller handles zero lines */
 int ozo_accurate_exponent(int64_t cmax, int base, const ozo_constants* c) {

@@ -80,6 +80,8 @@ int ozo_gemm_f64_consts(const double* a, const double* b, int64_t m, int64_t n, 
 /* pipeline with caller-given exponents (sharding checks) and the accurate budget */
 int ozo_gemm_f64_scaled(const double* a, const double* b, int64_t m, int64_t n, int64_t k, const ozo_constants* c,
                         const int32_t* mu, const int32_t* nu, int64_t block_k, double* out);
+int ozo_gemm_f32_scaled(const float* a, const float* b, int64_t m, int64_t n, int64_t k, const ozo_constants* c,
+                        const int32_t* mu, const int32_t* nu, int64_t block_k, double* out);
 int ozo_accurate_exponent(int64_t cmax, int base, const ozo_constants* c);
 
 /* debug: the uint8 residue products U_i of the pipeline (N consecutive m x n slices) */

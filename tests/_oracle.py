@@ -112,6 +112,7 @@ class Oracle:
             getattr(L, nm).argtypes = [_p, _p, _i64, _i64, _i64, C.c_int, C.c_int, _i64, _p]
         L.ozo_gemm_f64_consts.argtypes = [_p, _p, _i64, _i64, _i64, C.POINTER(Constants), C.c_int, _i64, _p]
         L.ozo_gemm_f64_scaled.argtypes = [_p, _p, _i64, _i64, _i64, C.POINTER(Constants), _p, _p, _i64, _p]
+        L.ozo_gemm_f32_scaled.argtypes = [_p, _p, _i64, _i64, _i64, C.POINTER(Constants), _p, _p, _i64, _p]
         L.ozo_accurate_exponent.argtypes = [C.c_int64, C.c_int, C.POINTER(Constants)]
 
     # -- constants -----------------------------------------------------------------
@@ -227,15 +228,20 @@ class Oracle:
             raise ValueError(f"status {st}")
         return c
 
-    def gemm_scaled(self, a, b, n_moduli, mu_exp, nu_exp, block_k=1 << 17):
-        a, b = _f(a, np.float64), _f(b, np.float64)
+    def gemm_scaled(self, a, b, n_moduli, mu_exp, nu_exp, block_k=1 << 17, prec=0):
+        """the pipeline after scaling, with given exponents: entry (i, j) depends only on
+        row i of a, column j of b, mu_exp[i], nu_exp[j] -- so sampled rows/columns of a
+        large problem reproduce those entries of its C exactly"""
+        dt = np.float64 if prec == 0 else np.float32
+        a, b = _f(a, dt), _f(b, dt)
         m, k = a.shape
         n = b.shape[1]
-        cs = self.constants(n_moduli)
+        cs = self.constants(n_moduli, prec)
         mu = np.ascontiguousarray(mu_exp, np.int32)
         nu = np.ascontiguousarray(nu_exp, np.int32)
         c = np.zeros((m, n), np.float64, order="F")
-        self.lib.ozo_gemm_f64_scaled(_ptr(a), _ptr(b), m, n, k, C.byref(cs), _ptr(mu), _ptr(nu), block_k, _ptr(c))
+        fn = self.lib.ozo_gemm_f64_scaled if prec == 0 else self.lib.ozo_gemm_f32_scaled
+        fn(_ptr(a), _ptr(b), m, n, k, C.byref(cs), _ptr(mu), _ptr(nu), block_k, _ptr(c))
         return c
 
     def accurate_exponent(self, cmax: int, base: int, n_moduli: int) -> int:
