@@ -358,34 +358,69 @@ def main():
         extra["native_fp64_tflops"] = native_gemm_tflops(n, torch.float64, 3)
         extra["native_fp32_tflops"] = native_gemm_tflops(n, torch.float32, 3)
         extra["int8_cublaslt_tops"] = int8_library_tops(n)
-        sweep = {}
-        for N in (12, 14, 16, 18, 20):
-            for md in (ScaleMode.Fast, ScaleMode.Accurate):
-                c2 = EmuConfig(n_moduli=N, mode=md)
-                ctx.gemm(A, B, c2, C)
-                torch.cuda.synchronize()
-                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s0.record(stream)
-                for _ in range(2):
-                    ctx.gemm(A, B, c2, C)
-                s1.record(stream)
-                torch.cuda.synchronize()
-                sweep[f"{md.name.lower()}{N}"] = flop / (s0.elapsed_time(s1) / 2 * 1e-3) / 1e12
-        extra["dgemm_sweep_tflops"] = sweep
-        # BLAS transposes (square problem: the stored operands are read as op(X) = X^T)
-        trans = {}
-        for ta, tb in ((False, False), (True, False), (False, True), (True, True)):
-            ctx.gemm(A, B, cfg, C, trans_a=ta, trans_b=tb)
+        def timed(Ax, Bx, c2, Cx, reps=2, **kw):
+            ctx.gemm(Ax, Bx, c2, Cx, **kw)
             torch.cuda.synchronize()
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
-            for _ in range(2):
-                ctx.gemm(A, B, cfg, C, trans_a=ta, trans_b=tb)
+            for _ in range(reps):
+                ctx.gemm(Ax, Bx, c2, Cx, **kw)
             s1.record(stream)
             torch.cuda.synchronize()
-            trans["TN"[not ta] + "TN"[not tb]] = flop / (s0.elapsed_time(s1) / 2 * 1e-3) / 1e12
-        extra["transposes_tflops"] = trans
-        # accuracy vs native FP64 on a sampled block (emulated vs torch fp64 vs exact-ish fp64 reference)
+            mm, nn = Cx.shape
+            kk = Ax.shape[0] if kw.get("trans_a") else Ax.shape[1]
+            return 2.0 * mm * nn * kk / (s0.elapsed_time(s1) / reps * 1e-3) / 1e12
+
+        sweep = {}
+        for N in (12, 14, 16, 18, 20):
+            for md in (ScaleMode.Fast, ScaleMode.Accurate):
+                sweep[f"{md.name.lower()}{N}"] = timed(A, B, EmuConfig(n_moduli=N, mode=md), C)
+        extra["dgemm_sweep_tflops"] = sweep
+        # BLAS transposes (square problem: the stored operands are read as op(X) = X^T)
+        extra["transposes_tflops"] = {"TN"[not ta] + "TN"[not tb]: timed(A, B, cfg, C, trans_a=ta, trans_b=tb)
+                                      for ta, tb in ((False, False), (True, False), (False, True), (True, True))}
+        # SGEMM emulation (BASELINE configs[2]): FP32 inputs, FP32 C, N = 6..10, vs native FP32
+        A32, B32 = A.float(), B.float()
+        C32 = torch.empty((n, m), dtype=torch.float32, device=dev).t()
+        extra["sgemm_sweep_tflops"] = {
+            f"{md.name.lower()}{N}": timed(A32, B32, EmuConfig(n_moduli=N, mode=md, precision=Precision.Fp32), C32)
+            for N in (6, 7, 8, 9, 10) for md in (ScaleMode.Fast, ScaleMode.Accurate)}
+        extra["sgemm_accuracy"] = accuracy_probe(ctx, A32, B32, EmuConfig(n_moduli=8, mode=ScaleMode.Fast,
+                                                                          precision=Precision.Fp32))
+        del A32, B32, C32
+        # input dynamic range (BASELINE configs[4]): phi sweep accuracy on a 1024^2 block, full k
+        extra["phi_sweep"] = {}
+        for phi in (0.5, 1.0, 1.5, 2.0, 3.0, 4.0):
+            Ap = gen_device(1024, k, phi, 11, torch.float64, dev)
+            Bp = gen_device(k, 1024, phi, 12, torch.float64, dev)
+            extra["phi_sweep"][str(phi)] = {
+                f"{md.name.lower()}{N}": accuracy_probe(ctx, Ap, Bp, EmuConfig(n_moduli=N, mode=md), short=True)
+                for N in (14, 16, 18) for md in (ScaleMode.Fast, ScaleMode.Accurate)}
+            extra["phi_sweep"][str(phi)]["native_fp64"] = accuracy_probe(ctx, Ap, Bp, None, short=True)
+            del Ap, Bp
+        # rectangular m = n = 8192, k = 65536 (configs[4]) and n = 32768 (configs[3] per-GPU problem)
+        del C
+        torch.cuda.empty_cache()
+        Ar = gen_device(8192, 65536, args.phi, 21, torch.float64, dev)
+        Br = gen_device(65536, 8192, args.phi, 22, torch.float64, dev)
+        Cr = torch.empty((8192, 8192), dtype=torch.float64, device=dev).t()
+        extra["rect_8192x8192x65536_tflops"] = {f"{md.name.lower()}{args.moduli}": timed(
+            Ar, Br, EmuConfig(n_moduli=args.moduli, mode=md), Cr) for md in (ScaleMode.Fast, ScaleMode.Accurate)}
+        extra["rect_accuracy"] = accuracy_probe(ctx, Ar, Br, cfg)
+        del Ar, Br, Cr
+        torch.cuda.empty_cache()
+        if not os.environ.get("OZK_BENCH_NO_32K"):
+            n2 = 32768
+            A2 = gen_device(n2, n2, args.phi, 31, torch.float64, dev)
+            B2 = gen_device(n2, n2, args.phi, 32, torch.float64, dev)
+            C2 = torch.empty((n2, n2), dtype=torch.float64, device=dev).t()
+            extra["dgemm_32768_tflops"] = {f"{md.name.lower()}{args.moduli}": timed(
+                A2, B2, EmuConfig(n_moduli=args.moduli, mode=md), C2, reps=1)
+                for md in (ScaleMode.Fast, ScaleMode.Accurate)}
+            extra["native_fp64_32768_tflops"] = native_gemm_tflops(n2, torch.float64, 1)
+            del A2, B2, C2
+            torch.cuda.empty_cache()
+        # accuracy vs native FP64 on a sampled block
         extra["accuracy"] = accuracy_probe(ctx, A, B, cfg)
         out["extra"] = extra
 
@@ -401,34 +436,54 @@ def main():
         dist.destroy_process_group()
 
 
-def accuracy_probe(ctx, A, B, cfg):
+def accuracy_probe(ctx, A, B, cfg, short=False):
     """Max componentwise relative error on a 1024 x 1024 block of C (full k),
-    for this configuration and for native FP64 (cuBLAS), against the N = 20
-    accurate-mode emulation of the same block, which is exact to about one
-    ulp at phi <= 2 (2.2e-16 .. 8.5e-16)."""
+    for this configuration and for native GEMM (cuBLAS, same precision),
+    against the N = 20 accurate-mode FP64 emulation of the same block, which is
+    exact to about one ulp at phi <= 4 (2.2e-16 .. 8.5e-16).
+    cfg None: native only."""
     import torch
 
     from paper_2508_03984_b200 import EmuConfig, ScaleMode
 
-    rows = cols = 1024
+    rows = min(1024, A.shape[0])
+    cols = min(1024, B.shape[1])
     a = A[:rows, :].t().contiguous().t()
     b = B[:, :cols].t().contiguous().t()
 
-    def emu(n_mod, mode):
+    def emu(c):
         out = torch.empty((cols, rows), dtype=torch.float64, device=A.device).t()
-        ctx.gemm(a, b, EmuConfig(n_moduli=n_mod, mode=mode), out)
+        ctx.gemm(a, b, c, out)
         return out
 
-    ref = emu(20, ScaleMode.Accurate)
+    ref = emu(EmuConfig(n_moduli=20, mode=ScaleMode.Accurate)) if a.dtype == torch.float64 else \
+        _exact_fp32_product(ctx, a, b)
     den = ref.abs().clamp_min(1e-300)
-    got = emu(cfg.n_moduli, cfg.mode)
-    native = a @ b
-    return {"block": f"{rows}x{cols}, full k", "against": "emulated N=20 accurate (~1 ulp)",
-            "emulated_max_rel": float(((got - ref).abs() / den).max()),
-            "emulated_median_rel": float(((got - ref).abs() / den).median()),
-            "native_fp64_max_rel": float(((native - ref).abs() / den).max()),
-            "native_fp64_median_rel": float(((native - ref).abs() / den).median())}
 
+    def stats(x):
+        r = (x.double() - ref).abs() / den
+        return float(r.max()), float(r.median())
+
+    native = stats(a @ b)
+    if cfg is None:
+        return native[0] if short else {"native_max_rel": native[0], "native_median_rel": native[1]}
+    got = stats(emu(cfg))
+    if short:
+        return got[0]
+    return {"block": f"{rows}x{cols}, full k", "against": "emulated N=20 accurate FP64 (~1 ulp)",
+            "emulated_max_rel": got[0], "emulated_median_rel": got[1],
+            "native_max_rel": native[0], "native_median_rel": native[1]}
+
+
+def _exact_fp32_product(ctx, a, b):
+    """FP32 inputs: their FP64 product through the N = 20 accurate FP64 emulation"""
+    import torch
+
+    from paper_2508_03984_b200 import EmuConfig, ScaleMode
+
+    out = torch.empty((b.shape[1], a.shape[0]), dtype=torch.float64, device=a.device).t()
+    ctx.gemm(a.double(), b.double(), EmuConfig(n_moduli=20, mode=ScaleMode.Accurate), out)
+    return out
 
 if __name__ == "__main__":
     main()

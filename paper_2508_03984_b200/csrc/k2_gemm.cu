@@ -63,7 +63,8 @@ struct K2Params {
     int p[OZK_MAX_MODULI];
     int pinv[OZK_MAX_MODULI];
     int group;             // tile rows per raster group
-    int hints;             // 1: L2 evict_last on operand loads, streaming U stores
+    int hints;             // bit 0: A loads evict_last, bit 1: B loads evict_last, bit 2: streaming U
+                           // stores, bit 3: B loads evict_first
     int sync_mode;         // 0 off; 1 tile lockstep (slack 1); 2 k-block lockstep
     int sync_window;       // mode 2: max k-blocks ahead of the slowest cluster
     int sync_every;        // mode 2: check every this many k-blocks
@@ -142,6 +143,16 @@ __device__ __forceinline__ void tma_load_3d_2sm_hint(uint32_t dst, const CUtenso
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
 __device__ __forceinline__ void st_stream_u8(uint8_t* p, uint32_t v) {
@@ -325,7 +336,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         int stage = 0;
         uint32_t phase = 0;
         const uint32_t full0_leader = CG == 2 ? mapa(smem_u32(full), 0) : smem_u32(full);
-        const uint64_t pol = policy_evict_last();
+        const uint64_t pol_a = (P.hints & 1) ? policy_evict_last() : policy_evict_normal();
+        const uint64_t pol_b = (P.hints & 2) ? policy_evict_last()
+                                             : ((P.hints & 8) ? policy_evict_first() : policy_evict_normal());
         const bool kstep = P.sync_mode == 2 && leader;
         int lt = 0;
         for (int t = cluster_id; t < total; t += nclusters, ++lt) {
@@ -371,9 +384,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     constexpr int kBBoxes = (B_MN && C::kBRows > 128) ? C::kBRows / 128 : 1;
                     if constexpr (CG == 2) {
                         const uint32_t lb = full0_leader + 8u * stage;
-                        if (P.hints) {
-                            tma_load_3d_2sm_hint(dA, &tmA, lb, ac0, ac1, mod, pol);
-                            tma_load_3d_2sm_hint(dB, &tmB, lb, bc0, bc1, mod, pol);
+                        if (P.hints & 11) {
+                            tma_load_3d_2sm_hint(dA, &tmA, lb, ac0, ac1, mod, pol_a);
+                            tma_load_3d_2sm_hint(dB, &tmB, lb, bc0, bc1, mod, pol_b);
                         } else {
                             tma_load_3d_2sm(dA, &tmA, lb, ac0, ac1, mod);
                             tma_load_3d_2sm(dB, &tmB, lb, bc0, bc1, mod);
@@ -468,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     u += *q;
                                     u = u >= static_cast<uint32_t>(pm) ? u - pm : u;
                                 }
-                                if (P.hints)
+                                if (P.hints & 4)
                                     st_stream_u8(q, u);
                                 else
                                     *q = static_cast<uint8_t>(u);
@@ -579,7 +592,7 @@ int launch_impl(const K2Launch& L, cudaStream_t s) {
         P.pinv[i] = L.c->pinv_mulhi[i];
     }
     P.group = env_int("OZK_K2_GROUP", 8);
-    P.hints = env_int("OZK_K2_HINTS", 0);
+    P.hints = env_int("OZK_K2_HINTS", 9);  // A evict_last, B evict_first (profiles/r01_k2_hints_sweep.md)
     // Lockstep (default on): co-resident clusters that share A/B panels stay
     // within one tile of each other, so the panels they all stream are still in
     // L2 when the trailing cluster reads them. Measured at 16384^3, N=14: DRAM

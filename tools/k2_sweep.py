@@ -33,7 +33,8 @@ def main():
     u = torch.empty((n_mod, n, (m + 15) // 16 * 16), dtype=torch.uint8, device="cuda")
     cfg = EmuConfig(n_moduli=n_mod)
     out = []
-    for v in VARIANTS:
+    variants = json.loads(os.environ["SWEEP_VARIANTS"]) if "SWEEP_VARIANTS" in os.environ else VARIANTS
+    for v in variants:
         os.environ.update(v)
         ctx.stage_products(cfg, m, n, k, pa, pb, _lib.OZK_PRODUCTS_U8, u, u.shape[2])  # warm
         torch.cuda.synchronize()
