@@ -86,6 +86,10 @@ struct Job {
     int64_t lda, ldb;
     int in_f32;
     int32_t *mu, *nu, *ma, *nb, *rowmax, *colmax, *flag_rows, *flag_cols;
+    // accurate mode with k > 2^19: the bound product Abar*Bbar exceeds int32, so it
+    // accumulates in int64 (per column block) and its maxima are uint64
+    bool wide_bound;
+    unsigned long long *rowmax64, *colmax64;
     int32_t* flags;  // [0] non-finite, [1] flagged rows, [2] flagged columns, [4..] K2 lockstep words (1 KB)
     double *amax, *asum, *bmax, *bsum;
     int splits, splits_b;  // k-partials of the row-stat reductions of op(A) (!ta) / op(B) (tb)
@@ -100,7 +104,7 @@ struct ozk_context {
     cudaStream_t stream = nullptr;              // compute stream (user-settable)
     cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of ozk_gemm_host
     int64_t launches = 0;
-    Buf planes_a, planes_b, u, stats, ints, flags, f32a, f32b, host_a, host_b, host_c;
+    Buf planes_a, planes_b, u, stats, ints, flags, f32a, f32b, host_a, host_b, host_c, wide, cbar;
     int32_t* flags_host = nullptr;  // pinned mirror of the device flag word
     // stage timing (ozk_profile): CUDA events on the compute stream
     bool profiling = false;
@@ -130,6 +134,9 @@ int cuda_fail(const char* what, cudaError_t e) {
         const int st_ = (call);        \
         if (st_ != OZK_OK) return st_; \
     } while (0)
+
+// entries of Abar*Bbar are <= 64 * 64 * k: int32 holds them up to k = 2^19
+constexpr int64_t kBoundInt32K = int64_t(1) << 19;
 
 int ensure(Buf& b, size_t bytes) {
     if (bytes <= b.bytes && b.p) return OZK_OK;
@@ -209,12 +216,6 @@ int validate(const ozk_config* cfg, const ozk_constants& c, int64_t m, int64_t n
         set_error("gemm_emulated: unknown scaling mode");
         return OZK_CONFIG_ERROR;
     }
-    if (cfg->mode == OZK_ACCURATE && k > (int64_t(1) << 19)) {
-        // the bound product Abar*Bbar (entries <= 64*64*k) accumulates in one
-        // int32 TMEM tile; beyond 2^19 it would need an int64 C-bar
-        set_error("accurate mode supports k <= 2^19 (bound-product accumulator range)");
-        return OZK_INPUT_ERROR;
-    }
     if (k > (int64_t(1) << 31) - 1) {
         set_error("k exceeds 2^31");
         return OZK_INPUT_ERROR;
@@ -268,6 +269,12 @@ int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c,
     J.colmax = J.rowmax + m;
     J.flag_rows = J.colmax + n;
     J.flag_cols = J.flag_rows + m;
+    J.wide_bound = cfg->mode == OZK_ACCURATE && k > kBoundInt32K;
+    if (J.wide_bound) {
+        OZK_TRY(ensure(h->wide, sizeof(unsigned long long) * (m + n)));
+        J.rowmax64 = static_cast<unsigned long long*>(h->wide.p);
+        J.colmax64 = J.rowmax64 + m;
+    }
     J.pa = static_cast<int8_t*>(h->planes_a.p);
     J.pb = static_cast<int8_t*>(h->planes_b.p);
     J.u = static_cast<uint8_t*>(h->u.p);
@@ -366,6 +373,7 @@ int stage_rows(ozk_context* h, Job& J) {
     launch_accurate_base(J.amax, J.splits, J.m, J.ma, h->stream);
     a_planes(h, J, J.ma, 1, J.pa, J.pa_stride);
     OZK_CUDA(cudaMemsetAsync(J.rowmax, 0, sizeof(int32_t) * J.m, h->stream));
+    if (J.wide_bound) OZK_CUDA(cudaMemsetAsync(J.rowmax64, 0, sizeof(unsigned long long) * J.m, h->stream));
     return check_launch(h, 2);
 }
 
@@ -391,6 +399,10 @@ int stage_cols(ozk_context* h, Job& J, int64_t j0, int64_t nj) {
     int8_t* bbar = J.pb + b_plane_off(J, j0);
     b_planes(h, J, j0, nj, J.nb, 1, J.pb, J.pb_stride);
     OZK_CUDA(cudaMemsetAsync(J.colmax + j0, 0, sizeof(int32_t) * nj, h->stream));
+    if (J.wide_bound) {
+        OZK_CUDA(cudaMemsetAsync(J.colmax64 + j0, 0, sizeof(unsigned long long) * nj, h->stream));
+        OZK_TRY(ensure(h->cbar, sizeof(long long) * J.m * nj));
+    }
     OZK_TRY(check_launch(h, 2));
     K2Launch L{};
     L.a_planes = J.pa;
@@ -411,12 +423,26 @@ int stage_cols(ozk_context* h, Job& J, int64_t j0, int64_t nj) {
     L.c = &J.dc;
     L.num_sms = h->num_sms;
     L.sync_counter = reinterpret_cast<unsigned int*>(J.flags + 4);
+    if (J.wide_bound) {  // int64 C-bar block, then its maxima (scaling.cpp:118-148 keeps C-bar in int64 too)
+        L.kind = K2_ACC64;
+        L.out = h->cbar.p;
+        L.ldo = J.m;
+        OZK_TRY(launch_k2(L, h->stream));
+        launch_bound_max64(static_cast<const long long*>(h->cbar.p), J.m, nj, J.m, J.rowmax64, J.colmax64 + j0,
+                           h->stream);
+        return check_launch(h, (J.k + (1 << 17) - 1) / (1 << 17) + 1);
+    }
     OZK_TRY(launch_k2(L, h->stream));
     return check_launch(h, 1);
 }
 
 // accurate mode, after every column block: the budgets (scaling.cpp:151-165)
 int stage_budget(ozk_context* h, Job& J) {
+    if (J.wide_bound) {
+        launch_accurate_budget64(J.ma, J.rowmax64, J.m, J.dc, J.mu, h->stream);
+        launch_accurate_budget64(J.nb, J.colmax64, J.n, J.dc, J.nu, h->stream);
+        return check_launch(h, 2);
+    }
     launch_accurate_budget(J.ma, J.rowmax, J.m, J.dc, J.mu, h->stream);
     launch_accurate_budget(J.nb, J.colmax, J.n, J.dc, J.nu, h->stream);
     return check_launch(h, 2);
@@ -706,7 +732,8 @@ int ozk_create(ozk_handle* handle, int device) {
 int ozk_destroy(ozk_handle h) {
     if (!h) return OZK_OK;
     cudaSetDevice(h->device);
-    for (Buf* b : {&h->planes_a, &h->planes_b, &h->u, &h->stats, &h->ints, &h->flags, &h->f32a, &h->f32b, &h->host_a,
+    for (Buf* b : {&h->wide, &h->cbar, &h->planes_a, &h->planes_b, &h->u, &h->stats, &h->ints, &h->flags, &h->f32a,
+                   &h->f32b, &h->host_a,
                    &h->host_b, &h->host_c})
         if (b->p) cudaFree(b->p);
     if (h->flags_host) cudaFreeHost(h->flags_host);
@@ -832,6 +859,11 @@ int ozk_shard_begin(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, i
     ozk_constants c;
     OZK_TRY(resolve(cfg, c));
     OZK_TRY(validate(cfg, c, m, n, k, lda, ldb));
+    if (cfg->mode == OZK_ACCURATE && k > kBoundInt32K) {
+        // ozk_shard_rowmax exchanges int32 maxima
+        set_error("column-shard accurate mode supports k <= 2^19");
+        return OZK_INPUT_ERROR;
+    }
     OZK_CUDA(cudaSetDevice(h->device));
     Job& J = h->shard;
     J = Job{};

@@ -216,12 +216,13 @@ __global__ void accurate_base_kernel(const double* __restrict__ pmax, int splits
 
 // budget of scaling.cpp:151-165: e = min(floor(pp_accu - 0.51 log2 cmax), cap),
 // mu = 2^clamp(mu' exponent + e); cmax == 0 keeps mu'; zero lines keep 1.
-__global__ void accurate_budget_kernel(const int32_t* __restrict__ base, const int32_t* __restrict__ cmax_in,
+template <typename CT>
+__global__ void accurate_budget_kernel(const int32_t* __restrict__ base, const CT* __restrict__ cmax_in,
                                        int64_t lines, float pp_accu, int prec, int32_t* __restrict__ exp_out) {
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= lines) return;
     const int32_t b0 = base[t];
-    const int32_t cmax = cmax_in[t];
+    const CT cmax = cmax_in[t];
     int32_t out = 0;
     if (b0 != INT32_MIN) {
         int e = 0;
@@ -284,8 +285,14 @@ void launch_accurate_base(const double* pmax, int splits, int64_t lines, int32_t
 
 void launch_accurate_budget(const int32_t* base, const int32_t* cmax, int64_t lines, const DevConsts& c,
                             int32_t* exp_out, cudaStream_t s) {
-    accurate_budget_kernel<<<static_cast<unsigned>((lines + 255) / 256), 256, 0, s>>>(base, cmax, lines, c.pp_accu,
-                                                                                      c.precision, exp_out);
+    accurate_budget_kernel<int32_t><<<static_cast<unsigned>((lines + 255) / 256), 256, 0, s>>>(
+        base, cmax, lines, c.pp_accu, c.precision, exp_out);
+}
+
+void launch_accurate_budget64(const int32_t* base, const unsigned long long* cmax, int64_t lines, const DevConsts& c,
+                              int32_t* exp_out, cudaStream_t s) {
+    accurate_budget_kernel<unsigned long long><<<static_cast<unsigned>((lines + 255) / 256), 256, 0, s>>>(
+        base, cmax, lines, c.pp_accu, c.precision, exp_out);
 }
 
 }  // namespace ozk

@@ -60,6 +60,7 @@ struct K2Params {
     long long plane_out;
     int* rowmax;
     int* colmax;
+    int acc_first;  // ACC64
     int p[OZK_MAX_MODULI];
     int pinv[OZK_MAX_MODULI];
     int group;             // tile rows per raster group
@@ -495,6 +496,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int j = 0; j < 32; ++j)
                             if (col0 + j < P.n) dst[static_cast<long long>(col0 + j) * P.ldo] = static_cast<int32_t>(v[j]);
                     }
+                } else if constexpr (KIND == K2_ACC64) {
+                    // bound product over k > 2^19 (entries up to 64*64*k): int64 sum of
+                    // 2^17-deep chunks, each exact in int32
+                    long long* dst = static_cast<long long*>(P.out) + row;
+                    if (row_ok) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col0 + j < P.n) {
+                                long long* q = dst + static_cast<long long>(col0 + j) * P.ldo;
+                                const long long x = static_cast<int32_t>(v[j]);
+                                *q = P.acc_first ? x : *q + x;
+                            }
+                    }
                 } else {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) rmax = max(rmax, static_cast<int32_t>(v[j]));
@@ -587,6 +601,7 @@ int launch_impl(const K2Launch& L, cudaStream_t s) {
     P.plane_out = L.out_stride;
     P.rowmax = L.rowmax;
     P.colmax = L.colmax;
+    P.acc_first = L.acc_first ? 1 : 0;
     for (int i = 0; i < L.n_mod && L.c; ++i) {
         P.p[i] = L.c->p[i];
         P.pinv[i] = L.c->pinv_mulhi[i];
@@ -645,6 +660,8 @@ int launch_kind(const K2Launch& L, cudaStream_t s) {
             return launch_impl<CG, K2_U8, A_MN, B_MN>(L, s);
         case K2_U8ACC:
             return launch_impl<CG, K2_U8ACC, A_MN, B_MN>(L, s);
+        case K2_ACC64:
+            return launch_impl<CG, K2_ACC64, A_MN, B_MN>(L, s);
         default:
             return launch_impl<CG, K2_MAX, A_MN, B_MN>(L, s);
     }
@@ -678,13 +695,16 @@ int launch_k2(const K2Launch& L, cudaStream_t s) {
     // chunks of 2^17, each chunk's residues added into U and reduced again —
     // the reference's blocked path (emulator.cpp:57-73), whose value does not
     // depend on where the blocks fall.
-    if (L.kind != K2_U8 || L.k <= kChunkK) return one(L);
+    if ((L.kind != K2_U8 && L.kind != K2_ACC64) || L.k <= kChunkK) return one(L);
     for (int64_t k0 = 0; k0 < L.k; k0 += kChunkK) {
         K2Launch X = L;
         X.k = L.k - k0 < kChunkK ? L.k - k0 : kChunkK;
         X.a_planes = L.a_planes + (L.a_mn ? k0 * L.lda : k0);  // MN-major: k columns; K-major: inside a column
         X.b_planes = L.b_planes + (L.b_mn ? k0 * L.ld : k0);
-        X.kind = k0 == 0 ? K2_U8 : K2_U8ACC;
+        if (L.kind == K2_U8)
+            X.kind = k0 == 0 ? K2_U8 : K2_U8ACC;
+        else
+            X.acc_first = k0 == 0;
         const int st = one(X);
         if (st != OZK_OK) return st;
     }

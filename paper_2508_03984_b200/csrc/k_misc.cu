@@ -83,7 +83,29 @@ __global__ void unscale_kernel(const double* __restrict__ cpp, int64_t m, int64_
     }
 }
 
+// row / column maxima of the int64 bound product (k > 2^19): one block per column
+__global__ void bound_max64_kernel(const long long* __restrict__ cbar, int64_t m, int64_t ld,
+                                   unsigned long long* __restrict__ rowmax, unsigned long long* __restrict__ colmax) {
+    const int64_t j = blockIdx.x;
+    unsigned long long cm = 0;
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const unsigned long long v = static_cast<unsigned long long>(cbar[i + j * ld]);  // >= 0
+        cm = v > cm ? v : cm;
+        atomicMax(rowmax + i, v);
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(0xffffffffu, cm, o);
+        cm = x > cm ? x : cm;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(colmax + j, cm);
+}
+
 }  // namespace
+
+void launch_bound_max64(const long long* cbar, int64_t m, int64_t n, int64_t ld, unsigned long long* rowmax,
+                        unsigned long long* colmax, cudaStream_t s) {
+    bound_max64_kernel<<<static_cast<unsigned>(n), kThreads, 0, s>>>(cbar, m, ld, rowmax, colmax);
+}
 
 void launch_truncate(int is_f32, const void* x, int64_t rows, int64_t cols, int64_t ldx, const int32_t* se, int side,
                      void* out, int64_t ldo, cudaStream_t s) {

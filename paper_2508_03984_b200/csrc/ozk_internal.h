@@ -61,6 +61,11 @@ void launch_fast_exact(const void* base, int is_f32, int64_t line_step, int64_t 
 void launch_accurate_base(const double* pmax, int splits, int64_t lines, int32_t* out, cudaStream_t s);
 void launch_accurate_budget(const int32_t* base, const int32_t* cmax, int64_t lines, const DevConsts& c,
                             int32_t* exp_out, cudaStream_t s);
+// k > 2^19: the bound product accumulates in int64 (K2_ACC64), maxima in uint64
+void launch_accurate_budget64(const int32_t* base, const unsigned long long* cmax, int64_t lines, const DevConsts& c,
+                              int32_t* exp_out, cudaStream_t s);
+void launch_bound_max64(const long long* cbar, int64_t m, int64_t n, int64_t ld, unsigned long long* rowmax,
+                        unsigned long long* colmax, cudaStream_t s);
 
 // Plane writers. kind 0: residues of trunc(x * 2^exp) (N planes);
 // kind 1: Abar/Bbar = ceil(|x| * 2^exp) (1 plane; exp INT32_MIN = zero line).
@@ -73,7 +78,8 @@ void launch_round_to_f32(const double* x, int64_t rows, int64_t cols, int64_t ld
                          cudaStream_t s);
 
 // ---- K2 (k2_gemm.cu) -------------------------------------------------------
-enum K2Kind { K2_I32 = 0, K2_U8 = 1, K2_MAX = 2, K2_U8ACC = 3 };
+// ACC64: int64 accumulation of the bound product over 2^17 k-chunks (accurate mode, k > 2^19)
+enum K2Kind { K2_I32 = 0, K2_U8 = 1, K2_MAX = 2, K2_U8ACC = 3, K2_ACC64 = 4 };
 struct K2Launch {
     // planes are column-major byte matrices with column pitch lda / ld:
     //   A MN-major (a_mn): k columns of m;  A K-major: m columns of k
@@ -86,8 +92,9 @@ struct K2Launch {
     int64_t out_stride;          // elements between output planes (I32 / U8)
     int n_mod;
     int kind;
-    void* out;  // I32 / U8: [n_mod][n][ldo]
+    void* out;  // I32 / U8: [n_mod][n][ldo]; ACC64: int64 [n][ldo]
     int64_t ldo;
+    bool acc_first = true;  // ACC64: this chunk initialises the sum
     int32_t* rowmax;  // MAX
     int32_t* colmax;
     const DevConsts* c;

@@ -310,10 +310,26 @@ def test_long_k_blocked_path(oracle, k, mode):
         np.testing.assert_array_equal(_bits(got), _bits(want))
 
 
-def test_accurate_k_limit():
+@pytest.mark.parametrize("k", [(1 << 19) + 1000, (1 << 20) + 17])
+def test_accurate_long_k_int64_bound(oracle, k):
+    """accurate mode beyond k = 2^19: entries of the bound product Abar*Bbar reach
+    64*64*k > 2^31, so it accumulates in int64 (scaling.cpp:118-148 keeps it in
+    int64 too). Near-2 entries make every Abar/Bbar entry 64: the row maxima are
+    exactly 4096*k."""
+    m, n = 5, 3
+    rng = np.random.default_rng(k)
+    a = np.asfortranarray(1.99 - 0.01 * rng.random((m, k)))
+    b = np.asfortranarray(1.99 - 0.01 * rng.random((k, n)))
+    b[:, 1] = gen_matrix(k, 1, 0.5, 3)[:, 0]
+    got = gemm_emulated(a, b, EmuConfig(n_moduli=14, mode=ScaleMode.Accurate)).c
+    np.testing.assert_array_equal(_bits(got), _bits(oracle.gemm(a, b, 14, 1)))
+
+
+def test_shard_accurate_long_k_rejected(ctx):
     from paper_2508_03984_b200 import InputError
 
-    a = np.zeros((2, (1 << 19) + 1), order="F")
-    b = np.zeros(((1 << 19) + 1, 2), order="F")
+    k = (1 << 19) + 1
+    A = _dev_colmajor(np.zeros((2, k)))
+    B = _dev_colmajor(np.zeros((k, 2)))
     with pytest.raises(InputError):
-        gemm_emulated(a, b, EmuConfig(n_moduli=8, mode=ScaleMode.Accurate))
+        ctx.shard_begin(A, B, EmuConfig(n_moduli=8, mode=ScaleMode.Accurate))
