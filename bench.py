@@ -320,6 +320,10 @@ def main():
                 "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (dense INT8 = 2 x dense BF16 on sm_100)"
                                 if bf16 else "2 x fallback 1.59 PFLOP/s bf16 (B200_PROFILING.md)"),
                 "stage_ms": {kname: v[0] / max(v[1], 1) for kname, v in prof.items()}}
+    if peaks.get("bf16_tflops_sustained"):
+        # K2 runs inside a long step: the sustained-clock denominator, for reference
+        roofline["peak_sustained"] = 2.0 * peaks["bf16_tflops_sustained"]
+        roofline["frac_sustained"] = achieved / roofline["peak_sustained"]
 
     out = {
         "metric": f"emulated DGEMM TFLOPS (2mnk/s) at n={n}, {args.moduli} moduli, {args.mode} mode",
