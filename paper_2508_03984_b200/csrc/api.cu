@@ -27,6 +27,9 @@
 #include <utility>
 #include <vector>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "ozaki2_b200.h"
 #include "ozk_internal.h"
 
@@ -569,6 +572,155 @@ int64_t host_block_cols(int64_t n) {
     return nb < 512 ? 512 : nb;
 }
 
+// ---- streamed host path (fast mode) -------------------------------------------
+// Fast-mode mu_i depends on row i of A only and nu_j on column j of B, so C
+// block (I, J) can be computed as soon as A's row block I and B's column
+// block J are on the device. The copy stream alternates A_0, B_0, A_1, B_1, ...
+// (A row blocks are pitched copies); each arrival triggers one rectangular
+// region: rows I x all columns that have arrived (after A_I), or all rows that
+// have arrived x columns J (after B_J). K2 therefore starts after 2/P of the
+// inputs instead of after all of A, and the tail after the last byte arrives
+// is one thin region plus its D2H. Results are identical to the unblocked
+// call: every stage is row/column-local in fast mode.
+
+int64_t stream_block(int64_t dim) {
+    int64_t b = (dim + 15) / 16;  // ~16 blocks per operand
+    b = (b + 255) / 256 * 256;    // whole 256-row/column GEMM tiles
+    return b < 512 ? 512 : b;
+}
+
+bool use_streamed(const Job& J, const ozk_config* cfg, double beta) {
+    return J.mode == OZK_FAST && !J.ta && !J.tb && beta == 0.0 && !rounds_inputs(J, cfg) && J.m >= 2048 &&
+           J.n >= 2048 && std::getenv("OZK_HOST_STREAM") == nullptr;
+}
+
+// rows [r0, r0+mr) of A: stats, mu, residue planes
+int stream_a_block(ozk_context* h, Job& J, int64_t r0, int64_t mr) {
+    const size_t es = J.in_f32 ? 4 : 8;
+    const void* a = static_cast<const char*>(J.a) + es * r0;
+    int splits = row_stats_splits(mr, J.k);
+    const int64_t cap = J.splits * J.m / mr;  // the [split][rows] partials live in J.amax / J.asum
+    if (splits > cap) splits = static_cast<int>(cap < 1 ? 1 : cap);
+    launch_row_stats(a, J.in_f32, mr, J.k, J.lda, splits, J.amax, J.asum, J.flags, h->stream);
+    OZK_CUDA(cudaMemsetAsync(J.flags + 1, 0, sizeof(int32_t), h->stream));
+    launch_fast_finalize(J.amax, J.asum, splits, mr, J.k, J.dc, J.mu + r0, J.flags + 1, J.flag_rows, h->stream);
+    launch_fast_exact(a, J.in_f32, 1, J.lda, J.k, J.dc, J.flags + 1, J.flag_rows, J.mu + r0, h->stream);
+    launch_a_planes(a, J.in_f32, mr, J.k, J.lda, J.mu + r0, J.dc, 0, J.pa + r0, J.lda_p, J.pa_stride, h->stream);
+    return check_launch(h, 4);
+}
+
+// C[r0:r0+mr, c0:c0+nc] from the planes (K2 + K3), then its D2H on the copy stream
+int stream_region(ozk_context* h, Job& J, int64_t r0, int64_t mr, int64_t c0, int64_t nc, double alpha, int c_f32,
+                  void* C_host, int64_t ldc, cudaEvent_t done) {
+    {
+        StageTimer t(h, OZK_PROFILE_PRODUCTS);
+        K2Launch L{};
+        L.a_planes = J.pa + r0;  // MN-major: rows are bytes inside a column
+        L.b_planes = J.pb + c0 * J.ld;
+        L.m = mr;
+        L.n = nc;
+        L.k = J.k;
+        L.ld = J.ld;
+        L.lda = J.lda_p;
+        L.a_stride = J.pa_stride;
+        L.b_stride = J.pb_stride;
+        L.n_mod = J.c.n_moduli;
+        L.kind = K2_U8;
+        L.out = J.u + c0 * J.ldu + r0;
+        L.ldo = J.ldu;
+        L.out_stride = J.n * J.ldu;
+        L.c = &J.dc;
+        L.num_sms = h->num_sms;
+        L.sync_counter = reinterpret_cast<unsigned int*>(J.flags + 4);
+        OZK_TRY(launch_k2(L, h->stream));
+        OZK_TRY(check_launch(h, 1));
+    }
+    const size_t cs = c_f32 ? 4 : 8;
+    char* cdev = static_cast<char*>(h->host_c.p) + cs * (c0 * ldc + r0);
+    {
+        StageTimer t(h, OZK_PROFILE_RECONSTRUCT);
+        launch_reconstruct(J.u + c0 * J.ldu + r0, J.ldu, J.n * J.ldu, mr, nc, J.mu + r0, J.nu + c0, J.dc, alpha, 0.0,
+                           cdev, ldc, c_f32, h->stream);
+        OZK_TRY(check_launch(h, 1));
+    }
+    OZK_CUDA(cudaEventRecord(done, h->stream));
+    OZK_CUDA(cudaStreamWaitEvent(h->d2h, done, 0));
+    OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(C_host) + cs * (c0 * ldc + r0), cs * ldc, cdev, cs * ldc, cs * mr,
+                               nc, cudaMemcpyDeviceToHost, h->d2h));
+    return OZK_OK;
+}
+
+int gemm_host_streamed(ozk_context* h, Job& J, double alpha, const void* A, int64_t lda, const void* B, int64_t ldb,
+                       void* C, int64_t ldc, int c_f32) {
+    const size_t es = J.in_f32 ? 4 : 8;
+    const int64_t m = J.m, n = J.n, k = J.k;
+    const int64_t bm = stream_block(m), bn = stream_block(n);
+    const int na = static_cast<int>((m + bm - 1) / bm), nb = static_cast<int>((n + bn - 1) / bn);
+    std::vector<cudaEvent_t> ev(na + nb + na + nb + 1);
+    for (auto& e : ev) OZK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    struct EventGuard {
+        std::vector<cudaEvent_t>& v;
+        ~EventGuard() {
+            for (auto& e : v) cudaEventDestroy(e);
+        }
+    } guard{ev};
+    cudaEvent_t evStart = ev.back();
+    auto ev_a = [&](int i) { return ev[i]; };
+    auto ev_b = [&](int j) { return ev[na + j]; };
+    auto ev_ra = [&](int i) { return ev[na + nb + i]; };
+    auto ev_rb = [&](int j) { return ev[na + nb + na + j]; };
+    OZK_CUDA(cudaEventRecord(evStart, h->stream));
+    OZK_CUDA(cudaStreamWaitEvent(h->h2d, evStart, 0));
+    OZK_CUDA(cudaStreamWaitEvent(h->d2h, evStart, 0));
+    // the copy stream: A_0, B_0, A_1, B_1, ...
+    for (int s = 0; s < na || s < nb; ++s) {
+        if (s < na) {
+            const int64_t r0 = s * bm, mr = std::min(bm, m - r0);
+            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(h->host_a.p) + es * r0, es * lda,
+                                       static_cast<const char*>(A) + es * r0, es * lda, es * mr, k,
+                                       cudaMemcpyHostToDevice, h->h2d));
+            OZK_CUDA(cudaEventRecord(ev_a(s), h->h2d));
+        }
+        if (s < nb) {
+            const int64_t c0 = s * bn, nc = std::min(bn, n - c0);
+            OZK_CUDA(cudaMemcpyAsync(static_cast<char*>(h->host_b.p) + es * ldb * c0,
+                                     static_cast<const char*>(B) + es * ldb * c0, es * ldb * nc,
+                                     cudaMemcpyHostToDevice, h->h2d));
+            OZK_CUDA(cudaEventRecord(ev_b(s), h->h2d));
+        }
+    }
+    StageTimer total(h, OZK_PROFILE_TOTAL);
+    int64_t rows_in = 0, cols_in = 0;  // prefix of A rows / B columns already on the device
+    for (int s = 0; s < na || s < nb; ++s) {
+        if (s < na) {
+            const int64_t r0 = s * bm, mr = std::min(bm, m - r0);
+            OZK_CUDA(cudaStreamWaitEvent(h->stream, ev_a(s), 0));
+            {
+                StageTimer t(h, OZK_PROFILE_SCALE);
+                OZK_TRY(stream_a_block(h, J, r0, mr));
+            }
+            rows_in = r0 + mr;
+            if (cols_in > 0) OZK_TRY(stream_region(h, J, r0, mr, 0, cols_in, alpha, c_f32, C, ldc, ev_ra(s)));
+        }
+        if (s < nb) {
+            const int64_t c0 = s * bn, nc = std::min(bn, n - c0);
+            OZK_CUDA(cudaStreamWaitEvent(h->stream, ev_b(s), 0));
+            {
+                StageTimer t(h, OZK_PROFILE_SCALE);
+                OZK_CUDA(cudaMemsetAsync(J.flags + 2, 0, sizeof(int32_t), h->stream));
+                OZK_TRY(stage_cols(h, J, c0, nc));
+            }
+            {
+                StageTimer t(h, OZK_PROFILE_RESIDUES);
+                OZK_TRY(stage_col_residues(h, J, c0, nc, J.nu, J.pb, J.pb_stride));
+            }
+            cols_in = c0 + nc;
+            if (rows_in > 0) OZK_TRY(stream_region(h, J, 0, rows_in, c0, nc, alpha, c_f32, C, ldc, ev_rb(s)));
+        }
+    }
+    return OZK_OK;
+}
+
 // Host operands: H2D of A, then of B column blocks, on one copy stream; the
 // compute of block j waits for its B block; C block j leaves on a second copy
 // stream while block j+1 computes.
@@ -593,6 +745,12 @@ int gemm_host(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int
     OZK_TRY(setup(h, J, cfg, c, m, n, k, h->host_a.p, lda, h->host_b.p, ldb, true));
     const void* b_src = h->host_b.p;
     const int c_f32 = cfg->c_type == OZK_R32F;
+    if (use_streamed(J, cfg, beta)) {
+        OZK_CUDA(cudaSetDevice(h->device));
+        OZK_TRY(gemm_host_streamed(h, J, alpha, A, lda, B, ldb, C, ldc, c_f32));
+        OZK_CUDA(cudaStreamSynchronize(h->d2h));
+        return finish_check(h, J, h->stream);
+    }
     const int64_t nb = host_block_cols(n);
     const int nblk = static_cast<int>((n + nb - 1) / nb);
     std::vector<cudaEvent_t> ev(2 * nblk + 2);
