@@ -28,8 +28,14 @@ def main():
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     m = k = n
-    pa = torch.randint(-128, 128, (n_mod, k, ctx.plane_ld(m)), dtype=torch.int8, device="cuda")
-    pb = torch.randint(-128, 128, (n_mod, n, ctx.plane_ld(k)), dtype=torch.int8, device="cuda")
+    data = os.environ.get("SWEEP_DATA", "random")  # random | zero | small (|x| <= 3): power vs operand toggling
+    if data == "zero":
+        pa = torch.zeros((n_mod, k, ctx.plane_ld(m)), dtype=torch.int8, device="cuda")
+        pb = torch.zeros((n_mod, n, ctx.plane_ld(k)), dtype=torch.int8, device="cuda")
+    else:
+        lo, hi = (-128, 128) if data == "random" else (-3, 4)
+        pa = torch.randint(lo, hi, (n_mod, k, ctx.plane_ld(m)), dtype=torch.int8, device="cuda")
+        pb = torch.randint(lo, hi, (n_mod, n, ctx.plane_ld(k)), dtype=torch.int8, device="cuda")
     u = torch.empty((n_mod, n, (m + 15) // 16 * 16), dtype=torch.uint8, device="cuda")
     cfg = EmuConfig(n_moduli=n_mod)
     out = []
