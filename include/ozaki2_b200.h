@@ -162,6 +162,28 @@ int ozk_shard_begin(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, i
 int32_t* ozk_shard_rowmax(ozk_handle h);
 int ozk_shard_end(ozk_handle h, double alpha, double beta, void* C, int64_t ldc);
 
+/* Row-streamed column shard (fast mode): A arrives in row blocks — e.g. one
+ * NCCL broadcast per block on another stream — and each block's work starts as
+ * soon as it lands, so the broadcast of A overlaps the residue GEMMs instead of
+ * preceding them. Fast-mode mu_i depends on row i of A only
+ * (scaling.cpp:65-82) and nu_j on column j of B (:84-97), so the blocks are
+ * bit-identical to the whole-A result.
+ *   ozk_shard_stream_begin  K1a + K1b for this shard's columns of B; C, alpha,
+ *                           beta fixed for the call (C = alpha A B + beta C);
+ *   ozk_shard_stream_rows   rows [r0, r0+mr) of A (r0 a multiple of 16) as an
+ *                           mr x k column-major block at A_rows (leading
+ *                           dimension lda_rows >= mr),
+ *                           ordered on the handle's stream after whatever
+ *                           produced it: K1a/K1b of those rows, then K2 + K3
+ *                           of C[r0:r0+mr, shard];
+ *   ozk_shard_stream_end    the non-finite check; the blocks must cover [0, m).
+ * OZK_CONFIG_ERROR for accurate mode (mu needs every column first), transposed
+ * operands or FP64 storage with FP32 precision: those use ozk_shard_begin. */
+int ozk_shard_stream_begin(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, const void* B,
+                           int64_t ldb, double alpha, double beta, void* C, int64_t ldc);
+int ozk_shard_stream_rows(ozk_handle h, int64_t r0, int64_t mr, const void* A_rows, int64_t lda_rows);
+int ozk_shard_stream_end(ozk_handle h);
+
 /* ---- stage-level exports (device pointers; parity / debug) -------------- */
 /* K1a: scale exponents mu_i = 2^mu_exp[i], nu_j = 2^nu_exp[j]
  *      (scale_fast / scale_accurate, scaling.hpp:28-36). */

@@ -32,6 +32,7 @@ EXPORTED_SYMBOLS = (
     "ozk_stage_scale", "ozk_plane_ld", "ozk_stage_residues", "ozk_stage_products", "ozk_stage_reconstruct",
     "ozk_kernel_launches", "ozk_profile", "ozk_profile_read",
     "ozk_shard_begin", "ozk_shard_rowmax", "ozk_shard_end",
+    "ozk_shard_stream_begin", "ozk_shard_stream_rows", "ozk_shard_stream_end",
     "ozk_int8_gemm", "ozk_truncate_scale", "ozk_residues", "ozk_mod_u8_array", "ozk_accumulate", "ozk_crt_reduce",
     "ozk_unscale",
 )
@@ -133,6 +134,10 @@ def load() -> C.CDLL:
     L.ozk_shard_rowmax.restype = p
     L.ozk_shard_rowmax.argtypes = [p]
     L.ozk_shard_end.argtypes = [p, C.c_double, C.c_double, p, i64]
+    L.ozk_shard_stream_begin.argtypes = [p, C.POINTER(OzkConfig), i64, i64, i64, p, i64, C.c_double, C.c_double,
+                                         p, i64]
+    L.ozk_shard_stream_rows.argtypes = [p, i64, i64, p, i64]
+    L.ozk_shard_stream_end.argtypes = [p]
     L.ozk_int8_gemm.argtypes = [p, i64, i64, i64, p, i64, p, i64, p, i64]
     L.ozk_truncate_scale.argtypes = [p, i32, i64, i64, p, i64, p, i32, p, i64]
     L.ozk_residues.argtypes = [p, C.POINTER(OzkConfig), i64, i64, p, i64, p, i64]

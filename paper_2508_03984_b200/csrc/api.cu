@@ -118,6 +118,12 @@ struct ozk_context {
     bool shard_open = false;
     ozk_config shard_cfg{};
     Job shard{};  // plain pointers into this handle's workspace
+    // the row-streamed shard (ozk_shard_stream_*): output and progress
+    bool stream_open = false;
+    double stream_alpha = 1.0, stream_beta = 0.0;
+    void* stream_c = nullptr;
+    int64_t stream_ldc = 0, stream_rows = 0;
+    int stream_c_f32 = 0;
 };
 
 namespace {
@@ -594,24 +600,29 @@ bool use_streamed(const Job& J, const ozk_config* cfg, double beta) {
            J.n >= 2048 && std::getenv("OZK_HOST_STREAM") == nullptr;
 }
 
-// rows [r0, r0+mr) of A: stats, mu, residue planes
-int stream_a_block(ozk_context* h, Job& J, int64_t r0, int64_t mr) {
-    const size_t es = J.in_f32 ? 4 : 8;
-    const void* a = static_cast<const char*>(J.a) + es * r0;
+// rows [r0, r0+mr) of A, stored as an mr x k column-major block at `a` with
+// leading dimension lda: stats, mu, residue planes (fast mode: all row-local)
+int rows_block(ozk_context* h, Job& J, int64_t r0, int64_t mr, const void* a, int64_t lda) {
     int splits = row_stats_splits(mr, J.k);
     const int64_t cap = J.splits * J.m / mr;  // the [split][rows] partials live in J.amax / J.asum
     if (splits > cap) splits = static_cast<int>(cap < 1 ? 1 : cap);
-    launch_row_stats(a, J.in_f32, mr, J.k, J.lda, splits, J.amax, J.asum, J.flags, h->stream);
+    launch_row_stats(a, J.in_f32, mr, J.k, lda, splits, J.amax, J.asum, J.flags, h->stream);
     OZK_CUDA(cudaMemsetAsync(J.flags + 1, 0, sizeof(int32_t), h->stream));
     launch_fast_finalize(J.amax, J.asum, splits, mr, J.k, J.dc, J.mu + r0, J.flags + 1, J.flag_rows, h->stream);
-    launch_fast_exact(a, J.in_f32, 1, J.lda, J.k, J.dc, J.flags + 1, J.flag_rows, J.mu + r0, h->stream);
-    launch_a_planes(a, J.in_f32, mr, J.k, J.lda, J.mu + r0, J.dc, 0, J.pa + r0, J.lda_p, J.pa_stride, h->stream);
+    launch_fast_exact(a, J.in_f32, 1, lda, J.k, J.dc, J.flags + 1, J.flag_rows, J.mu + r0, h->stream);
+    launch_a_planes(a, J.in_f32, mr, J.k, lda, J.mu + r0, J.dc, 0, J.pa + r0, J.lda_p, J.pa_stride, h->stream);
     return check_launch(h, 4);
 }
 
-// C[r0:r0+mr, c0:c0+nc] from the planes (K2 + K3), then its D2H on the copy stream
-int stream_region(ozk_context* h, Job& J, int64_t r0, int64_t mr, int64_t c0, int64_t nc, double alpha, int c_f32,
-                  void* C_host, int64_t ldc, cudaEvent_t done) {
+int stream_a_block(ozk_context* h, Job& J, int64_t r0, int64_t mr) {
+    const size_t es = J.in_f32 ? 4 : 8;
+    return rows_block(h, J, r0, mr, static_cast<const char*>(J.a) + es * r0, J.lda);
+}
+
+// C[r0:r0+mr, c0:c0+nc] = alpha (A B)[region] + beta C[region] from the planes:
+// K2 over the region's tiles, then K3. C is the full device matrix (ldc).
+int region_products(ozk_context* h, Job& J, int64_t r0, int64_t mr, int64_t c0, int64_t nc, double alpha,
+                    double beta, void* C, int64_t ldc, int c_f32) {
     {
         StageTimer t(h, OZK_PROFILE_PRODUCTS);
         K2Launch L{};
@@ -622,6 +633,7 @@ int stream_region(ozk_context* h, Job& J, int64_t r0, int64_t mr, int64_t c0, in
         L.k = J.k;
         L.ld = J.ld;
         L.lda = J.lda_p;
+        L.a_mn = true;
         L.a_stride = J.pa_stride;
         L.b_stride = J.pb_stride;
         L.n_mod = J.c.n_moduli;
@@ -636,13 +648,18 @@ int stream_region(ozk_context* h, Job& J, int64_t r0, int64_t mr, int64_t c0, in
         OZK_TRY(check_launch(h, 1));
     }
     const size_t cs = c_f32 ? 4 : 8;
-    char* cdev = static_cast<char*>(h->host_c.p) + cs * (c0 * ldc + r0);
-    {
-        StageTimer t(h, OZK_PROFILE_RECONSTRUCT);
-        launch_reconstruct(J.u + c0 * J.ldu + r0, J.ldu, J.n * J.ldu, mr, nc, J.mu + r0, J.nu + c0, J.dc, alpha, 0.0,
-                           cdev, ldc, c_f32, h->stream);
-        OZK_TRY(check_launch(h, 1));
-    }
+    StageTimer t(h, OZK_PROFILE_RECONSTRUCT);
+    launch_reconstruct(J.u + c0 * J.ldu + r0, J.ldu, J.n * J.ldu, mr, nc, J.mu + r0, J.nu + c0, J.dc, alpha, beta,
+                       static_cast<char*>(C) + cs * (c0 * ldc + r0), ldc, c_f32, h->stream);
+    return check_launch(h, 1);
+}
+
+// C[r0:r0+mr, c0:c0+nc] from the planes (K2 + K3), then its D2H on the copy stream
+int stream_region(ozk_context* h, Job& J, int64_t r0, int64_t mr, int64_t c0, int64_t nc, double alpha, int c_f32,
+                  void* C_host, int64_t ldc, cudaEvent_t done) {
+    OZK_TRY(region_products(h, J, r0, mr, c0, nc, alpha, 0.0, h->host_c.p, ldc, c_f32));
+    const size_t cs = c_f32 ? 4 : 8;
+    const char* cdev = static_cast<const char*>(h->host_c.p) + cs * (c0 * ldc + r0);
     OZK_CUDA(cudaEventRecord(done, h->stream));
     OZK_CUDA(cudaStreamWaitEvent(h->d2h, done, 0));
     OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(C_host) + cs * (c0 * ldc + r0), cs * ldc, cdev, cs * ldc, cs * mr,
@@ -1066,6 +1083,82 @@ int ozk_shard_end(ozk_handle h, double alpha, double beta, void* C, int64_t ldc)
         OZK_TRY(stage_row_residues(h, J, J.mu, J.pa));
     }
     OZK_TRY(compute_block(h, J, 0, J.n, alpha, beta, C, ldc, h->shard_cfg.c_type == OZK_R32F));
+    return finish_check(h, J, h->stream);
+}
+
+int ozk_shard_stream_begin(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, const void* B,
+                           int64_t ldb, double alpha, double beta, void* C, int64_t ldc) {
+    if (!h) return OZK_INPUT_ERROR;
+    ozk_constants c;
+    OZK_TRY(resolve(cfg, c));
+    OZK_TRY(validate(cfg, c, m, n, k, m, ldb));
+    if (cfg->mode != OZK_FAST || (cfg->flags & (OZK_FLAG_TRANS_A | OZK_FLAG_TRANS_B)) ||
+        (c.precision == OZK_FP32 && cfg->a_type == OZK_R64F)) {
+        // accurate-mode mu needs every column's bound first; rounding / transposed
+        // operands keep the whole-A path (ozk_shard_begin)
+        set_error("row-streamed shard: fast mode, untransposed operands stored in the compute precision only");
+        return OZK_CONFIG_ERROR;
+    }
+    if (ldc < m) {
+        set_error("gemm_emulated: ldc < m");
+        return OZK_INPUT_ERROR;
+    }
+    OZK_CUDA(cudaSetDevice(h->device));
+    Job& J = h->shard;
+    J = Job{};
+    OZK_TRY(setup(h, J, cfg, c, m, n, k, nullptr, m, B, ldb, true));
+    h->shard_cfg = *cfg;
+    h->shard_cfg.constants = nullptr;
+    h->stream_alpha = alpha;
+    h->stream_beta = beta;
+    h->stream_c = C;
+    h->stream_ldc = ldc;
+    h->stream_c_f32 = cfg->c_type == OZK_R32F;
+    h->stream_rows = 0;
+    {
+        StageTimer t(h, OZK_PROFILE_SCALE);
+        OZK_TRY(stage_cols(h, J, 0, n));
+    }
+    {
+        StageTimer t(h, OZK_PROFILE_RESIDUES);
+        OZK_TRY(stage_col_residues(h, J, 0, n, J.nu, J.pb, J.pb_stride));
+    }
+    h->stream_open = true;
+    return OZK_OK;
+}
+
+int ozk_shard_stream_rows(ozk_handle h, int64_t r0, int64_t mr, const void* A_rows, int64_t lda_rows) {
+    if (!h || !h->stream_open) {
+        set_error("ozk_shard_stream_rows without ozk_shard_stream_begin");
+        return OZK_INPUT_ERROR;
+    }
+    Job& J = h->shard;
+    if (r0 < 0 || mr < 1 || r0 + mr > J.m || lda_rows < mr || !A_rows || r0 % 16 != 0) {
+        set_error("ozk_shard_stream_rows: row block outside [0, m), lda < rows, or r0 not a multiple of 16");
+        return OZK_INPUT_ERROR;
+    }
+    OZK_CUDA(cudaSetDevice(h->device));
+    {
+        StageTimer t(h, OZK_PROFILE_SCALE);
+        OZK_TRY(rows_block(h, J, r0, mr, A_rows, lda_rows));
+    }
+    h->stream_rows += mr;
+    return region_products(h, J, r0, mr, 0, J.n, h->stream_alpha, h->stream_beta, h->stream_c, h->stream_ldc,
+                           h->stream_c_f32);
+}
+
+int ozk_shard_stream_end(ozk_handle h) {
+    if (!h || !h->stream_open) {
+        set_error("ozk_shard_stream_end without ozk_shard_stream_begin");
+        return OZK_INPUT_ERROR;
+    }
+    h->stream_open = false;
+    Job& J = h->shard;
+    if (h->stream_rows != J.m) {
+        set_error("ozk_shard_stream_end: the row blocks do not cover the m rows of A");
+        return OZK_INPUT_ERROR;
+    }
+    OZK_CUDA(cudaSetDevice(h->device));
     return finish_check(h, J, h->stream);
 }
 

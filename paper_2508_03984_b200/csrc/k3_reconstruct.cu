@@ -8,32 +8,19 @@
 //   Q  = rint(P_inv * c1);  C'' = fma(-P2, Q, fma(-P1, Q, c1) + c2)
 //   C  = ldexp(C'', -(e_mu_i + e_nu_j))
 // then the optional alpha/beta extension in FP64 and the FP32 down-cast of
-// to_fp32 (emulator.cpp:110-115) when C is single precision. Each thread owns
-// eight consecutive rows: one 64-bit load per plane, 64 B of C out, so a warp
-// moves 256 B per plane and 2 KB of C — HBM-bound at N + 8 bytes per element.
+// to_fp32 (emulator.cpp:110-115) when C is single precision. The planes reach
+// shared memory by bulk copies (below); each consumer thread owns eight
+// consecutive rows: one 8-byte shared load per plane, 64 B of C out with two
+// 32-byte stores. Algorithmic traffic N + 8 bytes per element; the exact FP64
+// chain (4 FP64 ops per element and modulus) makes it issue-bound on B200.
+#include <algorithm>
 #include <cstdlib>
+#include <string>
 
 #include "ozk_device.cuh"
 
 namespace ozk {
 namespace {
-
-// Rows per thread R: one R-byte load per plane, 8R bytes of C out. The plane
-// words of all N moduli are loaded up front, so registers grow with R x kMaxMod:
-// both are template parameters (kMaxMod = the modulus count rounded up to a
-// bucket) to keep occupancy up.
-template <int R>
-struct PlaneWord;
-template <>
-struct PlaneWord<8> {
-    using T = uint2;
-    static __device__ __forceinline__ uint32_t part(const uint2& w, int q) { return q < 4 ? w.x : w.y; }
-};
-template <>
-struct PlaneWord<4> {
-    using T = uint32_t;
-    static __device__ __forceinline__ uint32_t part(const uint32_t& w, int) { return w; }
-};
 
 // ldexp(x, e) as one multiply by 2^e when that is exact-and-correctly-rounded
 // (2^e normal, result normal); CUDA's general ldexp otherwise (subnormal or
@@ -63,163 +50,312 @@ __device__ __forceinline__ void st_v8_f32(float* p, const float* v) {
                  : "memory");
 }
 
-template <bool kF32Out, bool kPlain, bool kFp64Tables, int kRows, int kMaxMod>
-__global__ void __launch_bounds__(128)
-    reconstruct_kernel(const uint8_t* __restrict__ u, int64_t ldu, int64_t plane_stride, int64_t m, int64_t n,
-                       const int32_t* __restrict__ mu_exp, const int32_t* __restrict__ nu_exp, const DevConsts c,
-                       double alpha, double beta, void* __restrict__ C, int64_t ldc, bool vec_ok) {
-    const int64_t j = blockIdx.x;
-    const int64_t i0 = (static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x) * kRows;
-    if (i0 >= m) return;
-    double c1[kRows], c2[kRows];
-#pragma unroll
-    for (int q = 0; q < kRows; ++q) c1[q] = c2[q] = 0.0;
-    const uint8_t* src = u + j * ldu + i0;
+// ---- bulk-copy variant (the production path) ------------------------------
+// Persistent, warp-specialised blocks walk (row chunk, column) tiles of
+// kConsumers * R rows. One producer lane issues each tile's N plane slices as
+// 1-D bulk copies (cp.async.bulk, the TMA engine) into a kStages ring of shared
+// buffers (full/empty mbarriers); the consumer warps reconstruct from shared
+// memory, R consecutive rows per thread (one 16-byte LDS per plane). All N
+// loads of a tile are in flight at once, independent of register pressure or
+// of how ptxas schedules the FP64 chain (register-staged loads got interleaved
+// with it), and tiles t+1.. stream in while tile t computes. No block-wide
+// barrier: each consumer warp releases a slot on its own.
+// ring depth: two slots (1024 rows x N planes each); deeper rings and 8-warp
+// blocks measured the same (K3 is issue-bound)
+template <int kMaxMod>
+__host__ __device__ constexpr int bulk_stages() {
+    return 2;
+}
+
+// how C1 = sum s1_i u_i is formed (both equal the reference's rounded sum):
+// FP32 tables carry the full-width s1 (crt_tables.cpp:160-163), so the
+// reference's two roundings stay; with FP64 tables every product and partial
+// sum is exact (beta_i construction, crt_tables.cpp:165-169), so one DFMA.
+// (An exact int64 sum on the IMAD pipe measured 15 % slower: IMAD.WIDE is
+// the expensive op there.)
+constexpr int kC1TwoOp = 0, kC1Dfma = 1;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bulk_mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void bulk_mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(0x12F0000000000000ull)  // evict-first: U is read exactly once
+        : "memory");
+}
+
+// ldexp(x, e) by moving the exponent field when x and the result are normal
+// (exactly what ldexp returns there); scale_pow2 covers zero, subnormal,
+// non-finite and out-of-range cases
+__device__ __forceinline__ double unscale_fast(double x, int e) {
+    const int hi = __double2hiint(x);
+    const int ex = (hi >> 20) & 0x7ff;
+    if (ex != 0 && static_cast<unsigned>(ex + e - 1) < 2046u)
+        return __hiloint2double(hi + static_cast<int>(static_cast<unsigned>(e) << 20), __double2loint(x));
+    return scale_pow2(x, e);
+}
+
+template <int R>
+struct BulkWord;
+template <>
+struct BulkWord<8> {
+    using T = uint2;
+    static __device__ __forceinline__ uint32_t part(const uint2& w, int q) { return q < 4 ? w.x : w.y; }
+};
+
+template <bool kF32Out, bool kPlain, int kC1, int kMaxMod, int R, int kConsumers, int kStages>
+__global__ void __launch_bounds__(kConsumers + 32, 512 / kConsumers)
+    reconstruct_bulk_kernel(const uint8_t* __restrict__ u, int64_t ldu, int64_t plane_stride, int64_t m, int64_t n,
+                            int64_t row_chunks, const int32_t* __restrict__ mu_exp, const int32_t* __restrict__ nu_exp,
+                            const DevConsts c, double alpha, double beta, void* __restrict__ C, int64_t ldc,
+                            bool vec_ok) {
+    constexpr int kTile = kConsumers * R;  // rows per tile
+    extern __shared__ __align__(128) uint8_t sbuf[];  // [kStages][kMaxMod][kTile]
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
     const int n_mod = c.n;
-    // all plane loads first (predicated, compile-time indices: registers), so
-    // a thread has its N loads in flight at once instead of one per FP chain step
-    using W = PlaneWord<kRows>;
-    typename W::T w[kMaxMod];
-#pragma unroll
-    for (int t = 0; t < kMaxMod; ++t)
-        w[t] = t < n_mod ? __ldg(reinterpret_cast<const typename W::T*>(src + t * plane_stride)) : typename W::T{};
-#pragma unroll
-    for (int t = 0; t < kMaxMod; ++t) {  // compile-time bound: constants become immediates
-        if (t < n_mod) {
-#pragma unroll
-            for (int q = 0; q < kRows; ++q) {
-                const uint32_t word = W::part(w[t], q);
-                const uint32_t ub = __byte_perm(word, 0u, 0x4440u | (q & 3));  // byte q, zero-extended
-                // V = 2^52 + u exactly (no conversion instruction); v = u
-                const double V = __hiloint2double(0x43300000, static_cast<int>(ub));
-                const double v = __dsub_rn(V, 0x1.0p52);
-                // FP64 tables: s1*u is exact and so is the running sum (beta_i
-                // construction), so the fused form equals the reference's
-                // mul-then-add bit for bit. FP32 tables carry the full-width s1
-                // (crt_tables.cpp:160-163): keep the two roundings there.
-                c1[q] = kFp64Tables ? __fma_rn(c.s1[t], v, c1[q]) : __dadd_rn(c1[q], __dmul_rn(c.s1[t], v));
-                // fl(s2 u) = fma(s2, 2^52 + u, -s2 2^52): the reference's rounded
-                // product (emulator.cpp:53), then its rounded sum
-                c2[q] = __dadd_rn(c2[q], __fma_rn(c.s2[t], V, c.s2_m52[t]));
-            }
+    const int64_t tiles = row_chunks * n;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            bulk_mbar_init(smem_addr(&full[s]), 1);
+            bulk_mbar_init(smem_addr(&empty[s]), kConsumers / 32);
         }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    const int ne = nu_exp[j];
-    // full 8-row groups with aligned mu / C use 32-byte vector accesses: a
-    // warp's C stores then cover whole sectors instead of 8-byte pieces at a
-    // 64-byte lane stride
-    const bool vec = kRows == 8 && vec_ok && i0 + kRows <= m;
-    int me[kRows];
-    if (vec) {
-        ld_nc_v8(mu_exp + i0, me);
-    } else {
-#pragma unroll
-        for (int q = 0; q < kRows; ++q) me[q] = i0 + q < m ? mu_exp[i0 + q] : 0;
-    }
-    double r[kRows];
-#pragma unroll
-    for (int q = 0; q < kRows; ++q) {
-        const double qv = rint(__dmul_rn(c.P_inv, c1[q]));
-        const double cpp = __fma_rn(-c.P2, qv, __dadd_rn(__fma_rn(-c.P1, qv, c1[q]), c2[q]));
-        r[q] = scale_pow2(cpp, -(me[q] + ne));
-    }
-    if (!kPlain) {
-#pragma unroll
-        for (int q = 0; q < kRows; ++q) {
-            const int64_t i = i0 + q;
-            const double old = (beta != 0.0 && i < m)
-                                   ? (kF32Out ? static_cast<double>(static_cast<float*>(C)[i + j * ldc])
-                                              : static_cast<double*>(C)[i + j * ldc])
-                                   : 0.0;
-            r[q] = __dadd_rn(__dmul_rn(alpha, r[q]), __dmul_rn(beta, old));
+    __syncthreads();
+    // tile = chunk + row_chunks * j; this block takes blockIdx.x, +gridDim.x, ...
+    const int64_t dj = gridDim.x / row_chunks, dr = gridDim.x % row_chunks;
+    int64_t j = blockIdx.x / row_chunks, chunk = blockIdx.x % row_chunks;
+    auto advance = [&]() {
+        chunk += dr;
+        j += dj;
+        if (chunk >= row_chunks) {
+            chunk -= row_chunks;
+            ++j;
         }
-    }
-    if (vec) {
-        if constexpr (kF32Out) {
-            float f[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) f[q] = __double2float_rn(r[q]);
-            st_v8_f32(static_cast<float*>(C) + i0 + j * ldc, f);
-        } else {
-            st_v4_f64(static_cast<double*>(C) + i0 + j * ldc, r);
-            st_v4_f64(static_cast<double*>(C) + i0 + 4 + j * ldc, r + 4);
+    };
+
+    if (threadIdx.x >= kConsumers) {  // producer warp: one lane issues
+        if (threadIdx.x != kConsumers) return;
+        for (int64_t k = 0, tile = blockIdx.x; tile < tiles; ++k, tile += gridDim.x, advance()) {
+            const int s = static_cast<int>(k % kStages);
+            const uint32_t ph = static_cast<uint32_t>((k / kStages) & 1);
+            bulk_mbar_wait(smem_addr(&empty[s]), ph ^ 1u);
+            const int64_t i0 = chunk * kTile;
+            const int64_t rows = m - i0 < kTile ? m - i0 : kTile;
+            const uint32_t bytes = static_cast<uint32_t>((rows + 15) & ~int64_t(15));
+            const uint32_t fb = smem_addr(&full[s]);
+            bulk_expect_tx(fb, bytes * n_mod);
+            const uint8_t* src = u + j * ldu + i0;
+            const uint32_t dst = smem_addr(sbuf) + s * kMaxMod * kTile;
+            for (int t = 0; t < n_mod; ++t) bulk_g2s(dst + t * kTile, src + t * plane_stride, bytes, fb);
         }
         return;
     }
+
+    using W = BulkWord<R>;
+    const int lane = threadIdx.x & 31;
+    for (int64_t k = 0, tile = blockIdx.x; tile < tiles; ++k, tile += gridDim.x, advance()) {
+        const int s = static_cast<int>(k % kStages);
+        const int64_t i0 = chunk * kTile + threadIdx.x * R;
+        // the exponents do not depend on the planes: load them before waiting
+        const bool vec = vec_ok && i0 + R <= m;
+        int me[R];
+        if (vec) {
 #pragma unroll
-    for (int q = 0; q < kRows; ++q) {
-        const int64_t i = i0 + q;
-        if (i >= m) break;
-        if (kF32Out)
-            static_cast<float*>(C)[i + j * ldc] = __double2float_rn(r[q]);
-        else
-            static_cast<double*>(C)[i + j * ldc] = r[q];
+            for (int v = 0; v < R; v += 8) ld_nc_v8(mu_exp + i0 + v, me + v);
+        } else {
+#pragma unroll
+            for (int q = 0; q < R; ++q) me[q] = i0 + q < m ? mu_exp[i0 + q] : 0;
+        }
+        const int ne = nu_exp[j];
+        bulk_mbar_wait(smem_addr(&full[s]), static_cast<uint32_t>((k / kStages) & 1));
+        if (i0 < m) {
+            const uint8_t* sp = sbuf + s * kMaxMod * kTile + threadIdx.x * R;
+            double c2[R];
+            double c1[R];
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                c1[q] = c2[q] = 0.0;
+            }
+            // past n_mod the tables are zero (to_dev zero-fills them): those terms
+            // add +0 to non-negative sums, exact, and keep the chain branch-free
+#pragma unroll
+            for (int t = 0; t < kMaxMod; ++t) {
+                typename W::T w{};
+                if (t < n_mod) w = *reinterpret_cast<const typename W::T*>(sp + t * kTile);
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const uint32_t ub = __byte_perm(W::part(w, q), 0u, 0x4440u | (q & 3));
+                    const double V = __hiloint2double(0x43300000, static_cast<int>(ub));  // 2^52 + u
+                    if constexpr (kC1 == kC1Dfma) {  // exact products and sums: one DFMA
+                        c1[q] = __fma_rn(c.s1[t], __dsub_rn(V, 0x1.0p52), c1[q]);
+                    } else {
+                        c1[q] = __dadd_rn(c1[q], __dmul_rn(c.s1[t], __dsub_rn(V, 0x1.0p52)));
+                    }
+                    c2[q] = __dadd_rn(c2[q], __fma_rn(c.s2[t], V, c.s2_m52[t]));
+                }
+            }
+            double r[R];
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const double qv = rint(__dmul_rn(c.P_inv, c1[q]));
+                const double cpp = __fma_rn(-c.P2, qv, __dadd_rn(__fma_rn(-c.P1, qv, c1[q]), c2[q]));
+                r[q] = unscale_fast(cpp, -(me[q] + ne));
+            }
+            if (!kPlain) {
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const int64_t i = i0 + q;
+                    const double old = (beta != 0.0 && i < m)
+                                           ? (kF32Out ? static_cast<double>(static_cast<float*>(C)[i + j * ldc])
+                                                      : static_cast<double*>(C)[i + j * ldc])
+                                           : 0.0;
+                    r[q] = __dadd_rn(__dmul_rn(alpha, r[q]), __dmul_rn(beta, old));
+                }
+            }
+            if (vec) {
+                if constexpr (kF32Out) {
+#pragma unroll
+                    for (int v = 0; v < R; v += 8) {
+                        float f[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) f[q] = __double2float_rn(r[v + q]);
+                        st_v8_f32(static_cast<float*>(C) + i0 + v + j * ldc, f);
+                    }
+                } else {
+#pragma unroll
+                    for (int v = 0; v < R; v += 4) st_v4_f64(static_cast<double*>(C) + i0 + v + j * ldc, r + v);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const int64_t i = i0 + q;
+                    if (i < m) {
+                        if (kF32Out)
+                            static_cast<float*>(C)[i + j * ldc] = __double2float_rn(r[q]);
+                        else
+                            static_cast<double*>(C)[i + j * ldc] = r[q];
+                    }
+                }
+            }
+        }
+        // this warp is done with slot s (every LDS result has been consumed)
+        __syncwarp();
+        if (lane == 0) bulk_mbar_arrive(smem_addr(&empty[s]));
     }
 }
 
-int k3_rows() {
-    static const int r = [] {
-        const char* e = std::getenv("OZK_K3_ROWS");
-        return e && std::atoi(e) == 4 ? 4 : 8;
-    }();
-    return r;
+template <bool kF32Out, bool kPlain, int kC1, int kMaxMod, int R, int kConsumers = 128,
+          int kStages = bulk_stages<kMaxMod>()>
+void launch_bulk_t(int num_sms, cudaStream_t s, const uint8_t* u, int64_t ldu, int64_t stride, int64_t m, int64_t n,
+                   const int32_t* mu_exp, const int32_t* nu_exp, const DevConsts& c, double alpha, double beta,
+                   void* C, int64_t ldc, bool vec_ok) {
+    constexpr int kTile = kConsumers * R;
+    constexpr int kBulkThreads = kConsumers + 32;  // + one producer warp
+    auto kern = reconstruct_bulk_kernel<kF32Out, kPlain, kC1, kMaxMod, R, kConsumers, kStages>;
+    const int smem = kStages * kMaxMod * kTile;
+    static bool attr = false;  // per instantiation
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        attr = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBulkThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t row_chunks = (m + kTile - 1) / kTile;
+    const int64_t tiles = row_chunks * n;
+    const int64_t grid = std::min<int64_t>(tiles, static_cast<int64_t>(num_sms) * per_sm);
+    kern<<<static_cast<unsigned>(grid), kBulkThreads, smem, s>>>(u, ldu, stride, m, n, row_chunks, mu_exp, nu_exp, c,
+                                                                 alpha, beta, C, ldc, vec_ok);
 }
 
-template <bool kF32Out, bool kPlain, bool kFp64, int kRows>
-void launch_rows(int n_mod, dim3 grid, cudaStream_t s, const uint8_t* u, int64_t ldu, int64_t stride, int64_t m,
-                 int64_t n, const int32_t* mu_exp, const int32_t* nu_exp, const DevConsts& c, double alpha,
-                 double beta, void* C, int64_t ldc) {
-    // vector path: 32-byte aligned mu and C columns
-    const int esz = kF32Out ? 4 : 8;
-    const bool vec_ok = (reinterpret_cast<uintptr_t>(mu_exp) % 32 == 0) &&
-                        (reinterpret_cast<uintptr_t>(C) % 32 == 0) && ((ldc * esz) % 32 == 0);
-#define OZK_K3(MAXN)                                                                                       \
-    reconstruct_kernel<kF32Out, kPlain, kFp64, kRows, MAXN>                                                \
-        <<<grid, 128, 0, s>>>(u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, C, ldc, vec_ok)
-    if (n_mod <= 8)
-        OZK_K3(8);
-    else if (n_mod <= 12)
-        OZK_K3(12);
-    else if (n_mod <= 14)
-        OZK_K3(14);
-    else if (n_mod <= 16)
-        OZK_K3(16);
+template <bool kF32Out, bool kPlain, int kC1>
+void launch_bulk(int num_sms, cudaStream_t s, const uint8_t* u, int64_t ldu, int64_t stride, int64_t m, int64_t n,
+                 const int32_t* mu_exp, const int32_t* nu_exp, const DevConsts& c, double alpha, double beta, void* C,
+                 int64_t ldc, bool vec_ok) {
+#define OZK_K3B(MAXN, R)                                                                                          \
+    launch_bulk_t<kF32Out, kPlain, kC1, MAXN, R>(num_sms, s, u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, \
+                                                    C, ldc, vec_ok)
+    if (c.n <= 8)
+        OZK_K3B(8, 8);
+    else if (c.n <= 12)
+        OZK_K3B(12, 8);
+    else if (c.n <= 14)
+        OZK_K3B(14, 8);
+    else if (c.n <= 16)
+        OZK_K3B(16, 8);
     else
-        OZK_K3(OZK_MAX_MODULI);
-#undef OZK_K3
+        OZK_K3B(OZK_MAX_MODULI, 8);
+#undef OZK_K3B
+}
+
+bool k3_bulk() {
+    static const bool b = [] {
+        const char* e = std::getenv("OZK_K3_BULK");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return b;
 }
 
 template <bool kF32Out, bool kPlain>
 void launch_variant(const uint8_t* u, int64_t ldu, int64_t stride, int64_t m, int64_t n, const int32_t* mu_exp,
                     const int32_t* nu_exp, const DevConsts& c, double alpha, double beta, void* C, int64_t ldc,
                     cudaStream_t s) {
-    // with more than 16 planes the 8-row variant's prefetched words no longer stay
-    // in registers (ptxas sinks the loads into the FP64 chain): 4 rows there
-    const int rows = c.n > 16 ? 4 : k3_rows();
-    dim3 grid(static_cast<unsigned>(n), static_cast<unsigned>((m + 128 * rows - 1) / (128 * rows)));
-    const bool fp64 = c.precision == OZK_FP64;
-    if (rows == 8) {
-        if (fp64)
-            launch_rows<kF32Out, kPlain, true, 8>(c.n, grid, s, u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta,
-                                                   C, ldc);
-        else
-            launch_rows<kF32Out, kPlain, false, 8>(c.n, grid, s, u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha,
-                                                    beta, C, ldc);
-    } else {
-        if (fp64)
-            launch_rows<kF32Out, kPlain, true, 4>(c.n, grid, s, u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta,
-                                                   C, ldc);
-        else
-            launch_rows<kF32Out, kPlain, false, 4>(c.n, grid, s, u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha,
-                                                    beta, C, ldc);
-    }
+    const int esz = kF32Out ? 4 : 8;
+    const bool vec_ok = (reinterpret_cast<uintptr_t>(mu_exp) % 32 == 0) && (reinterpret_cast<uintptr_t>(C) % 32 == 0) &&
+                        ((ldc * esz) % 32 == 0);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (c.precision == OZK_FP64)
+        launch_bulk<kF32Out, kPlain, kC1Dfma>(sms, s, u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, C, ldc,
+                                              vec_ok);
+    else
+        launch_bulk<kF32Out, kPlain, kC1TwoOp>(sms, s, u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, C, ldc,
+                                               vec_ok);
 }
 
 }  // namespace
 
+// k3_regs.cu: the register-staged kernel (any layout)
+void launch_reconstruct_regs(const uint8_t* u, int64_t ldu, int64_t stride, int64_t m, int64_t n,
+                             const int32_t* mu_exp, const int32_t* nu_exp, const DevConsts& c, double alpha,
+                             double beta, void* C, int64_t ldc, int c_is_f32, cudaStream_t s);
+
 void launch_reconstruct(const uint8_t* u, int64_t ldu, int64_t stride, int64_t m, int64_t n, const int32_t* mu_exp,
                         const int32_t* nu_exp, const DevConsts& c, double alpha, double beta, void* C, int64_t ldc,
                         int c_is_f32, cudaStream_t s) {
+    // bulk copies need 16-byte aligned slices, i.e. the [N][n][ldu] layout with
+    // 16-byte ldu and plane stride (a partial chunk's over-read stays inside the
+    // column's ldu padding); other layouts (stage API callers) take the
+    // register-staged kernel, as does OZK_K3_BULK=0 (A/B timing)
+    const bool bulk_ok =
+        reinterpret_cast<uintptr_t>(u) % 16 == 0 && ldu % 16 == 0 && stride % 16 == 0 && ldu >= m && k3_bulk();
+    if (!bulk_ok) {
+        launch_reconstruct_regs(u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, C, ldc, c_is_f32, s);
+        return;
+    }
     const bool plain = alpha == 1.0 && beta == 0.0;
     if (c_is_f32) {
         if (plain)

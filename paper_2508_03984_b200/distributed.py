@@ -10,6 +10,14 @@ accurate-mode row bound: mu_i needs max_j of (Abar Bbar)_ij over ALL columns
   * the m int32 partial row maxima — one all-reduce(MAX), accurate mode only.
 The concatenated shards are bit-identical to the single-process result.
 
+Fast mode streams A by row blocks (``row_block``): mu_i depends on row i of A
+only, so each block's residues, GEMMs and reconstruction start as soon as that
+block's broadcast lands, and the broadcast of A overlaps the residue GEMMs of
+the blocks before it (engine calls shard_stream_begin / _rows / _end, backed
+by ozk_shard_stream_*). Blocks travel packed (mr x k, contiguous) because a
+row block of a column-major A is strided; the source packs them on a side
+stream and computes on its own A directly.
+
 ``engine`` is anything with shard_begin(A, B_local, cfg), shard_rowmax() ->
 tensor and shard_end(C_local, alpha, beta): the GPU ``Context`` here, or the
 CPU stand-in the gloo tests use to exercise exactly this exchange logic.
@@ -29,10 +37,33 @@ def column_shard(n: int, world: int, rank: int) -> tuple[int, int]:
     return j0, base + (1 if rank < extra else 0)
 
 
+def row_blocks(m: int, row_block: int, first: int | None = None) -> list[tuple[int, int]]:
+    """[(r0, mr)] covering [0, m): a smaller first block (its broadcast is the
+    only one nothing overlaps), then blocks of row_block rows. Every r0 is a
+    multiple of 16 (ozk_shard_stream_rows: the residue GEMM's operand base
+    must be 16-byte aligned), so sizes are rounded up to multiples of 16."""
+    row_block = max(16, (row_block + 15) // 16 * 16)
+    first = first if first is not None else row_block // 4
+    first = min(max(16, (first + 15) // 16 * 16), m)
+    out = [(0, first)]
+    r0 = first
+    while r0 < m:
+        mr = min(row_block, m - r0)
+        out.append((r0, mr))
+        r0 += mr
+    return out
+
+
 def gemm_sharded(engine, A, B_local, cfg, C_local, alpha: float = 1.0, beta: float = 0.0, group=None,
-                 src: int = 0, broadcast_a: bool = True) -> None:
+                 src: int = 0, broadcast_a: bool = True, row_block: int | None = 2048) -> None:
     """This rank's column shard of C = alpha A B + beta C (A column-major, the
-    same shape on every rank; only ``src``'s contents matter when broadcasting)."""
+    same shape on every rank; only ``src``'s contents matter when broadcasting).
+    Fast mode with ``row_block`` set streams A by row blocks; otherwise A is
+    broadcast whole before the shard runs."""
+    multi = dist.is_initialized() and dist.get_world_size(group) > 1
+    if row_block and cfg.mode == ScaleMode.Fast and hasattr(engine, "shard_stream_begin"):
+        _gemm_streamed(engine, A, B_local, cfg, C_local, alpha, beta, group, src, broadcast_a and multi, row_block)
+        return
     if broadcast_a and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.broadcast(_storage(A), src=src, group=group)
     engine.shard_begin(A, B_local, cfg)
@@ -49,3 +80,44 @@ def _storage(t: torch.Tensor) -> torch.Tensor:
     if tt.is_contiguous():
         return tt
     raise ValueError("A must be a dense column-major (or row-major) matrix")
+
+
+def _gemm_streamed(engine, A, B_local, cfg, C_local, alpha, beta, group, src, broadcast, row_block):
+    m, k = A.shape
+    blocks = row_blocks(m, row_block)
+    engine.shard_stream_begin(m, k, B_local, cfg, C_local, alpha, beta)
+    if not broadcast:
+        for r0, mr in blocks:
+            engine.shard_stream_rows(r0, A[r0:r0 + mr])
+        engine.shard_stream_end()
+        return
+    is_src = dist.get_rank() == src
+    # packed (mr x k column-major) block buffers; every broadcast is issued up
+    # front, so the comm stream runs ahead of the compute that waits on it
+    packs = [A.new_empty((k, mr)).t() for _, mr in blocks]
+    works = []
+    side = None
+    if A.is_cuda and is_src:
+        side = torch.cuda.Stream(device=A.device)
+        side.wait_stream(torch.cuda.current_stream(A.device))
+    for (r0, mr), pack in zip(blocks, packs):
+        if is_src:
+            if side is not None:
+                with torch.cuda.stream(side):
+                    pack.copy_(A[r0:r0 + mr])
+                    works.append(dist.broadcast(_storage(pack), src=src, group=group, async_op=True))
+            else:
+                pack.copy_(A[r0:r0 + mr])
+                works.append(dist.broadcast(_storage(pack), src=src, group=group, async_op=True))
+        else:
+            works.append(dist.broadcast(_storage(pack), src=src, group=group, async_op=True))
+    for (r0, mr), pack, work in zip(blocks, packs, works):
+        if is_src:
+            engine.shard_stream_rows(r0, A[r0:r0 + mr])  # the root's own rows need no wait
+        else:
+            work.wait()  # the compute stream waits for this block only
+            engine.shard_stream_rows(r0, pack)
+    engine.shard_stream_end()
+    if is_src:
+        for work in works:  # the packs stay alive until their sends are done
+            work.wait()

@@ -221,6 +221,25 @@ class Context:
         _lib.check(self._lib.ozk_shard_end(self.handle, float(alpha), float(beta), C_out.data_ptr(),
                                            _colmajor_ld(C_out)))
 
+    # ---- row-streamed column shard (fast mode; A arrives in row blocks) --------------
+    def shard_stream_begin(self, m: int, k: int, B, cfg: EmuConfig, C_out, alpha: float = 1.0,
+                           beta: float = 0.0) -> None:
+        """B's columns (this shard) are scaled and reduced now; C_out (m x n, FP64
+        or FP32) receives alpha A B + beta C_out as the row blocks of A arrive."""
+        n = B.shape[1]
+        self._stream_conf = _config(cfg, _dtype_code(B), _dtype_code(C_out))
+        _lib.check(self._lib.ozk_shard_stream_begin(self.handle, C.byref(self._stream_conf), m, n, k, B.data_ptr(),
+                                                    _colmajor_ld(B), float(alpha), float(beta), C_out.data_ptr(),
+                                                    _colmajor_ld(C_out)))
+
+    def shard_stream_rows(self, r0: int, A_rows) -> None:
+        """rows [r0, r0 + A_rows.shape[0]) of A as a column-major device block"""
+        _lib.check(self._lib.ozk_shard_stream_rows(self.handle, r0, A_rows.shape[0], A_rows.data_ptr(),
+                                                   _colmajor_ld(A_rows)))
+
+    def shard_stream_end(self) -> None:
+        _lib.check(self._lib.ozk_shard_stream_end(self.handle))
+
     # ---- stage exports (device tensors) --------------------------------------------
     def stage_scale(self, A, B, cfg: EmuConfig, mu_exp, nu_exp) -> None:
         m, k = A.shape

@@ -1,6 +1,7 @@
 """CPU stand-in for the GPU shard engine (TEST INFRASTRUCTURE): implements
 shard_begin / shard_rowmax / shard_end with the oracle, so the multi-process
-exchange logic of paper_2508_03984_b200.distributed runs under gloo on CPU.
+exchange logic of paper_2508_03984_b200.distributed runs under gloo on CPU
+(and shard_stream_begin / _rows / _end, the row-streamed fast-mode path).
 Per rank it computes exactly what ozk_shard_begin/_end compute on the GPU:
 fast mode scales from A and the local columns; accurate mode the partial row
 maxima of Abar*Bbar_local (scaling.cpp:118-148), then the budget from the
@@ -50,3 +51,19 @@ class CpuShardEngine:
                                 for c, e, am in zip(rm, self.ma, self.amax)], np.int32)
         out = self.o.gemm_scaled(self.a, self.b, self.N, self.mu, self.nu)
         C.copy_(torch.from_numpy(np.ascontiguousarray(out.T)).t())
+
+    # ---- row-streamed fast mode: C rows per block of A (mu is row-local) ----
+    def shard_stream_begin(self, m, k, B, cfg, C, alpha=1.0, beta=0.0):
+        assert int(cfg.mode) == 0 and alpha == 1.0 and beta == 0.0
+        self.b = np.asfortranarray(B.numpy())
+        self.C = C
+        self.rows = 0
+
+    def shard_stream_rows(self, r0, A_rows):
+        a = np.asfortranarray(A_rows.numpy())
+        out = self.o.gemm(a, self.b, self.N, 0)
+        self.C[r0:r0 + a.shape[0]].copy_(torch.from_numpy(np.ascontiguousarray(out.T)).t())
+        self.rows += a.shape[0]
+
+    def shard_stream_end(self):
+        assert self.rows == self.C.shape[0]

@@ -121,8 +121,10 @@ def test_residue_planes(ctx, oracle, prec, N):
 
 @pytest.mark.parametrize("N", [2, 9, 14, 20])
 @pytest.mark.parametrize("c_f32", [False, True])
-def test_reconstruct(ctx, oracle, N, c_f32):
-    m, n = 61, 37
+@pytest.mark.parametrize("m,n,pad", [(61, 37, 16), (70, 37, 8), (3000, 5, 16)])
+def test_reconstruct(ctx, oracle, N, c_f32, m, n, pad):
+    """pad 16: the bulk-copy kernel (several 1024-row tiles and a partial one at
+    m = 3000); pad 8 (ldu = 72, not 16-byte aligned): the register-staged fallback"""
     rng = np.random.default_rng(N)
     consts = oracle.constants(N)
     U = np.stack([rng.integers(0, p, size=(m, n)) for p in consts.moduli[:N]]).astype(np.uint8)
@@ -130,7 +132,7 @@ def test_reconstruct(ctx, oracle, N, c_f32):
     nu = rng.integers(-60, 60, size=n).astype(np.int32)
     c1, c2 = oracle.accumulate(U, N)
     want = oracle.unscale(oracle.crt_reduce(c1, c2, N), mu, nu)
-    ldu = (m + 15) // 16 * 16
+    ldu = (m + pad - 1) // pad * pad
     Ud = np.zeros((N, n, ldu), np.uint8)
     Ud[:, :, :m] = U.transpose(0, 2, 1)
     cdt = torch.float32 if c_f32 else torch.float64

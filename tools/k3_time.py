@@ -17,7 +17,7 @@ def main():
     ctx = Context(0)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
-    for N in (8, 14, 20):
+    for N in [int(x) for x in os.environ.get("K3_MODS", "8,14,20").split(",")]:
         ldu = (n + 15) // 16 * 16
         U = torch.randint(0, 173, (N, n, ldu), dtype=torch.uint8, device="cuda")
         mu = torch.zeros(n, dtype=torch.int32, device="cuda")
