@@ -17,8 +17,10 @@ exceed the 126 MB L2, so no explicit flush is needed between steps.
 
 Multi-GPU (torchrun, one rank per GPU): weak scaling by column blocks of B/C
 (SURVEY §8e); every rank owns an n = 16384 column block, rank 0's A is
-broadcast over NCCL inside each step (the north star's A broadcast), and
-"value" is the aggregate 2 m n_total k / max-over-ranks time.
+broadcast over NCCL inside each step (the north star's A broadcast) — in fast
+mode as row blocks that each rank starts computing on as they land
+(ozk_shard_stream_*, --row-block) — and "value" is the aggregate
+2 m n_total k / max-over-ranks time.
 """
 from __future__ import annotations
 
@@ -43,13 +45,18 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--n", type=int, default=DEFAULT_N)
+    p.add_argument("--size", "--n", dest="n", type=int, default=DEFAULT_N)
     p.add_argument("--moduli", type=int, default=MODULI)
     p.add_argument("--mode", choices=["fast", "accurate"], default="fast")
     p.add_argument("--phi", type=float, default=0.5)
     p.add_argument("--no-extra", action="store_true", help="skip the sweep / native / accuracy extras")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=256, help="rows/cols of the CPU baseline sample (full k)")
+    p.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                   help="torch.distributed backend for N > 1 (gloo + OZK_BENCH_ONE_DEVICE=1: a functional "
+                        "multi-rank run on one GPU; its timing means nothing)")
+    p.add_argument("--row-block", type=int, default=2048,
+                   help="fast mode, N > 1: A streams to the ranks in row blocks of this many rows (0: whole A)")
     return p.parse_args()
 
 
@@ -251,11 +258,14 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if os.environ.get("OZK_BENCH_ONE_DEVICE") else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     n = args.n
     m = k = n
@@ -272,7 +282,7 @@ def main():
     def step():
         if world > 1:
             # column shard: A broadcast from rank 0 + (accurate) row-bound all-reduce
-            gemm_sharded(ctx, A, B, cfg, C)
+            gemm_sharded(ctx, A, B, cfg, C, row_block=args.row_block or None)
         else:
             ctx.gemm(A, B, cfg, C)
 
@@ -309,8 +319,9 @@ def main():
 
     # ---- roofline of the dominant kernel (K2, tensor-bound) ------------------------
     peaks = load_peaks()
-    k2_ms = prof["products"][0] / max(prof["products"][1], 1)
-    k2_ops = args.moduli * 2.0 * m * n * k  # algorithmic int8 ops per launch
+    # per step: the streamed multi-GPU path launches K2 once per row block of A
+    k2_ms = prof["products"][0] / args.steps
+    k2_ops = args.moduli * 2.0 * m * n * k  # algorithmic int8 ops per step
     achieved = k2_ops / (k2_ms * 1e-3) / 1e12
     bf16 = peaks.get("bf16_tflops")
     peak = 2.0 * bf16 if bf16 else 2.0 * 1590.0
@@ -319,7 +330,8 @@ def main():
                 "traffic": traffic, "kernel": "residue_gemm_kernel (K2, tcgen05.mma kind::i8)",
                 "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (dense INT8 = 2 x dense BF16 on sm_100)"
                                 if bf16 else "2 x fallback 1.59 PFLOP/s bf16 (B200_PROFILING.md)"),
-                "stage_ms": {kname: v[0] / max(v[1], 1) for kname, v in prof.items()}}
+                "stage_ms": {kname: v[0] / args.steps for kname, v in prof.items()},
+                "k2_launches_per_step": prof["products"][1] / args.steps}
     if peaks.get("bf16_tflops_sustained"):
         # K2 runs inside a long step: the sustained-clock denominator, for reference
         roofline["peak_sustained"] = 2.0 * peaks["bf16_tflops_sustained"]
@@ -331,7 +343,9 @@ def main():
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (rand-0.5)*exp(phi*randn), phi={args.phi}, generated on device",
         "config": {"workload": f"DGEMM m=n=k={n} per GPU (column block of B/C), {args.moduli} moduli, {args.mode}",
-                   "l2": "inputs (2 x 2.1 GB) larger than L2; no flush", "parallelism": f"colshard{world}"},
+                   "l2": "inputs (2 x 2.1 GB) larger than L2; no flush", "parallelism": f"colshard{world}",
+                   "a_broadcast": (f"row blocks of {args.row_block}" if world > 1 and args.row_block
+                                   and args.mode == "fast" else ("whole" if world > 1 else "none"))},
         "gpu_launches": int(launches), "roofline": roofline, "clocks": clk.summary(),
     }
 
@@ -428,7 +442,7 @@ def main():
         extra["accuracy"] = accuracy_probe(ctx, A, B, cfg)
         out["extra"] = extra
 
-    if rank == 0 and not os.environ.get("OZK_BENCH_NO_CPU"):
+    if world == 1 and not os.environ.get("OZK_BENCH_NO_CPU"):  # the CPU leg: rank 0 at N = 1 only
         cb = cpu_reference_sample(args.cpu_sample, k, args.moduli, 0 if args.mode == "fast" else 1, args.phi)
         out["cpu_baseline"] = {
             "value": cb["tflops"], "unit": "TFLOPS", "cores": cb["threads"], "kind": "reference",
