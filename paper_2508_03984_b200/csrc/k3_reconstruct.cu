@@ -121,10 +121,15 @@ template <>
 struct BulkWord<8> {
     using T = uint2;
     static __device__ __forceinline__ uint32_t part(const uint2& w, int q) { return q < 4 ? w.x : w.y; }
+    static __device__ __forceinline__ uint2 lds(uint32_t addr) {
+        uint2 v;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+        return v;
+    }
 };
 
 template <bool kF32Out, bool kPlain, int kC1, int kMaxMod, int R, int kConsumers, int kStages>
-__global__ void __launch_bounds__(kConsumers + 32, 512 / kConsumers)
+__global__ void __launch_bounds__(kConsumers + 32, (kMaxMod <= 8 ? 384 : 512) / kConsumers)
     reconstruct_bulk_kernel(const uint8_t* __restrict__ u, int64_t ldu, int64_t plane_stride, int64_t m, int64_t n,
                             int64_t row_chunks, const int32_t* __restrict__ mu_exp, const int32_t* __restrict__ nu_exp,
                             const DevConsts c, double alpha, double beta, void* __restrict__ C, int64_t ldc,
@@ -174,6 +179,7 @@ __global__ void __launch_bounds__(kConsumers + 32, 512 / kConsumers)
 
     using W = BulkWord<R>;
     const int lane = threadIdx.x & 31;
+    const uint32_t sbase = smem_addr(sbuf);
     for (int64_t k = 0, tile = blockIdx.x; tile < tiles; ++k, tile += gridDim.x, advance()) {
         const int s = static_cast<int>(k % kStages);
         const int64_t i0 = chunk * kTile + threadIdx.x * R;
@@ -190,19 +196,20 @@ __global__ void __launch_bounds__(kConsumers + 32, 512 / kConsumers)
         const int ne = nu_exp[j];
         bulk_mbar_wait(smem_addr(&full[s]), static_cast<uint32_t>((k / kStages) & 1));
         if (i0 < m) {
-            const uint8_t* sp = sbuf + s * kMaxMod * kTile + threadIdx.x * R;
+            const uint32_t sp = sbase + static_cast<uint32_t>(s * kMaxMod * kTile) + threadIdx.x * R;
             double c2[R];
             double c1[R];
 #pragma unroll
             for (int q = 0; q < R; ++q) {
                 c1[q] = c2[q] = 0.0;
             }
-            // past n_mod the tables are zero (to_dev zero-fills them): those terms
-            // add +0 to non-negative sums, exact, and keep the chain branch-free
+            // Past n_mod the tables are zero (to_dev zero-fills them) and the
+            // slots hold stale bytes: those terms add +0 to non-negative sums,
+            // exactly, so every plane slot is read unconditionally and the
+            // chain stays branch- and predicate-free (compile-time offsets).
 #pragma unroll
             for (int t = 0; t < kMaxMod; ++t) {
-                typename W::T w{};
-                if (t < n_mod) w = *reinterpret_cast<const typename W::T*>(sp + t * kTile);
+                const typename W::T w = W::lds(sp + t * kTile);
 #pragma unroll
                 for (int q = 0; q < R; ++q) {
                     const uint32_t ub = __byte_perm(W::part(w, q), 0u, 0x4440u | (q & 3));
