@@ -40,6 +40,15 @@ __device__ __forceinline__ void ld_nc_v8(const int32_t* p, int* v) {
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                  : "l"(p));
 }
+__device__ __forceinline__ void ld_nc_v4(const int32_t* p, int* v) {
+    asm volatile("ld.global.nc.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "l"(p));
+}
+__device__ __forceinline__ void st_v4_f32(float* p, const float* v) {
+    asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3])
+                 : "memory");
+}
 __device__ __forceinline__ void st_v4_f64(double* p, const double* v) {
     asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
                  : "memory");
@@ -60,8 +69,9 @@ __device__ __forceinline__ void st_v8_f32(float* p, const float* v) {
 // of how ptxas schedules the FP64 chain (register-staged loads got interleaved
 // with it), and tiles t+1.. stream in while tile t computes. No block-wide
 // barrier: each consumer warp releases a slot on its own.
-// ring depth: two slots (1024 rows x N planes each); deeper rings and 8-warp
-// blocks measured the same (K3 is issue-bound)
+// ring depth: two slots (1024 rows x N planes each); deeper rings, 8-warp
+// blocks and 4 rows per thread (more warps) measured the same or slower
+//
 template <int kMaxMod>
 __host__ __device__ constexpr int bulk_stages() {
     return 2;
@@ -118,6 +128,16 @@ __device__ __forceinline__ double unscale_fast(double x, int e) {
 template <int R>
 struct BulkWord;
 template <>
+struct BulkWord<4> {
+    using T = uint32_t;
+    static __device__ __forceinline__ uint32_t part(const uint32_t& w, int) { return w; }
+    static __device__ __forceinline__ uint32_t lds(uint32_t addr) {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+        return v;
+    }
+};
+template <>
 struct BulkWord<8> {
     using T = uint2;
     static __device__ __forceinline__ uint32_t part(const uint2& w, int q) { return q < 4 ? w.x : w.y; }
@@ -129,7 +149,7 @@ struct BulkWord<8> {
 };
 
 template <bool kF32Out, bool kPlain, int kC1, int kMaxMod, int R, int kConsumers, int kStages>
-__global__ void __launch_bounds__(kConsumers + 32, (kMaxMod <= 8 ? 384 : 512) / kConsumers)
+__global__ void __launch_bounds__(kConsumers + 32, (kMaxMod <= 8 ? 384 : 512) / kConsumers * (8 / R))
     reconstruct_bulk_kernel(const uint8_t* __restrict__ u, int64_t ldu, int64_t plane_stride, int64_t m, int64_t n,
                             int64_t row_chunks, const int32_t* __restrict__ mu_exp, const int32_t* __restrict__ nu_exp,
                             const DevConsts c, double alpha, double beta, void* __restrict__ C, int64_t ldc,
@@ -188,7 +208,10 @@ __global__ void __launch_bounds__(kConsumers + 32, (kMaxMod <= 8 ? 384 : 512) / 
         int me[R];
         if (vec) {
 #pragma unroll
-            for (int v = 0; v < R; v += 8) ld_nc_v8(mu_exp + i0 + v, me + v);
+            if constexpr (R >= 8)
+                for (int v = 0; v < R; v += 8) ld_nc_v8(mu_exp + i0 + v, me + v);
+            else
+                ld_nc_v4(mu_exp + i0, me);
         } else {
 #pragma unroll
             for (int q = 0; q < R; ++q) me[q] = i0 + q < m ? mu_exp[i0 + q] : 0;
@@ -241,7 +264,12 @@ __global__ void __launch_bounds__(kConsumers + 32, (kMaxMod <= 8 ? 384 : 512) / 
                 }
             }
             if (vec) {
-                if constexpr (kF32Out) {
+                if constexpr (kF32Out && R < 8) {
+                    float f[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) f[q] = __double2float_rn(r[q]);
+                    st_v4_f32(static_cast<float*>(C) + i0 + j * ldc, f);
+                } else if constexpr (kF32Out) {
 #pragma unroll
                     for (int v = 0; v < R; v += 8) {
                         float f[8];
