@@ -59,6 +59,15 @@ extern "C" {
  * API (ozk_stage_residues / ozk_stage_products) takes untransposed operands. */
 #define OZK_FLAG_TRANS_A 2
 #define OZK_FLAG_TRANS_B 4
+/* Stream-ordered call (extension): device-pointer entry points (ozk_gemm,
+ * ozk_dgemm_ex, strided batches, the shard APIs) return after enqueuing, with
+ * no host synchronisation, so back-to-back calls pipeline and a call can be
+ * captured into a CUDA graph (after one warm-up call has sized the workspace).
+ * The non-finite-input check (emulator.cpp:19-22) is then deferred: its flag
+ * accumulates on the device until ozk_sync, which returns OZK_INPUT_ERROR if
+ * any call since the last ozk_sync saw NaN/Inf. Without the flag every call
+ * synchronises and reports it, like the reference. */
+#define OZK_FLAG_ASYNC 8
 
 /* storage types of A/B/C buffers */
 #define OZK_R64F 0
@@ -144,6 +153,10 @@ int ozk_dgemm_ex(ozk_handle h, int n_moduli, int mode, char transa, char transb,
 int ozk_gemm_strided_batched(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, double alpha,
                              const void* A, int64_t lda, int64_t stride_a, const void* B, int64_t ldb,
                              int64_t stride_b, double beta, void* C, int64_t ldc, int64_t stride_c, int64_t batch);
+
+/* Synchronise the handle's stream and collect the deferred non-finite check of
+ * the OZK_FLAG_ASYNC calls since the last ozk_sync (then cleared). */
+int ozk_sync(ozk_handle h);
 
 /* ---- column-sharded GEMM (multi-GPU) --------------------------
  * This process computes C[:, shard] = alpha * A * B[:, shard] + beta * C[:, shard]

@@ -21,6 +21,7 @@ OZK_PRODUCTS_I32, OZK_PRODUCTS_U8 = 0, 1
 OZK_FLAG_FAST_EXPONENT_FIX = 1
 OZK_FLAG_TRANS_A = 2
 OZK_FLAG_TRANS_B = 4
+OZK_FLAG_ASYNC = 8
 MAX_MODULI = 20
 ENGINE_MAX_K = 1 << 17
 
@@ -30,7 +31,7 @@ EXPORTED_SYMBOLS = (
     "ozk_select_moduli", "ozk_mod_inverse", "ozk_build_constants", "ozk_dump_tables_csv",
     "ozk_gemm", "ozk_gemm_host", "ozk_dgemm", "ozk_sgemm", "ozk_dgemm_ex", "ozk_gemm_strided_batched",
     "ozk_stage_scale", "ozk_plane_ld", "ozk_stage_residues", "ozk_stage_products", "ozk_stage_reconstruct",
-    "ozk_kernel_launches", "ozk_profile", "ozk_profile_read",
+    "ozk_kernel_launches", "ozk_profile", "ozk_profile_read", "ozk_sync",
     "ozk_shard_begin", "ozk_shard_rowmax", "ozk_shard_end",
     "ozk_shard_stream_begin", "ozk_shard_stream_rows", "ozk_shard_stream_end",
     "ozk_int8_gemm", "ozk_truncate_scale", "ozk_residues", "ozk_mod_u8_array", "ozk_accumulate", "ozk_crt_reduce",
@@ -130,6 +131,7 @@ def load() -> C.CDLL:
     L.ozk_kernel_launches.restype = i64
     L.ozk_kernel_launches.argtypes = [p]
     L.ozk_profile.argtypes = [p, i32]
+    L.ozk_sync.argtypes = [p]
     L.ozk_shard_begin.argtypes = [p, C.POINTER(OzkConfig), i64, i64, i64, p, i64, p, i64]
     L.ozk_shard_rowmax.restype = p
     L.ozk_shard_rowmax.argtypes = [p]

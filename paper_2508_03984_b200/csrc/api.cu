@@ -93,6 +93,7 @@ struct Job {
     // accumulates in int64 (per column block) and its maxima are uint64
     bool wide_bound;
     unsigned long long *rowmax64, *colmax64;
+    bool async = false;  // OZK_FLAG_ASYNC: no host sync, deferred non-finite check
     int32_t* flags;  // [0] non-finite, [1] flagged rows, [2] flagged columns, [4..] K2 lockstep words (1 KB)
     double *amax, *asum, *bmax, *bsum;
     int splits, splits_b;  // k-partials of the row-stat reductions of op(A) (!ta) / op(B) (tb)
@@ -292,7 +293,13 @@ int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c,
     J.lda = lda;
     J.ldb = ldb;
     J.in_f32 = cfg->a_type == OZK_R32F;
-    OZK_CUDA(cudaMemsetAsync(J.flags, 0, 16, h->stream));
+    // flag word 0 (non-finite input) stays sticky across stream-ordered calls
+    // until ozk_sync collects it
+    J.async = (cfg->flags & OZK_FLAG_ASYNC) != 0;
+    if (J.async)
+        OZK_CUDA(cudaMemsetAsync(J.flags + 1, 0, 12, h->stream));
+    else
+        OZK_CUDA(cudaMemsetAsync(J.flags, 0, 16, h->stream));
     return OZK_OK;
 }
 
@@ -523,6 +530,7 @@ int compute_block(ozk_context* h, Job& J, int64_t j0, int64_t nj, double alpha, 
 }
 
 int finish_check(ozk_context* h, Job& J, cudaStream_t s) {
+    if (J.async) return OZK_OK;  // deferred to ozk_sync
     OZK_CUDA(cudaMemcpyAsync(h->flags_host, J.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     OZK_CUDA(cudaStreamSynchronize(s));
     if (h->flags_host[0]) {
@@ -744,6 +752,9 @@ int gemm_host_streamed(ozk_context* h, Job& J, double alpha, const void* A, int6
 int gemm_host(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int64_t m, int64_t n, int64_t k,
               double alpha, const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C,
               int64_t ldc) {
+    ozk_config hc = *cfg;  // host buffers: the call always completes (no OZK_FLAG_ASYNC)
+    hc.flags &= ~OZK_FLAG_ASYNC;
+    cfg = &hc;
     OZK_TRY(validate(cfg, c, m, n, k, lda, ldb));
     if (ldc < m) {
         set_error("gemm_emulated: ldc < m");
@@ -900,6 +911,14 @@ int ozk_create(ozk_handle* handle, int device) {
         delete h;
         return cuda_fail("cudaMallocHost", e);
     }
+    // the device flag words (non-finite, flagged lines, K2 lockstep counters):
+    // allocated and cleared once, so the sticky OZK_FLAG_ASYNC word starts at 0
+    if (ensure(h->flags, 2048) != OZK_OK || cudaMemset(h->flags.p, 0, 2048) != cudaSuccess) {
+        const std::string err = ozk_last_error();
+        ozk_destroy(h);
+        set_error("flag buffer: " + err);
+        return OZK_CUDA_ERROR;
+    }
     *handle = h;
     return OZK_OK;
 }
@@ -961,6 +980,20 @@ int ozk_profile_read(ozk_handle h, double* ms, int64_t* calls, int reset) {
 }
 
 int64_t ozk_plane_ld(int64_t k) { return plane_ld(k); }
+
+int ozk_sync(ozk_handle h) {
+    if (!h) return OZK_INPUT_ERROR;
+    OZK_CUDA(cudaSetDevice(h->device));
+    OZK_CUDA(cudaStreamSynchronize(h->stream));
+    if (!h->flags.p) return OZK_OK;
+    OZK_CUDA(cudaMemcpy(h->flags_host, h->flags.p, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (h->flags_host[0]) {
+        OZK_CUDA(cudaMemset(h->flags.p, 0, sizeof(int32_t)));
+        set_error("gemm_emulated: non-finite entry in A or B");
+        return OZK_INPUT_ERROR;
+    }
+    return OZK_OK;
+}
 
 int ozk_gemm(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, int64_t k, double alpha, const void* A,
              int64_t lda, const void* B, int64_t ldb, double beta, void* C, int64_t ldc) {

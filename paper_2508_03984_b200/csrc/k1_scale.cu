@@ -243,7 +243,7 @@ __global__ void accurate_budget_kernel(const int32_t* __restrict__ base, const C
 int row_stats_splits(int64_t m, int64_t k) {
     const int64_t row_blocks = (m + kRowTile - 1) / kRowTile;
     int64_t splits = (4 * 148 + row_blocks - 1) / row_blocks;  // ~4 waves of blocks
-    const int64_t max_splits = (k + 255) / 256;                 // keep >= 256 columns per split
+    const int64_t max_splits = (k + 63) / 64;                   // keep >= 64 columns per split
     if (splits > max_splits) splits = max_splits;
     if (splits < 1) splits = 1;
     if (splits > 64) splits = 64;

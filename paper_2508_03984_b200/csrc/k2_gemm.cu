@@ -11,7 +11,8 @@
 //               reference's uint32 accumulator (int8_engine.cpp:12-38);
 //   warp 2      TMEM allocator (two 256-column accumulators: the epilogue of
 //               tile t overlaps the MMAs of tile t+1);
-//   warps 4-7   epilogue: tcgen05.ld 32 columns at a time, then
+//   warps 4-11  epilogue (two per TMEM lane quarter, half the columns each):
+//               tcgen05.ld 32 columns at a time, then
 //               U8  : U_i = mod_u8(C'_i)  -> 1 byte per element to HBM,
 //               I32 : raw C'_i (debug / parity export),
 //               MAX : row/column maxima of Cbar via atomics (the reference
@@ -35,8 +36,9 @@ namespace {
 constexpr int kBK = 128;  // bytes (= int8 elements) of K per stage: one 128B swizzle atom
 constexpr int64_t kChunkK = OZK_ENGINE_MAX_K;  // longest exact int32 accumulation
 constexpr int kAccCols = 256;
-constexpr int kThreads = 256;
 constexpr int kEpiWarp0 = 4;
+constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, each draining half the columns
+constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
 
 template <int CG>
 struct Cfg {
@@ -315,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
-            mbar_init(tempty + a, 4 * CG);  // one arrival per epilogue warp of every CTA
+            mbar_init(tempty + a, kEpiWarps * CG);  // one arrival per epilogue warp of every CTA
         }
         fence_barrier_init();
     }
@@ -450,7 +452,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= kEpiWarp0) {
         // ---------------- epilogue ----------------
-        const int q = warp - kEpiWarp0;  // TMEM lane quarter
+        const int q = (warp - kEpiWarp0) % 4;     // TMEM lane quarter (warp % 4: the lanes it may read)
+        const int half = (warp - kEpiWarp0) / 4;  // which half of the tile's columns it drains
         const uint32_t tempty0_leader = CG == 2 ? mapa(smem_u32(tempty), 0) : smem_u32(tempty);
         int lt = 0;
         for (int t = cluster_id; t < total; t += nclusters, ++lt) {
@@ -463,7 +466,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int row = tm * C::kTileM + static_cast<int>(rank) * C::kBM + q * 32 + lane;
             const bool row_ok = row < P.m;
             int32_t rmax = 0;
-            for (int cb = 0; cb < C::kTileN / 32; ++cb) {
+            constexpr int kChunks = C::kTileN / 32 / (kEpiWarps / 4);
+            for (int cb = half * kChunks; cb < (half + 1) * kChunks; ++cb) {
                 uint32_t v[32];
                 tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kAccCols + cb * 32, v);
                 const int col0 = tn * C::kTileN + cb * 32;

@@ -49,6 +49,10 @@ class EmuConfig:
     # extension (not in the reference): subtract the max exponent in fast-mode
     # scaling, the term scaling.cpp:50-56 omits. Off = reference bits.
     fast_exponent_fix: bool = False
+    # extension: stream-ordered device calls (OZK_FLAG_ASYNC) — no host sync per
+    # call, CUDA-graph capturable; the non-finite check is collected by
+    # Context.synchronize(). Host-buffer calls ignore it.
+    stream_ordered: bool = False
 
 
 @dataclasses.dataclass
@@ -101,6 +105,7 @@ def _config(cfg: EmuConfig, a_type: int, c_type: int, constants=None, trans_a: b
     c.block_k = int(cfg.block_k)
     c.flags = _lib.OZK_FLAG_FAST_EXPONENT_FIX if getattr(cfg, "fast_exponent_fix", False) else 0
     c.flags |= (_lib.OZK_FLAG_TRANS_A if trans_a else 0) | (_lib.OZK_FLAG_TRANS_B if trans_b else 0)
+    c.flags |= _lib.OZK_FLAG_ASYNC if getattr(cfg, "stream_ordered", False) else 0
     c.constants = C.pointer(constants) if constants is not None else None
     return c
 
@@ -164,6 +169,11 @@ class Context:
         _lib.check(self._lib.ozk_gemm_host(self.handle, C.byref(conf), m, n, k, float(alpha), a.ctypes.data,
                                            a.shape[0], b.ctypes.data, b.shape[0], float(beta), out.ctypes.data, m))
         return out
+
+    def synchronize(self) -> None:
+        """wait for the handle's stream; raises InputError if a stream-ordered call
+        since the last synchronize saw a non-finite input (ozk_sync)"""
+        _lib.check(self._lib.ozk_sync(self.handle))
 
     # ---- device GEMM (torch CUDA tensors, column-major) ------------------------------
     def gemm(self, A, B, cfg: EmuConfig, C_out, alpha: float = 1.0, beta: float = 0.0, constants=None,
