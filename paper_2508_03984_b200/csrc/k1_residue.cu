@@ -10,7 +10,7 @@
 // bytes (read K-major). So both operands stream through the same kernel: each
 // thread reads 8 consecutive elements of one column (64 B of FP64, a warp
 // covers 2 KB contiguous) and writes 8 bytes per plane (256 B per warp) — no
-// transpose, no shared-memory staging beyond the per-modulus constants.
+// transpose, no shared-memory staging.
 // Residues use the exact conversion-free symmetric-residue form where it
 // provably equals rmod_fast (ozk_device.cuh), else the literal sequence.
 // Each input element is read once and each plane byte written once: the pass
@@ -42,16 +42,13 @@ __device__ __forceinline__ uint32_t literal_byte(T x, const DevConsts& c, int t)
 // column, plane_stride bytes apart). ROW_EXP: the scale exponent is per row
 // (A: mu), else per column (B: nu). Each thread handles 8 consecutive rows of
 // one column: 64 (FP64) contiguous bytes in, 8 bytes out per plane.
-template <typename T, int KIND, bool ROW_EXP>
+// kMaxMod: the modulus count rounded up to a bucket (8/12/14/16/20): the
+// modulus loop is unrolled, so p_t and 1/p_t are constant-bank operands of the
+// DFMA / IMAD and the plane address advances by one add per modulus.
+template <typename T, int KIND, bool ROW_EXP, int kMaxMod>
 __global__ void __launch_bounds__(128)
     planes_kernel(const T* __restrict__ b, int64_t k, int64_t n, int64_t ldb, const int32_t* __restrict__ exps,
                   const DevConsts c, int8_t* __restrict__ planes, int64_t ld, int64_t plane_stride, int64_t extent) {
-    __shared__ double s_pinv[OZK_MAX_MODULI];
-    __shared__ uint32_t s_p[OZK_MAX_MODULI];
-    if (threadIdx.x < OZK_MAX_MODULI) {
-        s_pinv[threadIdx.x] = c.pinv64[threadIdx.x];
-        s_p[threadIdx.x] = static_cast<uint32_t>(c.p[threadIdx.x]);
-    }
     const int64_t j = blockIdx.x;
     const int64_t i0 = (static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x) * kBPerThread;
     const bool active = i0 < extent;  // rows up to plane_ld(rows): the zero padding K2's 16-byte rows need
@@ -75,7 +72,6 @@ __global__ void __launch_bounds__(128)
         }
     }
     fast = __all_sync(0xffffffffu, fast);
-    __syncthreads();  // s_p / s_pinv
     // extent is a multiple of 16, so a thread's 8 bytes are either all in [0, extent) or all past it
     if (!active) return;
     int8_t* dst0 = planes + j * ld + i0;
@@ -93,23 +89,26 @@ __global__ void __launch_bounds__(128)
         xlo[u] = static_cast<uint32_t>(__double2loint(__dadd_rn(static_cast<double>(x[u]), kMagic52)));
     // the fast/literal choice is warp-uniform: branch once, outside the modulus loop
     if (fast) {
-#pragma unroll 1
-        for (int t = 0; t < c.n; ++t) {
-            const uint32_t pt = s_p[t];
-            const double pinvt = s_pinv[t];
-            uint2 word;
-            if (pt == 256) {  // p = 256: the residue is the low byte of x
-                word = make_uint2(pack_low_bytes(xlo[0], xlo[1], xlo[2], xlo[3]),
-                                  pack_low_bytes(xlo[4], xlo[5], xlo[6], xlo[7]));
-            } else {
-                const uint32_t neg_p = 0u - pt;
-                uint32_t v[kBPerThread];
+        int8_t* dst = dst0;
 #pragma unroll
-                for (int u = 0; u < kBPerThread; ++u)
-                    v[u] = symmetric_residue(static_cast<double>(x[u]), xlo[u], neg_p, pinvt);
-                word = make_uint2(pack_low_bytes(v[0], v[1], v[2], v[3]), pack_low_bytes(v[4], v[5], v[6], v[7]));
+        for (int t = 0; t < kMaxMod; ++t) {
+            if (t < c.n) {  // uniform
+                const uint32_t pt = static_cast<uint32_t>(c.p[t]);
+                uint2 word;
+                if (pt == 256) {  // p = 256: the residue is the low byte of x
+                    word = make_uint2(pack_low_bytes(xlo[0], xlo[1], xlo[2], xlo[3]),
+                                      pack_low_bytes(xlo[4], xlo[5], xlo[6], xlo[7]));
+                } else {
+                    const uint32_t neg_p = 0u - pt;
+                    uint32_t v[kBPerThread];
+#pragma unroll
+                    for (int u = 0; u < kBPerThread; ++u)
+                        v[u] = symmetric_residue(static_cast<double>(x[u]), xlo[u], neg_p, c.pinv64[t]);
+                    word = make_uint2(pack_low_bytes(v[0], v[1], v[2], v[3]), pack_low_bytes(v[4], v[5], v[6], v[7]));
+                }
+                *reinterpret_cast<uint2*>(dst) = word;
+                dst += plane_stride;
             }
-            *reinterpret_cast<uint2*>(dst0 + t * plane_stride) = word;
         }
     } else {
 #pragma unroll 1
@@ -141,12 +140,28 @@ void planes_dispatch(const void* x, int is_f32, int64_t rows, int64_t cols, int6
     const int64_t extent = plane_ld(rows);
     dim3 grid(static_cast<unsigned>(cols),
               static_cast<unsigned>((extent + 128 * kBPerThread - 1) / (128 * kBPerThread)));
-    if (is_f32)
-        planes_kernel<float, KIND, ROW_EXP><<<grid, 128, 0, s>>>(static_cast<const float*>(x), rows, cols, ldx, exps,
-                                                                 c, planes, ld, stride, extent);
+#define OZK_K1B(MAXN)                                                                                            \
+    do {                                                                                                         \
+        if (is_f32)                                                                                              \
+            planes_kernel<float, KIND, ROW_EXP, MAXN><<<grid, 128, 0, s>>>(static_cast<const float*>(x), rows,   \
+                                                                           cols, ldx, exps, c, planes, ld,       \
+                                                                           stride, extent);                      \
+        else                                                                                                     \
+            planes_kernel<double, KIND, ROW_EXP, MAXN><<<grid, 128, 0, s>>>(static_cast<const double*>(x), rows, \
+                                                                            cols, ldx, exps, c, planes, ld,      \
+                                                                            stride, extent);                     \
+    } while (0)
+    if (KIND == 1 || c.n <= 8)  // the bound planes have no modulus loop
+        OZK_K1B(8);
+    else if (c.n <= 12)
+        OZK_K1B(12);
+    else if (c.n <= 14)
+        OZK_K1B(14);
+    else if (c.n <= 16)
+        OZK_K1B(16);
     else
-        planes_kernel<double, KIND, ROW_EXP><<<grid, 128, 0, s>>>(static_cast<const double*>(x), rows, cols, ldx,
-                                                                  exps, c, planes, ld, stride, extent);
+        OZK_K1B(OZK_MAX_MODULI);
+#undef OZK_K1B
 }
 
 }  // namespace
