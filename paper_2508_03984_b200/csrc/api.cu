@@ -597,6 +597,30 @@ int64_t host_block_cols(int64_t n) {
 // is one thin region plus its D2H. Results are identical to the unblocked
 // call: every stage is row/column-local in fast mode.
 
+int64_t stream_block(int64_t dim);
+bool tail_split() {
+    static const bool on = std::getenv("OZK_HOST_TAIL") == nullptr || std::atoi(std::getenv("OZK_HOST_TAIL")) != 0;
+    return on;
+}
+
+// block boundaries along one operand dimension: ~16 blocks of whole 256-wide
+// GEMM tiles, the last one split into halving pieces (b/2, b/4, ...) so the
+// region computed after the final transfer, and its D2H, are short
+std::vector<std::pair<int64_t, int64_t>> stream_blocks(int64_t dim) {
+    const int64_t b = stream_block(dim);
+    std::vector<std::pair<int64_t, int64_t>> out;
+    int64_t r0 = 0;
+    while (r0 < dim) {
+        int64_t sz = std::min(b, dim - r0);
+        const int64_t rest = dim - r0;
+        if (rest <= b && rest > 256 && tail_split()) sz = std::max<int64_t>(256, (rest / 2 + 255) / 256 * 256);
+        if (sz > rest) sz = rest;
+        out.push_back({r0, sz});
+        r0 += sz;
+    }
+    return out;
+}
+
 int64_t stream_block(int64_t dim) {
     int64_t b = (dim + 15) / 16;  // ~16 blocks per operand
     b = (b + 255) / 256 * 256;    // whole 256-row/column GEMM tiles
@@ -679,8 +703,8 @@ int gemm_host_streamed(ozk_context* h, Job& J, double alpha, const void* A, int6
                        void* C, int64_t ldc, int c_f32) {
     const size_t es = J.in_f32 ? 4 : 8;
     const int64_t m = J.m, n = J.n, k = J.k;
-    const int64_t bm = stream_block(m), bn = stream_block(n);
-    const int na = static_cast<int>((m + bm - 1) / bm), nb = static_cast<int>((n + bn - 1) / bn);
+    const auto blocks_a = stream_blocks(m), blocks_b = stream_blocks(n);
+    const int na = static_cast<int>(blocks_a.size()), nb = static_cast<int>(blocks_b.size());
     std::vector<cudaEvent_t> ev(na + nb + na + nb + 1);
     for (auto& e : ev) OZK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     struct EventGuard {
@@ -700,14 +724,14 @@ int gemm_host_streamed(ozk_context* h, Job& J, double alpha, const void* A, int6
     // the copy stream: A_0, B_0, A_1, B_1, ...
     for (int s = 0; s < na || s < nb; ++s) {
         if (s < na) {
-            const int64_t r0 = s * bm, mr = std::min(bm, m - r0);
+            const int64_t r0 = blocks_a[s].first, mr = blocks_a[s].second;
             OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(h->host_a.p) + es * r0, es * lda,
                                        static_cast<const char*>(A) + es * r0, es * lda, es * mr, k,
                                        cudaMemcpyHostToDevice, h->h2d));
             OZK_CUDA(cudaEventRecord(ev_a(s), h->h2d));
         }
         if (s < nb) {
-            const int64_t c0 = s * bn, nc = std::min(bn, n - c0);
+            const int64_t c0 = blocks_b[s].first, nc = blocks_b[s].second;
             OZK_CUDA(cudaMemcpyAsync(static_cast<char*>(h->host_b.p) + es * ldb * c0,
                                      static_cast<const char*>(B) + es * ldb * c0, es * ldb * nc,
                                      cudaMemcpyHostToDevice, h->h2d));
@@ -718,7 +742,7 @@ int gemm_host_streamed(ozk_context* h, Job& J, double alpha, const void* A, int6
     int64_t rows_in = 0, cols_in = 0;  // prefix of A rows / B columns already on the device
     for (int s = 0; s < na || s < nb; ++s) {
         if (s < na) {
-            const int64_t r0 = s * bm, mr = std::min(bm, m - r0);
+            const int64_t r0 = blocks_a[s].first, mr = blocks_a[s].second;
             OZK_CUDA(cudaStreamWaitEvent(h->stream, ev_a(s), 0));
             {
                 StageTimer t(h, OZK_PROFILE_SCALE);
@@ -728,7 +752,7 @@ int gemm_host_streamed(ozk_context* h, Job& J, double alpha, const void* A, int6
             if (cols_in > 0) OZK_TRY(stream_region(h, J, r0, mr, 0, cols_in, alpha, c_f32, C, ldc, ev_ra(s)));
         }
         if (s < nb) {
-            const int64_t c0 = s * bn, nc = std::min(bn, n - c0);
+            const int64_t c0 = blocks_b[s].first, nc = blocks_b[s].second;
             OZK_CUDA(cudaStreamWaitEvent(h->stream, ev_b(s), 0));
             {
                 StageTimer t(h, OZK_PROFILE_SCALE);

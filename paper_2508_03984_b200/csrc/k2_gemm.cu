@@ -66,8 +66,8 @@ struct K2Params {
     int p[OZK_MAX_MODULI];
     int pinv[OZK_MAX_MODULI];
     int group;             // tile rows per raster group
-    int hints;             // bit 0: A loads evict_last, bit 1: B loads evict_last, bit 2: streaming U
-                           // stores, bit 3: B loads evict_first
+    int hints;             // bit 0: A loads evict_last, bit 1: B loads evict_last, bit 3: B loads
+                           // evict_first (bit 2, streaming U stores, measured no gain: removed)
     int sync_mode;         // 0 off; 1 tile lockstep (slack 1); 2 k-block lockstep
     int sync_window;       // mode 2: max k-blocks ahead of the slowest cluster
     int sync_every;        // mode 2: check every this many k-blocks
@@ -109,6 +109,13 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+// relaxed: orders nothing but the arrival itself. The epilogue's TMEM reads are
+// ordered by tcgen05.wait::ld + tcgen05.fence::before_thread_sync; its global
+// stores need no ordering against the MMA warp, and a release at cluster scope
+// compiles to a GPU-wide MEMBAR that waits for them (µs per tile at small k)
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_bar) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
                                             int c2) {
@@ -157,9 +164,6 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
     return p;
-}
-__device__ __forceinline__ void st_stream_u8(uint8_t* p, uint32_t v) {
-    asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void st_release(unsigned int* p, unsigned int v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -475,10 +479,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint8_t* dst = static_cast<uint8_t*>(P.out) + static_cast<long long>(mod) * P.plane_out + row;
                     const int pm = P.p[mod], pinv = P.pinv[mod];
                     if (row_ok) {
+                        uint8_t* q = dst + static_cast<long long>(col0) * P.ldo;
+                        const long long ldo = P.ldo;
+                        if constexpr (KIND == K2_U8) {
+                            if (col0 + 32 <= P.n) {  // interior chunk: no per-column checks
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) {
+                                    *q = static_cast<uint8_t>(mod_u8(static_cast<int32_t>(v[j]), pm, pinv));
+                                    q += ldo;
+                                }
+                                continue;
+                            }
+                        }
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
                             if (col0 + j < P.n) {
-                                uint8_t* q = dst + static_cast<long long>(col0 + j) * P.ldo;
                                 uint32_t u = mod_u8(static_cast<int32_t>(v[j]), pm, pinv);
                                 if constexpr (KIND == K2_U8ACC) {
                                     // later k chunk (emulator.cpp:57-73): sum of per-block
@@ -486,11 +501,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     u += *q;
                                     u = u >= static_cast<uint32_t>(pm) ? u - pm : u;
                                 }
-                                if (P.hints & 4)
-                                    st_stream_u8(q, u);
-                                else
-                                    *q = static_cast<uint8_t>(u);
+                                *q = static_cast<uint8_t>(u);
                             }
+                            q += ldo;
                         }
                     }
                 } else if constexpr (KIND == K2_I32) {
@@ -525,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(tempty0_leader + 8u * acc);
+            if (lane == 0) mbar_arrive_cluster_relaxed(tempty0_leader + 8u * acc);
         }
     }
 
