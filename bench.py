@@ -330,6 +330,9 @@ def main():
                 "traffic": traffic, "kernel": "residue_gemm_kernel (K2, tcgen05.mma kind::i8)",
                 "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (dense INT8 = 2 x dense BF16 on sm_100)"
                                 if bf16 else "2 x fallback 1.59 PFLOP/s bf16 (B200_PROFILING.md)"),
+                # per stage and step, summed over launches; the A-side and B-side K1
+                # chains run on two streams (overlapping), so scale + residues can
+                # exceed their wall-clock share
                 "stage_ms": {kname: v[0] / args.steps for kname, v in prof.items()},
                 "k2_launches_per_step": prof["products"][1] / args.steps}
     if peaks.get("bf16_tflops_sustained"):

@@ -107,6 +107,8 @@ struct ozk_context {
     int num_sms = 148;
     cudaStream_t stream = nullptr;              // compute stream (user-settable)
     cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of ozk_gemm_host
+    cudaStream_t side = nullptr;                // B-side K1 chain of ozk_gemm (fork/join events)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t launches = 0;
     Buf planes_a, planes_b, u, stats, ints, flags, f32a, f32b, host_a, host_b, host_c, wide, cbar;
     int32_t* flags_host = nullptr;  // pinned mirror of the device flag word
@@ -175,6 +177,14 @@ struct StageTimer {
         cudaEventRecord(e1, h->stream);
         h->pending.push_back({slot, {e0, e1}});
     }
+};
+
+// runs the enclosed stages on the handle's side stream (h->stream swapped)
+struct OnSideStream {
+    ozk_context* h;
+    cudaStream_t saved;
+    explicit OnSideStream(ozk_context* hh) : h(hh), saved(hh->stream) { h->stream = h->side; }
+    ~OnSideStream() { h->stream = saved; }
 };
 
 int check_launch(ozk_context* h, int n_kernels) {
@@ -395,11 +405,15 @@ int stage_rows(ozk_context* h, Job& J) {
 
 // columns [j0, j0+nj) of B: stats and fast-mode nu, or accurate-mode nu', the
 // Bbar block and the bound GEMM Abar * Bbar_block (row maxima accumulate)
-int stage_cols(ozk_context* h, Job& J, int64_t j0, int64_t nj) {
+// part: 0 everything; 1 up to the bound operand (accurate: B-bar planes), which
+// needs only B; 2 the bound GEMM alone (needs the A-bar planes too)
+int stage_cols(ozk_context* h, Job& J, int64_t j0, int64_t nj, int part = 0) {
     const void* bj = b_block(J, j0);
     // this block's [split][nj] partials
     double* bmax = J.bmax + J.splits_b * j0;
     double* bsum = J.bsum + J.splits_b * j0;
+    int8_t* bbar = J.pb + b_plane_off(J, j0);
+    if (part == 2) goto bound_gemm;
     if (J.tb)
         launch_row_stats(bj, J.in_f32, nj, J.k, J.ldb, J.splits_b, bmax, bsum, J.flags, h->stream);
     else
@@ -412,7 +426,6 @@ int stage_cols(ozk_context* h, Job& J, int64_t j0, int64_t nj) {
         return check_launch(h, 2);
     }
     launch_accurate_base(bmax, J.splits_b, nj, J.nb + j0, h->stream);
-    int8_t* bbar = J.pb + b_plane_off(J, j0);
     b_planes(h, J, j0, nj, J.nb, 1, J.pb, J.pb_stride);
     OZK_CUDA(cudaMemsetAsync(J.colmax + j0, 0, sizeof(int32_t) * nj, h->stream));
     if (J.wide_bound) {
@@ -420,6 +433,8 @@ int stage_cols(ozk_context* h, Job& J, int64_t j0, int64_t nj) {
         OZK_TRY(ensure(h->cbar, sizeof(long long) * J.m * nj));
     }
     OZK_TRY(check_launch(h, 2));
+    if (part == 1) return OZK_OK;
+bound_gemm:
     K2Launch L{};
     L.a_planes = J.pa;
     L.b_planes = bbar;
@@ -564,17 +579,54 @@ int gemm_device(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, i
     Job J{};
     OZK_TRY(setup(h, J, cfg, c, m, n, k, A, lda, B, ldb, true));
     const int c_f32 = cfg->c_type == OZK_R32F;
+    const bool fast = J.mode == OZK_FAST;
     {
         StageTimer total(h, OZK_PROFILE_TOTAL);
+        // A's rows on the handle's stream, B's columns on the side stream: the two
+        // chains of small K1 kernels overlap (what bounds small problems); they
+        // share no buffers (separate partials, exponents and flag words)
+        OZK_CUDA(cudaEventRecord(h->ev_fork, h->stream));
+        OZK_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
         {
             StageTimer t(h, OZK_PROFILE_SCALE);
-            OZK_TRY(scale_all(h, J, cfg));
+            OZK_TRY(round_a(h, J, cfg));
+            OZK_TRY(stage_rows(h, J));
         }
-        {
+        if (fast) {
             StageTimer t(h, OZK_PROFILE_RESIDUES);
             OZK_TRY(stage_row_residues(h, J, J.mu, J.pa));
         }
-        OZK_TRY(compute_block(h, J, 0, n, alpha, beta, C, ldc, c_f32));
+        {
+            OnSideStream side(h);
+            {
+                StageTimer t(h, OZK_PROFILE_SCALE);
+                OZK_TRY(round_b(h, J, cfg, J.b, J.ldb, 0, n));
+                OZK_TRY(stage_cols(h, J, 0, n, fast ? 0 : 1));
+            }
+            if (fast) {
+                StageTimer t(h, OZK_PROFILE_RESIDUES);
+                OZK_TRY(stage_col_residues(h, J, 0, n, J.nu, J.pb, J.pb_stride));
+            }
+            OZK_CUDA(cudaEventRecord(h->ev_join, h->stream));
+        }
+        OZK_CUDA(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+        if (!fast) {  // the bound GEMM needs both bound operands, mu and nu need its maxima
+            {
+                StageTimer t(h, OZK_PROFILE_SCALE);
+                OZK_TRY(stage_cols(h, J, 0, n, 2));
+                OZK_TRY(stage_budget(h, J));
+            }
+            StageTimer t(h, OZK_PROFILE_RESIDUES);
+            OZK_TRY(stage_row_residues(h, J, J.mu, J.pa));
+            OZK_TRY(stage_col_residues(h, J, 0, n, J.nu, J.pb, J.pb_stride));
+        }
+        {
+            StageTimer t(h, OZK_PROFILE_PRODUCTS);
+            OZK_TRY(stage_products(h, J, 0, n, J.pa, J.pa_stride, J.pb, J.pb_stride, OZK_PRODUCTS_U8, J.u, J.ldu,
+                                   J.n * J.ldu));
+        }
+        StageTimer t(h, OZK_PROFILE_RECONSTRUCT);
+        OZK_TRY(stage_reconstruct(h, J, 0, n, J.u, J.ldu, J.n * J.ldu, J.mu, J.nu, alpha, beta, C, ldc, c_f32));
     }
     return finish_check(h, J, h->stream);
 }
@@ -935,6 +987,13 @@ int ozk_create(ozk_handle* handle, int device) {
         delete h;
         return cuda_fail("cudaMallocHost", e);
     }
+    if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        ozk_destroy(h);
+        set_error("side stream / events");
+        return OZK_CUDA_ERROR;
+    }
     // the device flag words (non-finite, flagged lines, K2 lockstep counters):
     // allocated and cleared once, so the sticky OZK_FLAG_ASYNC word starts at 0
     if (ensure(h->flags, 2048) != OZK_OK || cudaMemset(h->flags.p, 0, 2048) != cudaSuccess) {
@@ -955,6 +1014,9 @@ int ozk_destroy(ozk_handle h) {
                    &h->host_b, &h->host_c})
         if (b->p) cudaFree(b->p);
     if (h->flags_host) cudaFreeHost(h->flags_host);
+    if (h->side) cudaStreamDestroy(h->side);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->h2d) cudaStreamDestroy(h->h2d);
     if (h->d2h) cudaStreamDestroy(h->d2h);
     for (auto& p : h->pending) {
