@@ -86,6 +86,72 @@ __global__ void __launch_bounds__(kRowTile* kColGroups)
     }
 }
 
+// FP64 rows, vectorised: a block still owns 64 rows x one k-split, but each
+// lane reads two adjacent rows (16 B) of a column and the 8 warps take every
+// 8th column, 4 columns in flight per lane: a warp moves 512 B per column
+// and a thread keeps 64 B of loads outstanding (the scalar kernel above has
+// 16 B). Needs 16-byte aligned columns (even lda, aligned A) and full 64-row
+// tiles; anything else takes row_stats_kernel. The sums run in a different
+// order than the scalar kernel's, which the fast-mode guard band allows for
+// (any order is within (k+1)u of the exact sum).
+constexpr int kVecGroups = 8;
+__global__ void __launch_bounds__(32 * kVecGroups)
+    row_stats_vec_kernel(const double* __restrict__ a, int64_t m, int64_t k, int64_t lda, int64_t k_per_split,
+                         double* __restrict__ pmax, double* __restrict__ psum, int32_t* __restrict__ nonfinite) {
+    __shared__ double smax[kVecGroups][kRowTile];
+    __shared__ double ssum[kVecGroups][kRowTile];
+    const int lane = threadIdx.x % 32, g = threadIdx.x / 32;
+    const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kRowTile + 2 * lane;
+    const int64_t j0 = static_cast<int64_t>(blockIdx.y) * k_per_split;
+    const int64_t j1 = j0 + k_per_split < k ? j0 + k_per_split : k;
+    const double* p = a + row0;
+    double mx0 = 0.0, mx1 = 0.0, s0 = 0.0, s1 = 0.0, t0 = 0.0, t1 = 0.0;
+    int64_t j = j0 + g;
+    for (; j + 3 * kVecGroups < j1; j += 4 * kVecGroups) {
+        double2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const double2*>(p + (j + u * kVecGroups) * lda));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            mx0 = fmax(mx0, fabs(v[u].x));
+            mx1 = fmax(mx1, fabs(v[u].y));
+            if (u & 1) {
+                t0 = __fma_rn(v[u].x, v[u].x, t0);
+                t1 = __fma_rn(v[u].y, v[u].y, t1);
+            } else {
+                s0 = __fma_rn(v[u].x, v[u].x, s0);
+                s1 = __fma_rn(v[u].y, v[u].y, s1);
+            }
+        }
+    }
+    for (; j < j1; j += kVecGroups) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(p + j * lda));
+        mx0 = fmax(mx0, fabs(v.x));
+        mx1 = fmax(mx1, fabs(v.y));
+        s0 = __fma_rn(v.x, v.x, s0);
+        s1 = __fma_rn(v.y, v.y, s1);
+    }
+    s0 += t0;
+    s1 += t1;
+    if (__any_sync(0xffffffffu, isinf(mx0) || isinf(mx1) || isnan(s0 + s1)) && lane == 0) atomicOr(nonfinite, 1);
+    smax[g][2 * lane] = mx0;
+    smax[g][2 * lane + 1] = mx1;
+    ssum[g][2 * lane] = s0;
+    ssum[g][2 * lane + 1] = s1;
+    __syncthreads();
+    if (threadIdx.x < kRowTile) {
+        const int r = threadIdx.x;
+        double M = smax[0][r], S = ssum[0][r];
+        for (int q = 1; q < kVecGroups; ++q) {
+            M = fmax(M, smax[q][r]);
+            S += ssum[q][r];
+        }
+        const int64_t row = static_cast<int64_t>(blockIdx.x) * kRowTile + r;
+        pmax[static_cast<int64_t>(blockIdx.y) * m + row] = M;
+        psum[static_cast<int64_t>(blockIdx.y) * m + row] = S;
+    }
+}
+
 // one warp per column of B (contiguous), 8 loads in flight per lane
 __global__ void __launch_bounds__(256)
     col_stats_kernel(const void* __restrict__ b, int is_f32, int64_t k, int64_t n, int64_t ldb,
@@ -253,6 +319,12 @@ int row_stats_splits(int64_t m, int64_t k) {
 void launch_row_stats(const void* a, int is_f32, int64_t m, int64_t k, int64_t lda, int splits, double* pmax,
                       double* psum, int32_t* nonfinite, cudaStream_t s) {
     const int64_t kps = (k + splits - 1) / splits;
+    if (!is_f32 && m % kRowTile == 0 && lda % 2 == 0 && reinterpret_cast<uintptr_t>(a) % 16 == 0) {
+        dim3 grid(static_cast<unsigned>(m / kRowTile), static_cast<unsigned>(splits));
+        row_stats_vec_kernel<<<grid, 32 * kVecGroups, 0, s>>>(static_cast<const double*>(a), m, k, lda, kps, pmax,
+                                                              psum, nonfinite);
+        return;
+    }
     dim3 grid(static_cast<unsigned>((m + kRowTile - 1) / kRowTile), static_cast<unsigned>(splits));
     row_stats_kernel<<<grid, kRowTile * kColGroups, 0, s>>>(a, is_f32, m, k, lda, kps, pmax, psum, nonfinite);
 }
