@@ -363,3 +363,43 @@ def test_host_streamed_matches_oracle(oracle):
     b = gen_matrix(k, n, 0.5, 74)
     got = gemm_emulated(a, b, EmuConfig(n_moduli=13)).c
     np.testing.assert_array_equal(_bits(got), _bits(oracle.gemm(a, b, 13, 0)))
+
+
+@pytest.mark.parametrize("entry", [3, 8, 13])
+def test_fault_injection_corrupt_s1_is_located(ctx, oracle, entry):
+    """SPEC.md:461 fault injection through the explicit-constants overload
+    (emulator.hpp:28-32): one corrupted s1 entry must make the CRT exactness
+    check fail, and the stage exports locate it — the residue planes and the
+    per-modulus U_i still equal the oracle, only the reconstruction differs.
+    (Not entry 0: integer inputs scaled by 2^mu >= 2^8 have all residues mod
+    256 equal to 0, so s1[0] never contributes; fast mode is excluded because
+    it is inexact on these inputs in the reference too.)"""
+    from paper_2508_03984_b200 import build_constants
+
+    N, m, n, k = 14, 48, 40, 64
+    a = gen_int_matrix(m, k, 100, seed=17)
+    b = gen_int_matrix(k, n, 100, seed=18)
+    exact = a @ b  # small integers: the FP64 product is exact
+    good = build_constants(N)
+    bad = build_constants(N)
+    bad.s1[entry] = bad.s1[entry] * (1.0 + 2.0 ** -20)
+    A = torch.from_numpy(np.ascontiguousarray(a.T)).cuda().t()
+    B = torch.from_numpy(np.ascontiguousarray(b.T)).cuda().t()
+    cfg = EmuConfig(n_moduli=N, mode=ScaleMode.Accurate)
+    C_good = torch.zeros((n, m), dtype=torch.float64, device="cuda").t()
+    C_bad = torch.zeros((n, m), dtype=torch.float64, device="cuda").t()
+    ctx.gemm(A, B, cfg, C_good, constants=good)
+    ctx.gemm(A, B, cfg, C_bad, constants=bad)
+    np.testing.assert_array_equal(C_good.cpu().numpy(), exact)  # the exactness check passes ...
+    assert not np.array_equal(C_bad.cpu().numpy(), exact)      # ... and catches the corruption
+    # locate it: the products stage (independent of s1) still matches the oracle
+    mu = torch.zeros(m, dtype=torch.int32, device="cuda")
+    nu = torch.zeros(n, dtype=torch.int32, device="cuda")
+    ctx.stage_scale(A, B, cfg, mu, nu)
+    pa = torch.zeros((N, k, ctx.plane_ld(m)), dtype=torch.int8, device="cuda")
+    pb = torch.zeros((N, n, ctx.plane_ld(k)), dtype=torch.int8, device="cuda")
+    ctx.stage_residues(A, B, cfg, mu, nu, pa, pb)
+    ldu = (m + 15) // 16 * 16
+    U = torch.zeros((N, n, ldu), dtype=torch.uint8, device="cuda")
+    ctx.stage_products(cfg, m, n, k, pa, pb, _lib.OZK_PRODUCTS_U8, U, ldu)
+    np.testing.assert_array_equal(U.cpu().numpy()[:, :, :m].transpose(0, 2, 1), oracle.products_u8(a, b, N, 1))
