@@ -97,6 +97,7 @@ struct Job {
     int32_t* flags;  // [0] non-finite, [1] flagged rows, [2] flagged columns, [4..] K2 lockstep words (1 KB)
     double *amax, *asum, *bmax, *bsum;
     int splits, splits_b;  // k-partials of the row-stat reductions of op(A) (!ta) / op(B) (tb)
+    int32_t *cnt_a, *cnt_b;  // last-block counters of the row-stat reductions (A side / B side)
     int8_t *pa, *pb;
     uint8_t* u;
 };
@@ -110,7 +111,7 @@ struct ozk_context {
     cudaStream_t side = nullptr;                // B-side K1 chain of ozk_gemm (fork/join events)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t launches = 0;
-    Buf planes_a, planes_b, u, stats, ints, flags, f32a, f32b, host_a, host_b, host_c, wide, cbar;
+    Buf planes_a, planes_b, u, stats, ints, flags, f32a, f32b, host_a, host_b, host_c, wide, cbar, counters;
     int32_t* flags_host = nullptr;  // pinned mirror of the device flag word
     // stage timing (ozk_profile): CUDA events on the compute stream
     bool profiling = false;
@@ -266,6 +267,14 @@ int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c,
     OZK_TRY(ensure(h->flags, 2048));
     OZK_TRY(ensure(h->stats, sizeof(double) * (2 * J.splits * m + 2 * J.splits_b * n)));
     OZK_TRY(ensure(h->ints, sizeof(int32_t) * 4 * (m + n)));
+    {
+        const size_t cbytes = sizeof(int32_t) * (row_stat_groups(m) + row_stat_groups(n) + 2);
+        const bool grow = !h->counters.p || cbytes > h->counters.bytes;
+        OZK_TRY(ensure(h->counters, cbytes));
+        if (grow) OZK_CUDA(cudaMemsetAsync(h->counters.p, 0, h->counters.bytes, h->stream));  // then self-resetting
+        J.cnt_a = static_cast<int32_t*>(h->counters.p);
+        J.cnt_b = J.cnt_a + row_stat_groups(m) + 1;
+    }
     if (need_products) {
         OZK_TRY(ensure(h->planes_a, static_cast<size_t>(N * J.pa_stride)));
         OZK_TRY(ensure(h->planes_b, static_cast<size_t>(N * J.pb_stride)));
@@ -358,12 +367,36 @@ const void* b_block(const Job& J, int64_t j0) {
 // byte offset of op(B)'s column j0 inside a B plane
 int64_t b_plane_off(const Job& J, int64_t j0) { return J.tb ? j0 : j0 * J.ld; }
 
-// op(A)'s rows: row stats over A's rows, or column stats over the stored k x m A^T
+// what the reductions finalize per line: fast-mode exponents (exp_out), or
+// accurate-mode bases (exp_out) with the bound maxima cleared (zero_out);
+// element h of line l at base[l*line_step + h*elem_step] for the exact recompute
+LineFinal line_final(const Job& J, int32_t* exp_out, int32_t* zero_out, const void* base, int64_t line_step,
+                     int64_t elem_step) {
+    LineFinal F{};
+    F.mode = J.mode;
+    F.prec = J.dc.precision;
+    F.fix = J.dc.fast_fix;
+    F.pp_fast = J.dc.pp_fast;
+    F.k = J.k;
+    F.exp_out = exp_out;
+    F.zero_out = zero_out;
+    F.base = base;
+    F.is_f32 = J.in_f32;
+    F.line_step = line_step;
+    F.elem_step = elem_step;
+    return F;
+}
+
+// op(A)'s rows: row stats over A's rows, or column stats over the stored k x m A^T,
+// finalized into mu (fast) or mu' (accurate, rowmax cleared)
 void a_line_stats(ozk_context* h, Job& J) {
+    const bool fast = J.mode == OZK_FAST;
+    const LineFinal F = line_final(J, fast ? J.mu : J.ma, fast ? nullptr : J.rowmax, J.a, J.ta ? J.lda : 1,
+                                   J.ta ? 1 : J.lda);
     if (J.ta)
-        launch_col_stats(J.a, J.in_f32, J.k, J.m, J.lda, J.amax, J.asum, J.flags, h->stream);
+        launch_col_stats(J.a, J.in_f32, J.k, J.m, J.lda, J.amax, J.asum, J.flags, F, h->stream);
     else
-        launch_row_stats(J.a, J.in_f32, J.m, J.k, J.lda, J.splits, J.amax, J.asum, J.flags, h->stream);
+        launch_row_stats(J.a, J.in_f32, J.m, J.k, J.lda, J.splits, J.amax, J.asum, J.flags, J.cnt_a, F, h->stream);
 }
 
 // residues (kind 0) or the bound plane (kind 1) of op(A), in the layout K2 reads
@@ -390,17 +423,10 @@ void b_planes(ozk_context* h, Job& J, int64_t j0, int64_t nj, const int32_t* nu,
 int stage_rows(ozk_context* h, Job& J) {
     a_line_stats(h, J);
     OZK_TRY(check_launch(h, 1));
-    if (J.mode == OZK_FAST) {
-        launch_fast_finalize(J.amax, J.asum, J.splits, J.m, J.k, J.dc, J.mu, J.flags + 1, J.flag_rows, h->stream);
-        launch_fast_exact(J.a, J.in_f32, J.ta ? J.lda : 1, J.ta ? 1 : J.lda, J.k, J.dc, J.flags + 1, J.flag_rows,
-                          J.mu, h->stream);
-        return check_launch(h, 2);
-    }
-    launch_accurate_base(J.amax, J.splits, J.m, J.ma, h->stream);
+    if (J.mode == OZK_FAST) return OZK_OK;
     a_planes(h, J, J.ma, 1, J.pa, J.pa_stride);
-    OZK_CUDA(cudaMemsetAsync(J.rowmax, 0, sizeof(int32_t) * J.m, h->stream));
     if (J.wide_bound) OZK_CUDA(cudaMemsetAsync(J.rowmax64, 0, sizeof(unsigned long long) * J.m, h->stream));
-    return check_launch(h, 2);
+    return check_launch(h, 1);
 }
 
 // columns [j0, j0+nj) of B: stats and fast-mode nu, or accurate-mode nu', the
@@ -414,20 +440,18 @@ int stage_cols(ozk_context* h, Job& J, int64_t j0, int64_t nj, int part = 0) {
     double* bsum = J.bsum + J.splits_b * j0;
     int8_t* bbar = J.pb + b_plane_off(J, j0);
     if (part == 2) goto bound_gemm;
-    if (J.tb)
-        launch_row_stats(bj, J.in_f32, nj, J.k, J.ldb, J.splits_b, bmax, bsum, J.flags, h->stream);
-    else
-        launch_col_stats(bj, J.in_f32, J.k, nj, J.ldb, bmax, bsum, J.flags, h->stream);
-    OZK_TRY(check_launch(h, 1));
-    if (J.mode == OZK_FAST) {
-        launch_fast_finalize(bmax, bsum, J.splits_b, nj, J.k, J.dc, J.nu + j0, J.flags + 2, J.flag_cols, h->stream);
-        launch_fast_exact(bj, J.in_f32, J.tb ? 1 : J.ldb, J.tb ? J.ldb : 1, J.k, J.dc, J.flags + 2, J.flag_cols,
-                          J.nu + j0, h->stream);
-        return check_launch(h, 2);
+    {
+        const bool fast = J.mode == OZK_FAST;
+        const LineFinal F = line_final(J, fast ? J.nu + j0 : J.nb + j0, fast ? nullptr : J.colmax + j0, bj,
+                                       J.tb ? 1 : J.ldb, J.tb ? J.ldb : 1);
+        if (J.tb)
+            launch_row_stats(bj, J.in_f32, nj, J.k, J.ldb, J.splits_b, bmax, bsum, J.flags, J.cnt_b, F, h->stream);
+        else
+            launch_col_stats(bj, J.in_f32, J.k, nj, J.ldb, bmax, bsum, J.flags, F, h->stream);
     }
-    launch_accurate_base(bmax, J.splits_b, nj, J.nb + j0, h->stream);
+    OZK_TRY(check_launch(h, 1));
+    if (J.mode == OZK_FAST) return OZK_OK;
     b_planes(h, J, j0, nj, J.nb, 1, J.pb, J.pb_stride);
-    OZK_CUDA(cudaMemsetAsync(J.colmax + j0, 0, sizeof(int32_t) * nj, h->stream));
     if (J.wide_bound) {
         OZK_CUDA(cudaMemsetAsync(J.colmax64 + j0, 0, sizeof(unsigned long long) * nj, h->stream));
         OZK_TRY(ensure(h->cbar, sizeof(long long) * J.m * nj));
@@ -690,12 +714,10 @@ int rows_block(ozk_context* h, Job& J, int64_t r0, int64_t mr, const void* a, in
     int splits = row_stats_splits(mr, J.k);
     const int64_t cap = J.splits * J.m / mr;  // the [split][rows] partials live in J.amax / J.asum
     if (splits > cap) splits = static_cast<int>(cap < 1 ? 1 : cap);
-    launch_row_stats(a, J.in_f32, mr, J.k, lda, splits, J.amax, J.asum, J.flags, h->stream);
-    OZK_CUDA(cudaMemsetAsync(J.flags + 1, 0, sizeof(int32_t), h->stream));
-    launch_fast_finalize(J.amax, J.asum, splits, mr, J.k, J.dc, J.mu + r0, J.flags + 1, J.flag_rows, h->stream);
-    launch_fast_exact(a, J.in_f32, 1, lda, J.k, J.dc, J.flags + 1, J.flag_rows, J.mu + r0, h->stream);
+    launch_row_stats(a, J.in_f32, mr, J.k, lda, splits, J.amax, J.asum, J.flags, J.cnt_a,
+                     line_final(J, J.mu + r0, nullptr, a, 1, lda), h->stream);
     launch_a_planes(a, J.in_f32, mr, J.k, lda, J.mu + r0, J.dc, 0, J.pa + r0, J.lda_p, J.pa_stride, h->stream);
-    return check_launch(h, 4);
+    return check_launch(h, 2);
 }
 
 int stream_a_block(ozk_context* h, Job& J, int64_t r0, int64_t mr) {
@@ -1009,7 +1031,7 @@ int ozk_create(ozk_handle* handle, int device) {
 int ozk_destroy(ozk_handle h) {
     if (!h) return OZK_OK;
     cudaSetDevice(h->device);
-    for (Buf* b : {&h->wide, &h->cbar, &h->planes_a, &h->planes_b, &h->u, &h->stats, &h->ints, &h->flags, &h->f32a,
+    for (Buf* b : {&h->wide, &h->cbar, &h->counters, &h->planes_a, &h->planes_b, &h->u, &h->stats, &h->ints, &h->flags, &h->f32a,
                    &h->f32b, &h->host_a,
                    &h->host_b, &h->host_c})
         if (b->p) cudaFree(b->p);

@@ -1,22 +1,24 @@
 // K1a — scale exponents (reference: scaling.cpp:20-184).
 //
 // Memory-bound reductions over the FP64/FP32 inputs, one HBM read of A and of
-// B per pass:
+// B per pass, with the per-line exponent step fused in (no separate launches):
 //   * row_stats  : per row of column-major A, max|a| and sum a^2 (partial per
-//                  k-split), 64 rows x 8 B = 512 B coalesced per column;
-//   * col_stats  : per column of B, one warp streams the contiguous column;
+//                  k-split); the last block of each 64-row group combines the
+//                  splits and finalizes those rows;
+//   * col_stats  : per column of B, one warp streams the contiguous column and
+//                  finalizes it;
 //   * finalize   : fast mode evaluates the budget of fast_exponent
-//                  (scaling.cpp:50-56) from the order-free sum and FLAGS every
-//                  line whose floor() argument lies within `guard` of an
-//                  integer (or whose magnitude leaves the a^2-safe range);
-//   * exact      : flagged lines are recomputed in the reference's sequential
-//                  order (scaling.cpp:69-78 rows, :90-94 columns) — products in
-//                  parallel across a warp, the additions strictly in index
-//                  order on lane 0 — so mu/nu are bit-identical to the
-//                  reference (the floor can only differ inside the guard band).
-//   * accurate   : mu'/nu' = 2^(5 - ilogb max) (scaling.cpp:110-116) and, after
-//                  the Abar*Bbar bound GEMM (K2 with the max epilogue), the
-//                  budget of scaling.cpp:151-165.
+//                  (scaling.cpp:50-56) from the order-free sum; a line whose
+//                  floor() argument lies within `guard` of an integer (or whose
+//                  magnitude leaves the a^2-safe range) is recomputed at once
+//                  in the reference's sequential order (scaling.cpp:69-78 rows,
+//                  :90-94 columns) — products in parallel across a warp, the
+//                  additions strictly in index order — so mu/nu are
+//                  bit-identical to the reference (the floor can only differ
+//                  inside the guard band). Accurate mode: mu'/nu' =
+//                  2^(5 - ilogb max) (scaling.cpp:110-116), the line's bound
+//                  maximum cleared; after the Abar*Bbar bound GEMM (K2 with the
+//                  max epilogue) the budget of scaling.cpp:151-165.
 #include <cfloat>
 #include <climits>
 
@@ -28,9 +30,96 @@ namespace {
 constexpr int kRowTile = 64;  // rows per block in row_stats
 constexpr int kColGroups = 4; // column groups per block in row_stats
 
+// Guard band of the parallel sum against the reference's sequential one: both
+// approximate S = sum (a 2^-g)^2 within (k+1) u S, so their budgets differ by
+// at most 0.51 * 2 (k+1) u / ln 2 < 1.5 (k+1) u; log2/round-off adds < 1e-13.
+__device__ __forceinline__ double guard_band(int64_t k) { return 4.0 * static_cast<double>(k + 2) * 0x1.0p-53 + 1e-11; }
+
+__device__ __forceinline__ bool needs_exact(double y, double mx, int64_t k) {
+    const double d = fmin(y - floor(y), ceil(y) - y);
+    // |x| >= 2^500 could overflow sum x^2; tiny maxima could underflow it
+    return d < guard_band(k) || mx >= 0x1.0p+500 || mx < 0x1.0p-400;
+}
+
+// fast / accurate exponent of one line from its max and sum of squares;
+// returns whether the line needs the exact sequential recompute
+__device__ __forceinline__ bool finalize_line(const LineFinal& F, int64_t line, double mx, double s) {
+    if (F.mode == OZK_FAST) {
+        int e = 0;  // zero line: sentinel mu = 1 (scaling.cpp:80, :88)
+        bool flag = false;
+        if (mx != 0.0) {
+            const int g = ilogb(mx);
+            const double y = fast_budget(ldexp(s, -2 * g), F.k, F.pp_fast);
+            e = fast_exponent_from_budget(y, g, F.prec, F.fix);
+            flag = needs_exact(y, mx, F.k);
+        }
+        F.exp_out[line] = e;
+        return flag;
+    }
+    F.exp_out[line] = mx != 0.0 ? 5 - ilogb(mx) : INT32_MIN;
+    if (F.zero_out) F.zero_out[line] = 0;
+    return false;
+}
+
+// Warp-collective, reference order: s = 0; for h: nh = ldexp(x_h, -g); s += nh*nh (no FMA).
+__device__ void exact_line(const LineFinal& F, int64_t line, int lane) {
+    const int64_t off = line * F.line_step;
+    const int64_t k = F.k;
+    double mx = 0.0;
+    for (int64_t h = lane; h < k; h += 32) mx = fmax(mx, fabs(load_as_double(F.base, off + h * F.elem_step, F.is_f32)));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int g = ilogb(mx);
+    double s = 0.0;
+    for (int64_t h0 = 0; h0 < k; h0 += 32) {
+        const int64_t h = h0 + lane;
+        double sq = 0.0;
+        if (h < k) {
+            const double nh = ldexp(load_as_double(F.base, off + h * F.elem_step, F.is_f32), -g);
+            sq = __dmul_rn(nh, nh);
+        }
+        const int cnt = k - h0 < 32 ? static_cast<int>(k - h0) : 32;
+        for (int q = 0; q < cnt; ++q) s = __dadd_rn(s, __shfl_sync(0xffffffffu, sq, q));
+    }
+    if (lane == 0) F.exp_out[line] = fast_exponent_from_budget(fast_budget(s, k, F.pp_fast), g, F.prec, F.fix);
+}
+
+// The last block of a 64-row group (over its k-splits) combines the partials
+// [split][lines] of its rows, finalizes them and recomputes flagged rows.
+// Called by every block after writing its partials; returns at once unless last.
+__device__ void row_group_finalize(const LineFinal& F, const double* pmax, const double* psum, int splits,
+                                   int64_t lines, int32_t* counters) {
+    __shared__ int s_last, s_nflag;
+    __shared__ int s_flag[kRowTile];
+    __syncthreads();  // this block's partials are written
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(counters + blockIdx.x, 1) == splits - 1;
+        s_nflag = 0;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();  // the other splits' partials are visible
+    if (threadIdx.x == 0) counters[blockIdx.x] = 0;  // ready for the next call
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * kRowTile + threadIdx.x;
+    if (threadIdx.x < kRowTile && row < lines) {
+        double mx = pmax[row], sm = psum[row];
+        for (int q = 1; q < splits; ++q) {
+            mx = fmax(mx, pmax[q * lines + row]);
+            sm += psum[q * lines + row];
+        }
+        if (finalize_line(F, row, mx, sm)) s_flag[atomicAdd(&s_nflag, 1)] = threadIdx.x;
+    }
+    __syncthreads();
+    const int nflag = s_nflag;
+    for (int w = threadIdx.x / 32; w < nflag; w += blockDim.x / 32)
+        exact_line(F, static_cast<int64_t>(blockIdx.x) * kRowTile + s_flag[w], threadIdx.x % 32);
+}
+
 __global__ void __launch_bounds__(kRowTile* kColGroups)
     row_stats_kernel(const void* __restrict__ a, int is_f32, int64_t m, int64_t k, int64_t lda, int64_t k_per_split,
-                     double* __restrict__ pmax, double* __restrict__ psum, int32_t* __restrict__ nonfinite) {
+                     double* __restrict__ pmax, double* __restrict__ psum, int32_t* __restrict__ nonfinite,
+                     int32_t* __restrict__ counters, const LineFinal F) {
     __shared__ double smax[kColGroups][kRowTile];
     __shared__ double ssum[kColGroups][kRowTile];
     const int r = threadIdx.x % kRowTile, g = threadIdx.x / kRowTile;
@@ -84,6 +173,7 @@ __global__ void __launch_bounds__(kRowTile* kColGroups)
         pmax[static_cast<int64_t>(blockIdx.y) * m + row] = M;
         psum[static_cast<int64_t>(blockIdx.y) * m + row] = S;
     }
+    row_group_finalize(F, pmax, psum, gridDim.y, m, counters);
 }
 
 // FP64 rows, vectorised: a block still owns 64 rows x one k-split, but each
@@ -97,7 +187,8 @@ __global__ void __launch_bounds__(kRowTile* kColGroups)
 constexpr int kVecGroups = 8;
 __global__ void __launch_bounds__(32 * kVecGroups)
     row_stats_vec_kernel(const double* __restrict__ a, int64_t m, int64_t k, int64_t lda, int64_t k_per_split,
-                         double* __restrict__ pmax, double* __restrict__ psum, int32_t* __restrict__ nonfinite) {
+                         double* __restrict__ pmax, double* __restrict__ psum, int32_t* __restrict__ nonfinite,
+                         int32_t* __restrict__ counters, const LineFinal F) {
     __shared__ double smax[kVecGroups][kRowTile];
     __shared__ double ssum[kVecGroups][kRowTile];
     const int lane = threadIdx.x % 32, g = threadIdx.x / 32;
@@ -150,12 +241,14 @@ __global__ void __launch_bounds__(32 * kVecGroups)
         pmax[static_cast<int64_t>(blockIdx.y) * m + row] = M;
         psum[static_cast<int64_t>(blockIdx.y) * m + row] = S;
     }
+    row_group_finalize(F, pmax, psum, gridDim.y, m, counters);
 }
 
 // one warp per column of B (contiguous), 8 loads in flight per lane
 __global__ void __launch_bounds__(256)
     col_stats_kernel(const void* __restrict__ b, int is_f32, int64_t k, int64_t n, int64_t ldb,
-                     double* __restrict__ cmax, double* __restrict__ csum, int32_t* __restrict__ nonfinite) {
+                     double* __restrict__ cmax, double* __restrict__ csum, int32_t* __restrict__ nonfinite,
+                     const LineFinal F) {
     const int lane = threadIdx.x % 32;
     const int64_t col = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
     if (col >= n) return;
@@ -203,81 +296,9 @@ __global__ void __launch_bounds__(256)
         csum[col] = sum;
         if (isinf(mx) || isnan(sum)) atomicOr(nonfinite, 1);
     }
-}
-
-// Guard band of the parallel sum against the reference's sequential one: both
-// approximate S = sum (a 2^-g)^2 within (k+1) u S, so their budgets differ by
-// at most 0.51 * 2 (k+1) u / ln 2 < 1.5 (k+1) u; log2/round-off adds < 1e-13.
-__device__ __forceinline__ double guard_band(int64_t k) { return 4.0 * static_cast<double>(k + 2) * 0x1.0p-53 + 1e-11; }
-
-__device__ __forceinline__ bool needs_exact(double y, double mx, int64_t k) {
-    const double d = fmin(y - floor(y), ceil(y) - y);
-    // |x| >= 2^500 could overflow sum x^2; tiny maxima could underflow it
-    return d < guard_band(k) || mx >= 0x1.0p+500 || mx < 0x1.0p-400;
-}
-
-// One thread per line (a row of A or a column of a B block). Rows combine
-// `splits` k-partials laid out [split][lines].
-__global__ void fast_finalize_kernel(const double* __restrict__ pmax, const double* __restrict__ psum, int splits,
-                                     int64_t lines, int64_t k, float pp_fast, int prec, int fix,
-                                     int32_t* __restrict__ exp_out, int32_t* __restrict__ flag_count,
-                                     int32_t* __restrict__ flag_list) {
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= lines) return;
-    double mx = pmax[t], s = psum[t];
-    for (int q = 1; q < splits; ++q) {
-        mx = fmax(mx, pmax[q * lines + t]);
-        s += psum[q * lines + t];
-    }
-    int e = 0;  // zero line: sentinel mu = 1 (scaling.cpp:80, :88)
-    if (mx != 0.0) {
-        const int g = ilogb(mx);
-        const double y = fast_budget(ldexp(s, -2 * g), k, pp_fast);
-        e = fast_exponent_from_budget(y, g, prec, fix);
-        if (needs_exact(y, mx, k)) flag_list[atomicAdd(flag_count, 1)] = static_cast<int32_t>(t);
-    }
-    exp_out[t] = e;
-}
-
-// One warp per flagged line: element h of line l sits at base[l*line_step + h*elem_step].
-// Reference order: s = 0; for h: nh = ldexp(x_h, -g); s += nh*nh (no FMA).
-__global__ void fast_exact_kernel(const void* __restrict__ base, int is_f32, int64_t line_step, int64_t elem_step,
-                                  int64_t k, float pp_fast, int prec, int fix, const int32_t* __restrict__ flag_count,
-                                  const int32_t* __restrict__ flag_list, int32_t* __restrict__ exp_out) {
-    const int lane = threadIdx.x % 32;
-    const int warps = gridDim.x * (blockDim.x / 32);
-    const int count = *flag_count;
-    for (int w = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; w < count; w += warps) {
-        const int64_t line = flag_list[w];
-        const int64_t off = line * line_step;
-        double mx = 0.0;
-        for (int64_t h = lane; h < k; h += 32) mx = fmax(mx, fabs(load_as_double(base, off + h * elem_step, is_f32)));
-#pragma unroll
-        for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        const int g = ilogb(mx);
-        double s = 0.0;
-        for (int64_t h0 = 0; h0 < k; h0 += 32) {
-            const int64_t h = h0 + lane;
-            double sq = 0.0;
-            if (h < k) {
-                const double nh = ldexp(load_as_double(base, off + h * elem_step, is_f32), -g);
-                sq = __dmul_rn(nh, nh);
-            }
-            const int cnt = k - h0 < 32 ? static_cast<int>(k - h0) : 32;
-            for (int q = 0; q < cnt; ++q) s = __dadd_rn(s, __shfl_sync(0xffffffffu, sq, q));
-        }
-        if (lane == 0) exp_out[line] = fast_exponent_from_budget(fast_budget(s, k, pp_fast), g, prec, fix);
-    }
-}
-
-// mu' = 2^(5 - ilogb max|a_i.|) (scaling.cpp:112-116); INT32_MIN marks a zero line
-__global__ void accurate_base_kernel(const double* __restrict__ pmax, int splits, int64_t lines,
-                                     int32_t* __restrict__ out) {
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= lines) return;
-    double mx = pmax[t];
-    for (int q = 1; q < splits; ++q) mx = fmax(mx, pmax[q * lines + t]);
-    out[t] = mx != 0.0 ? 5 - ilogb(mx) : INT32_MIN;
+    // every lane holds the reduced mx / sum: finalize on lane 0, recompute as a warp
+    const bool flag = __shfl_sync(0xffffffffu, lane == 0 ? finalize_line(F, col, mx, sum) : false, 0);
+    if (flag) exact_line(F, col, lane);
 }
 
 // budget of scaling.cpp:151-165: e = min(floor(pp_accu - 0.51 log2 cmax), cap),
@@ -316,43 +337,26 @@ int row_stats_splits(int64_t m, int64_t k) {
     return static_cast<int>(splits);
 }
 
+int64_t row_stat_groups(int64_t m) { return (m + kRowTile - 1) / kRowTile; }
+
 void launch_row_stats(const void* a, int is_f32, int64_t m, int64_t k, int64_t lda, int splits, double* pmax,
-                      double* psum, int32_t* nonfinite, cudaStream_t s) {
+                      double* psum, int32_t* nonfinite, int32_t* counters, const LineFinal& fin, cudaStream_t s) {
     const int64_t kps = (k + splits - 1) / splits;
     if (!is_f32 && m % kRowTile == 0 && lda % 2 == 0 && reinterpret_cast<uintptr_t>(a) % 16 == 0) {
         dim3 grid(static_cast<unsigned>(m / kRowTile), static_cast<unsigned>(splits));
         row_stats_vec_kernel<<<grid, 32 * kVecGroups, 0, s>>>(static_cast<const double*>(a), m, k, lda, kps, pmax,
-                                                              psum, nonfinite);
+                                                              psum, nonfinite, counters, fin);
         return;
     }
-    dim3 grid(static_cast<unsigned>((m + kRowTile - 1) / kRowTile), static_cast<unsigned>(splits));
-    row_stats_kernel<<<grid, kRowTile * kColGroups, 0, s>>>(a, is_f32, m, k, lda, kps, pmax, psum, nonfinite);
+    dim3 grid(static_cast<unsigned>(row_stat_groups(m)), static_cast<unsigned>(splits));
+    row_stats_kernel<<<grid, kRowTile * kColGroups, 0, s>>>(a, is_f32, m, k, lda, kps, pmax, psum, nonfinite,
+                                                            counters, fin);
 }
 
 void launch_col_stats(const void* b, int is_f32, int64_t k, int64_t n, int64_t ldb, double* pmax, double* psum,
-                      int32_t* nonfinite, cudaStream_t s) {
-    col_stats_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, s>>>(b, is_f32, k, n, ldb, pmax, psum, nonfinite);
-}
-
-void launch_fast_finalize(const double* pmax, const double* psum, int splits, int64_t lines, int64_t k,
-                          const DevConsts& c, int32_t* exp_out, int32_t* flag_count, int32_t* flag_list,
-                          cudaStream_t s) {
-    cudaMemsetAsync(flag_count, 0, sizeof(int32_t), s);
-    fast_finalize_kernel<<<static_cast<unsigned>((lines + 255) / 256), 256, 0, s>>>(
-        pmax, psum, splits, lines, k, c.pp_fast, c.precision, c.fast_fix, exp_out, flag_count, flag_list);
-}
-
-void launch_fast_exact(const void* base, int is_f32, int64_t line_step, int64_t elem_step, int64_t k,
-                       const DevConsts& c, const int32_t* flag_count, const int32_t* flag_list, int32_t* exp_out,
-                       cudaStream_t s) {
-    // The flagged count lives on the device; a fixed grid strides over it, so
-    // the common case (nothing flagged) costs one tiny launch and no host sync.
-    fast_exact_kernel<<<148, 256, 0, s>>>(base, is_f32, line_step, elem_step, k, c.pp_fast, c.precision, c.fast_fix,
-                                          flag_count, flag_list, exp_out);
-}
-
-void launch_accurate_base(const double* pmax, int splits, int64_t lines, int32_t* out, cudaStream_t s) {
-    accurate_base_kernel<<<static_cast<unsigned>((lines + 255) / 256), 256, 0, s>>>(pmax, splits, lines, out);
+                      int32_t* nonfinite, const LineFinal& fin, cudaStream_t s) {
+    col_stats_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, s>>>(b, is_f32, k, n, ldb, pmax, psum, nonfinite,
+                                                                        fin);
 }
 
 void launch_accurate_budget(const int32_t* base, const int32_t* cmax, int64_t lines, const DevConsts& c,

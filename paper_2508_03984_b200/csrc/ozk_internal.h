@@ -43,22 +43,31 @@ inline int64_t u_ld(int64_t m) { return (m + 15) / 16 * 16; }
 // Per-line reductions (rows of A split over k into `splits` partials laid out
 // [split][m]; columns of B one warp each): max |x| and sum x^2, plus the
 // non-finite flag of emulator.cpp:19-22.
+// The per-line exponent step fused into the reductions above (no separate
+// finalize launches): fast mode writes mu/nu (lines whose budget lies within
+// the guard band of an integer are recomputed in the reference's sequential
+// order by one warp, element h of line l at base[l*line_step + h*elem_step]);
+// accurate mode writes mu'/nu' (5 - ilogb max; INT32_MIN = zero line) and
+// clears the line's bound-GEMM maximum (zero_out). Row reductions split over
+// k finish in the last block of each 64-row group (counters: one int per
+// group, zero between calls; the last block resets its own).
+struct LineFinal {
+    int mode;  // OZK_FAST / OZK_ACCURATE
+    int prec, fix;
+    float pp_fast;
+    int64_t k;
+    int32_t* exp_out;
+    int32_t* zero_out;
+    const void* base;
+    int is_f32;
+    int64_t line_step, elem_step;
+};
 int row_stats_splits(int64_t m, int64_t k);
+int64_t row_stat_groups(int64_t m);  // counters a launch_row_stats over m lines needs
 void launch_row_stats(const void* a, int is_f32, int64_t m, int64_t k, int64_t lda, int splits, double* pmax,
-                      double* psum, int32_t* nonfinite, cudaStream_t s);
+                      double* psum, int32_t* nonfinite, int32_t* counters, const LineFinal& fin, cudaStream_t s);
 void launch_col_stats(const void* b, int is_f32, int64_t k, int64_t n, int64_t ldb, double* pmax, double* psum,
-                      int32_t* nonfinite, cudaStream_t s);
-// fast mode: exponents + near-boundary flags -> exact sequential recompute.
-// Element h of line l is at base[l*line_step + h*elem_step].
-void launch_fast_finalize(const double* pmax, const double* psum, int splits, int64_t lines, int64_t k,
-                          const DevConsts& c, int32_t* exp_out, int32_t* flag_count, int32_t* flag_list,
-                          cudaStream_t s);
-void launch_fast_exact(const void* base, int is_f32, int64_t line_step, int64_t elem_step, int64_t k,
-                       const DevConsts& c, const int32_t* flag_count, const int32_t* flag_list, int32_t* exp_out,
-                       cudaStream_t s);
-// accurate mode: mu'/nu' exponents (5 - ilogb max; INT32_MIN = zero line) and
-// the budget from the bound-GEMM maxima
-void launch_accurate_base(const double* pmax, int splits, int64_t lines, int32_t* out, cudaStream_t s);
+                      int32_t* nonfinite, const LineFinal& fin, cudaStream_t s);
 void launch_accurate_budget(const int32_t* base, const int32_t* cmax, int64_t lines, const DevConsts& c,
                             int32_t* exp_out, cudaStream_t s);
 // k > 2^19: the bound product accumulates in int64 (K2_ACC64), maxima in uint64

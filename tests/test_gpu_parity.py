@@ -98,6 +98,37 @@ def test_scale_exponents(ctx, oracle, prec, mode, phi):
     np.testing.assert_array_equal(nu.cpu().numpy(), wnu)
 
 
+@pytest.mark.parametrize("m", [192, 190])  # whole 64-row groups (vectorised rows) and a ragged one
+@pytest.mark.parametrize("trans", [False, True])
+def test_scale_flagged_lines_exact_path(ctx, oracle, m, trans):
+    """Lines the fast budget cannot decide from the parallel sum — here maxima
+    outside [2^-400, 2^500) — take the exact sequential recompute inside the
+    reduction kernels (the last block of a row group / the column's warp)."""
+    n, k = 130, 3000
+    a = gen_matrix(m, k, 0.5, 41)
+    b = gen_matrix(k, n, 0.5, 42)
+    a[[3, 70, m - 1], :] *= 2.0 ** -450
+    a[[9, 100], :] *= 2.0 ** 510
+    b[:, [0, 64, n - 1]] *= 2.0 ** -450
+    b[:, [11]] *= 2.0 ** 505
+    cfg = EmuConfig(n_moduli=14, mode=ScaleMode.Fast)
+    wmu, wnu = oracle.scale(a, b, 14, 0)
+    mu = torch.zeros(m, dtype=torch.int32, device="cuda")
+    nu = torch.zeros(n, dtype=torch.int32, device="cuda")
+    ctx.stage_scale(_dev_colmajor(a), _dev_colmajor(b), cfg, mu, nu)
+    np.testing.assert_array_equal(mu.cpu().numpy(), wmu)
+    np.testing.assert_array_equal(nu.cpu().numpy(), wnu)
+    want = oracle.gemm(a, b, 14, 0)
+    if trans:  # the same lines through the transposed-operand reductions (A^T columns, B^T rows)
+        C = torch.zeros((n, m), dtype=torch.float64, device="cuda").t()
+        ctx.gemm(_dev_colmajor(np.asfortranarray(a.T)), _dev_colmajor(np.asfortranarray(b.T)), cfg, C,
+                 trans_a=True, trans_b=True)
+        got = C.cpu().numpy()
+    else:
+        got = gemm_emulated(a, b, cfg).c
+    np.testing.assert_array_equal(_bits(got), _bits(want))
+
+
 @pytest.mark.parametrize("prec", [0, 1])
 @pytest.mark.parametrize("N", [2, 8, 12, 13, 16, 19, 20])
 def test_residue_planes(ctx, oracle, prec, N):
