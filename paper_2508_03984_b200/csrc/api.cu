@@ -493,14 +493,11 @@ bound_gemm:
 
 // accurate mode, after every column block: the budgets (scaling.cpp:151-165)
 int stage_budget(ozk_context* h, Job& J) {
-    if (J.wide_bound) {
-        launch_accurate_budget64(J.ma, J.rowmax64, J.m, J.dc, J.mu, h->stream);
-        launch_accurate_budget64(J.nb, J.colmax64, J.n, J.dc, J.nu, h->stream);
-        return check_launch(h, 2);
-    }
-    launch_accurate_budget(J.ma, J.rowmax, J.m, J.dc, J.mu, h->stream);
-    launch_accurate_budget(J.nb, J.colmax, J.n, J.dc, J.nu, h->stream);
-    return check_launch(h, 2);
+    if (J.wide_bound)
+        launch_accurate_budget64(J.ma, J.rowmax64, J.m, J.mu, J.nb, J.colmax64, J.n, J.nu, J.dc, h->stream);
+    else
+        launch_accurate_budget(J.ma, J.rowmax, J.m, J.mu, J.nb, J.colmax, J.n, J.nu, J.dc, h->stream);
+    return check_launch(h, 1);
 }
 
 int stage_row_residues(ozk_context* h, Job& J, const int32_t* mu, int8_t* pa) {
@@ -640,9 +637,20 @@ int gemm_device(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, i
                 OZK_TRY(stage_cols(h, J, 0, n, 2));
                 OZK_TRY(stage_budget(h, J));
             }
-            StageTimer t(h, OZK_PROFILE_RESIDUES);
-            OZK_TRY(stage_row_residues(h, J, J.mu, J.pa));
-            OZK_TRY(stage_col_residues(h, J, 0, n, J.nu, J.pb, J.pb_stride));
+            // both residue passes at once again (A on this stream, B on the side stream)
+            OZK_CUDA(cudaEventRecord(h->ev_fork, h->stream));
+            OZK_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+            {
+                StageTimer t(h, OZK_PROFILE_RESIDUES);
+                OZK_TRY(stage_row_residues(h, J, J.mu, J.pa));
+            }
+            {
+                OnSideStream side(h);
+                StageTimer t(h, OZK_PROFILE_RESIDUES);
+                OZK_TRY(stage_col_residues(h, J, 0, n, J.nu, J.pb, J.pb_stride));
+                OZK_CUDA(cudaEventRecord(h->ev_join, h->stream));
+            }
+            OZK_CUDA(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
         }
         {
             StageTimer t(h, OZK_PROFILE_PRODUCTS);

@@ -303,11 +303,21 @@ __global__ void __launch_bounds__(256)
 
 // budget of scaling.cpp:151-165: e = min(floor(pp_accu - 0.51 log2 cmax), cap),
 // mu = 2^clamp(mu' exponent + e); cmax == 0 keeps mu'; zero lines keep 1.
+// rows and columns in one launch: lines [0, lines) with (base, cmax_in,
+// exp_out), then [lines, lines + lines2) with the second triple
 template <typename CT>
 __global__ void accurate_budget_kernel(const int32_t* __restrict__ base, const CT* __restrict__ cmax_in,
-                                       int64_t lines, float pp_accu, int prec, int32_t* __restrict__ exp_out) {
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= lines) return;
+                                       int64_t lines, float pp_accu, int prec, int32_t* __restrict__ exp_out,
+                                       const int32_t* __restrict__ base2, const CT* __restrict__ cmax2,
+                                       int64_t lines2, int32_t* __restrict__ exp_out2) {
+    int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= lines) {
+        t -= lines;
+        if (t >= lines2) return;
+        base = base2;
+        cmax_in = cmax2;
+        exp_out = exp_out2;
+    }
     const int32_t b0 = base[t];
     const CT cmax = cmax_in[t];
     int32_t out = 0;
@@ -359,16 +369,18 @@ void launch_col_stats(const void* b, int is_f32, int64_t k, int64_t n, int64_t l
                                                                         fin);
 }
 
-void launch_accurate_budget(const int32_t* base, const int32_t* cmax, int64_t lines, const DevConsts& c,
-                            int32_t* exp_out, cudaStream_t s) {
-    accurate_budget_kernel<int32_t><<<static_cast<unsigned>((lines + 255) / 256), 256, 0, s>>>(
-        base, cmax, lines, c.pp_accu, c.precision, exp_out);
+void launch_accurate_budget(const int32_t* base, const int32_t* cmax, int64_t lines, int32_t* exp_out,
+                            const int32_t* base2, const int32_t* cmax2, int64_t lines2, int32_t* exp_out2,
+                            const DevConsts& c, cudaStream_t s) {
+    accurate_budget_kernel<int32_t><<<static_cast<unsigned>((lines + lines2 + 255) / 256), 256, 0, s>>>(
+        base, cmax, lines, c.pp_accu, c.precision, exp_out, base2, cmax2, lines2, exp_out2);
 }
 
-void launch_accurate_budget64(const int32_t* base, const unsigned long long* cmax, int64_t lines, const DevConsts& c,
-                              int32_t* exp_out, cudaStream_t s) {
-    accurate_budget_kernel<unsigned long long><<<static_cast<unsigned>((lines + 255) / 256), 256, 0, s>>>(
-        base, cmax, lines, c.pp_accu, c.precision, exp_out);
+void launch_accurate_budget64(const int32_t* base, const unsigned long long* cmax, int64_t lines, int32_t* exp_out,
+                              const int32_t* base2, const unsigned long long* cmax2, int64_t lines2,
+                              int32_t* exp_out2, const DevConsts& c, cudaStream_t s) {
+    accurate_budget_kernel<unsigned long long><<<static_cast<unsigned>((lines + lines2 + 255) / 256), 256, 0, s>>>(
+        base, cmax, lines, c.pp_accu, c.precision, exp_out, base2, cmax2, lines2, exp_out2);
 }
 
 }  // namespace ozk

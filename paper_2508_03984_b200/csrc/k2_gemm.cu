@@ -553,6 +553,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         tmem_dealloc<CG>(tmem_base, 2 * kAccCols);
     }
+    // the last cluster out resets the lockstep words for the next launch (no
+    // per-launch memset; every other cluster is past all of its waits)
+    if (P.sync_mode > 0 && leader && threadIdx.x == 0) {
+        unsigned int* finished = P.done + 8;
+        __threadfence();
+        if (atomicAdd(finished, 1u) == static_cast<unsigned int>(nclusters - 1)) {
+            *P.done = 0;
+            if (P.sync_mode == 2)
+                for (int cl = 0; cl < nclusters; ++cl) P.progress[cl] = 0;
+            *finished = 0;
+            __threadfence();
+        }
+    }
 }
 
 // ------------------------------------------------------------- host helpers
@@ -636,7 +649,8 @@ int launch_impl(const K2Launch& L, cudaStream_t s) {
     if (P.sync_every < 1) P.sync_every = 1;
     P.done = L.sync_counter;
     P.progress = L.sync_counter ? L.sync_counter + 16 : nullptr;
-    if (P.sync_mode > 0) cudaMemsetAsync(P.done, 0, sizeof(unsigned int) * 16 * 16, s);
+    // the lockstep words start at zero (the handle clears its flag buffer once)
+    // and each launch's last cluster resets them
     const long long total = static_cast<long long>(L.n_mod) * P.tiles_m * P.tiles_n;
     long long clusters = L.num_sms / CG;
     if (clusters > total) clusters = total;

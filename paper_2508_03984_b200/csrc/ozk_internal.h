@@ -68,11 +68,14 @@ void launch_row_stats(const void* a, int is_f32, int64_t m, int64_t k, int64_t l
                       double* psum, int32_t* nonfinite, int32_t* counters, const LineFinal& fin, cudaStream_t s);
 void launch_col_stats(const void* b, int is_f32, int64_t k, int64_t n, int64_t ldb, double* pmax, double* psum,
                       int32_t* nonfinite, const LineFinal& fin, cudaStream_t s);
-void launch_accurate_budget(const int32_t* base, const int32_t* cmax, int64_t lines, const DevConsts& c,
-                            int32_t* exp_out, cudaStream_t s);
-// k > 2^19: the bound product accumulates in int64 (K2_ACC64), maxima in uint64
-void launch_accurate_budget64(const int32_t* base, const unsigned long long* cmax, int64_t lines, const DevConsts& c,
-                              int32_t* exp_out, cudaStream_t s);
+// accurate-mode budgets from the bound-GEMM maxima (scaling.cpp:151-165), rows
+// and columns in one launch; k > 2^19: int64 bound product, uint64 maxima
+void launch_accurate_budget(const int32_t* base, const int32_t* cmax, int64_t lines, int32_t* exp_out,
+                            const int32_t* base2, const int32_t* cmax2, int64_t lines2, int32_t* exp_out2,
+                            const DevConsts& c, cudaStream_t s);
+void launch_accurate_budget64(const int32_t* base, const unsigned long long* cmax, int64_t lines, int32_t* exp_out,
+                              const int32_t* base2, const unsigned long long* cmax2, int64_t lines2,
+                              int32_t* exp_out2, const DevConsts& c, cudaStream_t s);
 void launch_bound_max64(const long long* cbar, int64_t m, int64_t n, int64_t ld, unsigned long long* rowmax,
                         unsigned long long* colmax, cudaStream_t s);
 
