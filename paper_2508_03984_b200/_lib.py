@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "lib", "libozaki2_b200.so")
+# OZK_LIB_PATH: another build of the same library (A/B timing of two commits)
+LIB_PATH = os.environ.get("OZK_LIB_PATH") or os.path.join(PKG_DIR, "lib", "libozaki2_b200.so")
 
 OZK_OK, OZK_CONFIG_ERROR, OZK_INPUT_ERROR, OZK_CUDA_ERROR, OZK_DOMAIN_ERROR, OZK_INTERNAL_ERROR = range(6)
 OZK_FP64, OZK_FP32 = 0, 1
