@@ -88,13 +88,13 @@ struct Job {
     const void* b;
     int64_t lda, ldb;
     int in_f32;
-    int32_t *mu, *nu, *ma, *nb, *rowmax, *colmax, *flag_rows, *flag_cols;
+    int32_t *mu, *nu, *ma, *nb, *rowmax, *colmax;
     // accurate mode with k > 2^19: the bound product Abar*Bbar exceeds int32, so it
     // accumulates in int64 (per column block) and its maxima are uint64
     bool wide_bound;
     unsigned long long *rowmax64, *colmax64;
     bool async = false;  // OZK_FLAG_ASYNC: no host sync, deferred non-finite check
-    int32_t* flags;  // [0] non-finite, [1] flagged rows, [2] flagged columns, [4..] K2 lockstep words (1 KB)
+    int32_t* flags;  // [0] non-finite input, [4..] K2 lockstep words (1 KB)
     double *amax, *asum, *bmax, *bsum;
     int splits, splits_b;  // k-partials of the row-stat reductions of op(A) (!ta) / op(B) (tb)
     int32_t *cnt_a, *cnt_b;  // last-block counters of the row-stat reductions (A side / B side)
@@ -296,8 +296,6 @@ int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c,
     J.nb = J.ma + m;
     J.rowmax = J.nb + n;
     J.colmax = J.rowmax + m;
-    J.flag_rows = J.colmax + n;
-    J.flag_cols = J.flag_rows + m;
     J.wide_bound = cfg->mode == OZK_ACCURATE && k > kBoundInt32K;
     if (J.wide_bound) {
         OZK_TRY(ensure(h->wide, sizeof(unsigned long long) * (m + n)));
@@ -312,13 +310,10 @@ int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c,
     J.lda = lda;
     J.ldb = ldb;
     J.in_f32 = cfg->a_type == OZK_R32F;
-    // flag word 0 (non-finite input) stays sticky across stream-ordered calls
-    // until ozk_sync collects it
+    // flag word 0 (non-finite input): cleared per synchronous call; sticky
+    // across stream-ordered calls until ozk_sync collects it
     J.async = (cfg->flags & OZK_FLAG_ASYNC) != 0;
-    if (J.async)
-        OZK_CUDA(cudaMemsetAsync(J.flags + 1, 0, 12, h->stream));
-    else
-        OZK_CUDA(cudaMemsetAsync(J.flags, 0, 16, h->stream));
+    if (!J.async) OZK_CUDA(cudaMemsetAsync(J.flags, 0, sizeof(int32_t), h->stream));
     return OZK_OK;
 }
 
@@ -838,7 +833,6 @@ int gemm_host_streamed(ozk_context* h, Job& J, double alpha, const void* A, int6
             OZK_CUDA(cudaStreamWaitEvent(h->stream, ev_b(s), 0));
             {
                 StageTimer t(h, OZK_PROFILE_SCALE);
-                OZK_CUDA(cudaMemsetAsync(J.flags + 2, 0, sizeof(int32_t), h->stream));
                 OZK_TRY(stage_cols(h, J, c0, nc));
             }
             {
