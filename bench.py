@@ -118,12 +118,12 @@ def run_reference_arm(args):
     sample = f"C block {s}x{s} of the {args.n}^3 problem (full k={k}), oracle/_ref gemm_emulated, threads={threads}"
     print(json.dumps({
         "impl": "reference",
-        "metric": f"emulated DGEMM TFLOPS (2mnk/s), N={args.moduli} {args.mode}",
+        "metric": f"emulated DGEMM TFLOPS (2mnk/s) at n={args.n}, {args.moduli} moduli, {args.mode} mode",
         "value": v, "unit": "TFLOPS", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (rand-0.5)*exp(phi*randn), phi=%g" % args.phi,
-        "config": {"workload": f"DGEMM m=n=k={args.n}, {args.moduli} moduli, {args.mode} mode",
-                   "sample": sample},
+        "config": {"workload": f"DGEMM m=n=k={args.n} per GPU (column block of B/C), {args.moduli} moduli, "
+                               f"{args.mode}", "sample": sample},
         "cpu_baseline": {"value": v, "unit": "TFLOPS", "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": v, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
