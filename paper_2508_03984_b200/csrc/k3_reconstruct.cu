@@ -83,7 +83,11 @@ __host__ __device__ constexpr int bulk_stages() {
 // sum is exact (beta_i construction, crt_tables.cpp:165-169), so one DFMA.
 // (An exact int64 sum on the IMAD pipe measured 15 % slower: IMAD.WIDE is
 // the expensive op there.)
-constexpr int kC1TwoOp = 0, kC1Dfma = 1;
+// FP32 tables also have s2 = 0 and P2 = 0 (crt_tables.cpp:160-163, :135): C2
+// is +0 throughout and C'' = fma(-P1, Q, C1) exactly (C1 >= 0, so that is never
+// -0 and the reference's "+ C2" and "fma(-P2, Q, .)" leave it unchanged), so
+// kC1TwoOpNoC2 drops the C2 chain: 3 instead of 5 FP64 ops per element-modulus.
+constexpr int kC1TwoOp = 0, kC1Dfma = 1, kC1TwoOpNoC2 = 2;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -242,14 +246,16 @@ __global__ void __launch_bounds__(kConsumers + 32, (kMaxMod <= 8 ? 384 : 512) / 
                     } else {
                         c1[q] = __dadd_rn(c1[q], __dmul_rn(c.s1[t], __dsub_rn(V, 0x1.0p52)));
                     }
-                    c2[q] = __dadd_rn(c2[q], __fma_rn(c.s2[t], V, c.s2_m52[t]));
+                    if constexpr (kC1 != kC1TwoOpNoC2) c2[q] = __dadd_rn(c2[q], __fma_rn(c.s2[t], V, c.s2_m52[t]));
                 }
             }
             double r[R];
 #pragma unroll
             for (int q = 0; q < R; ++q) {
                 const double qv = rint(__dmul_rn(c.P_inv, c1[q]));
-                const double cpp = __fma_rn(-c.P2, qv, __dadd_rn(__fma_rn(-c.P1, qv, c1[q]), c2[q]));
+                const double cpp = kC1 == kC1TwoOpNoC2
+                                       ? __fma_rn(-c.P1, qv, c1[q])
+                                       : __fma_rn(-c.P2, qv, __dadd_rn(__fma_rn(-c.P1, qv, c1[q]), c2[q]));
                 r[q] = unscale_fast(cpp, -(me[q] + ne));
             }
             if (!kPlain) {
@@ -366,9 +372,16 @@ void launch_variant(const uint8_t* u, int64_t ldu, int64_t stride, int64_t m, in
     if (c.precision == OZK_FP64)
         launch_bulk<kF32Out, kPlain, kC1Dfma>(sms, s, u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, C, ldc,
                                               vec_ok);
-    else
-        launch_bulk<kF32Out, kPlain, kC1TwoOp>(sms, s, u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, C, ldc,
-                                               vec_ok);
+    else {
+        bool no_c2 = c.P2 == 0.0;
+        for (int t = 0; t < c.n; ++t) no_c2 = no_c2 && c.s2[t] == 0.0;
+        if (no_c2)
+            launch_bulk<kF32Out, kPlain, kC1TwoOpNoC2>(sms, s, u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta,
+                                                       C, ldc, vec_ok);
+        else
+            launch_bulk<kF32Out, kPlain, kC1TwoOp>(sms, s, u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, C,
+                                                   ldc, vec_ok);
+    }
 }
 
 }  // namespace

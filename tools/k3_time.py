@@ -7,7 +7,7 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2508_03984_b200 import Context, EmuConfig  # noqa: E402
+from paper_2508_03984_b200 import Context, EmuConfig, Precision  # noqa: E402
 
 
 def main():
@@ -21,8 +21,9 @@ def main():
         ldu = (n + 15) // 16 * 16
         U = torch.randint(0, 173, (N, n, ldu), dtype=torch.uint8, device="cuda")
         mu = torch.zeros(n, dtype=torch.int32, device="cuda")
-        C = torch.empty((n, n), dtype=torch.float64, device="cuda").t()
-        cfg = EmuConfig(n_moduli=N)
+        prec = int(os.environ.get("K3_PREC", "0"))  # 1: FP32 tables (SGEMM), FP32 C
+        C = torch.empty((n, n), dtype=torch.float32 if prec else torch.float64, device="cuda").t()
+        cfg = EmuConfig(n_moduli=N, precision=Precision(prec))
         ctx.stage_reconstruct(cfg, n, n, U, ldu, mu, mu, C)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -33,7 +34,7 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
         out[f"N{N}_ms"] = round(ms, 3)
-        out[f"N{N}_TBs"] = round((N + 8) * n * n / ms / 1e9, 2)
+        out[f"N{N}_TBs"] = round((N + (4 if prec else 8)) * n * n / ms / 1e9, 2)
         del U
     print(json.dumps(out))
 
