@@ -63,7 +63,10 @@ DevConsts to_dev(const ozk_constants& c) {
     d.P_inv = c.P_inv;
     d.pp_fast = c.pp_fast;
     d.pp_accu = c.pp_accu;
-    for (int i = 0; i < c.n_moduli; ++i) d.s2_m52[i] = -c.s2[i] * 0x1p52;
+    for (int i = 0; i < c.n_moduli; ++i) {
+        d.s2_m52[i] = -c.s2[i] * 0x1p52;
+        d.s1_m52[i] = -c.s1[i] * 0x1p52;
+    }
     return d;
 }
 

@@ -243,8 +243,8 @@ __global__ void __launch_bounds__(kConsumers + 32, (kMaxMod <= 8 ? 384 : 512) / 
                     const double V = __hiloint2double(0x43300000, static_cast<int>(ub));  // 2^52 + u
                     if constexpr (kC1 == kC1Dfma) {  // exact products and sums: one DFMA
                         c1[q] = __fma_rn(c.s1[t], __dsub_rn(V, 0x1.0p52), c1[q]);
-                    } else {
-                        c1[q] = __dadd_rn(c1[q], __dmul_rn(c.s1[t], __dsub_rn(V, 0x1.0p52)));
+                    } else {  // FP32 tables: fl(s1 u) from the pair, then the rounded sum
+                        c1[q] = __dadd_rn(c1[q], __fma_rn(c.s1[t], V, c.s1_m52[t]));
                     }
                     if constexpr (kC1 != kC1TwoOpNoC2) c2[q] = __dadd_rn(c2[q], __fma_rn(c.s2[t], V, c.s2_m52[t]));
                 }

@@ -28,6 +28,7 @@ struct DevConsts {
     double P1, P2, P_inv;
     float pp_fast, pp_accu;
     double s2_m52[OZK_MAX_MODULI];
+    double s1_m52[OZK_MAX_MODULI];  // -s1_i * 2^52: fl(s1*u) = fma(s1, 2^52 + u, -s1 * 2^52) (FP32 tables)
     int fast_fix;  // OZK_FLAG_FAST_EXPONENT_FIX  // -s2_i * 2^52 (for fl(s2*u) = fma(s2, 2^52 + u, -s2 * 2^52))
 };
 
