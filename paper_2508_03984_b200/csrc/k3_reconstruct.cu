@@ -104,6 +104,24 @@ __device__ __forceinline__ void bulk_mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// producer-side wait: a lane polling a ring slot with try_wait in a tight loop
+// issued ~40 instructions per element of K3 (a quarter of the SM's issue
+// slots, taken from the consumer warps); it has a full stage of slack, so it
+// backs off with nanosleep between polls
+__device__ __forceinline__ void bulk_mbar_wait_backoff(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    for (;;) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (done) return;
+        __nanosleep(256);
+    }
+}
 __device__ __forceinline__ void bulk_mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -188,7 +206,7 @@ __global__ void __launch_bounds__(kConsumers + 32, (kMaxMod <= 8 ? 384 : 512) / 
         for (int64_t k = 0, tile = blockIdx.x; tile < tiles; ++k, tile += gridDim.x, advance()) {
             const int s = static_cast<int>(k % kStages);
             const uint32_t ph = static_cast<uint32_t>((k / kStages) & 1);
-            bulk_mbar_wait(smem_addr(&empty[s]), ph ^ 1u);
+            bulk_mbar_wait_backoff(smem_addr(&empty[s]), ph ^ 1u);
             const int64_t i0 = chunk * kTile;
             const int64_t rows = m - i0 < kTile ? m - i0 : kTile;
             const uint32_t bytes = static_cast<uint32_t>((rows + 15) & ~int64_t(15));
@@ -391,9 +409,15 @@ void launch_reconstruct_regs(const uint8_t* u, int64_t ldu, int64_t stride, int6
                              const int32_t* mu_exp, const int32_t* nu_exp, const DevConsts& c, double alpha,
                              double beta, void* C, int64_t ldc, int c_is_f32, cudaStream_t s);
 
+// k3_tc.cu: C1 on the tensor cores (FP64 tables); false = not applicable
+bool launch_reconstruct_tc(const uint8_t* u, int64_t ldu, int64_t stride, int64_t m, int64_t n, const int32_t* mu_exp,
+                           const int32_t* nu_exp, const DevConsts& c, double alpha, double beta, void* C, int64_t ldc,
+                           int c_is_f32, cudaStream_t s);
+
 void launch_reconstruct(const uint8_t* u, int64_t ldu, int64_t stride, int64_t m, int64_t n, const int32_t* mu_exp,
                         const int32_t* nu_exp, const DevConsts& c, double alpha, double beta, void* C, int64_t ldc,
                         int c_is_f32, cudaStream_t s) {
+    if (launch_reconstruct_tc(u, ldu, stride, m, n, mu_exp, nu_exp, c, alpha, beta, C, ldc, c_is_f32, s)) return;
     // bulk copies need 16-byte aligned slices, i.e. the [N][n][ldu] layout with
     // 16-byte ldu and plane stride (a partial chunk's over-read stays inside the
     // column's ldu padding); other layouts (stage API callers) take the
