@@ -66,6 +66,7 @@ struct K2Params {
     int p[OZK_MAX_MODULI];
     int pinv[OZK_MAX_MODULI];
     int group;             // tile rows per raster group
+    int snake;             // odd groups sweep the columns right to left (B panels reused across the group edge)
     int hints;             // bit 0: A loads evict_last, bit 1: B loads evict_last, bit 3: B loads
                            // evict_first (bit 2, streaming U stores, measured no gain: removed)
     int sync_mode;         // 0 off; 1 tile lockstep (slack 1); 2 k-block lockstep
@@ -259,7 +260,8 @@ __host__ __device__ constexpr uint32_t idesc_i8() {
 
 // work item t -> (modulus, tile row, tile column), grouped raster of 8 tile
 // rows per modulus so the co-resident tiles share A/B panels in L2
-__device__ __forceinline__ void decode_tile(int t, int tiles_m, int tiles_n, int G, int& mod, int& tm, int& tn) {
+__device__ __forceinline__ void decode_tile(int t, int tiles_m, int tiles_n, int G, int snake, int& mod, int& tm,
+                                            int& tn) {
     const int per_mod = tiles_m * tiles_n;
     mod = t / per_mod;
     const int r = t - mod * per_mod;
@@ -269,6 +271,7 @@ __device__ __forceinline__ void decode_tile(int t, int tiles_m, int tiles_n, int
     const int w = r - group * G * tiles_n;
     tm = first + w % gsize;
     tn = w / gsize;
+    if (snake && (group & 1)) tn = tiles_n - 1 - tn;
 }
 
 // max over the 32 lanes of column `lane` of a 32 x 32 register tile
@@ -358,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             __syncwarp();
             int mod, tm, tn;
-            decode_tile(t, P.tiles_m, P.tiles_n, P.group, mod, tm, tn);
+            decode_tile(t, P.tiles_m, P.tiles_n, P.group, P.snake, mod, tm, tn);
             const int m0 = tm * C::kTileM + static_cast<int>(rank) * C::kBM;
             const int n0 = tn * C::kTileN + static_cast<int>(rank) * C::kBRows;
             for (int kb = 0; kb < P.num_kb; ++kb) {
@@ -464,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int acc = lt & 1;
             const uint32_t acc_phase = (lt >> 1) & 1;
             int mod, tm, tn;
-            decode_tile(t, P.tiles_m, P.tiles_n, P.group, mod, tm, tn);
+            decode_tile(t, P.tiles_m, P.tiles_n, P.group, P.snake, mod, tm, tn);
             mbar_wait(smem_u32(tfull + acc), acc_phase);
             tc_fence_after();
             const int row = tm * C::kTileM + static_cast<int>(rank) * C::kBM + q * 32 + lane;
@@ -637,6 +640,7 @@ int launch_impl(const K2Launch& L, cudaStream_t s) {
         P.pinv[i] = L.c->pinv_mulhi[i];
     }
     P.group = env_int("OZK_K2_GROUP", 8);
+    P.snake = env_int("OZK_K2_SNAKE", 0);
     P.hints = env_int("OZK_K2_HINTS", 9);  // A evict_last, B evict_first (profiles/r01_k2_hints_sweep.md)
     // Lockstep (default on): co-resident clusters that share A/B panels stay
     // within one tile of each other, so the panels they all stream are still in
