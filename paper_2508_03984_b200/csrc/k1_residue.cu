@@ -89,6 +89,10 @@ __global__ void __launch_bounds__(128)
         xlo[u] = static_cast<uint32_t>(__double2loint(__dadd_rn(static_cast<double>(x[u]), kMagic52)));
     // the fast/literal choice is warp-uniform: branch once, outside the modulus loop
     if (fast) {
+        // modulus-independent half of the packed residue words (see below)
+        uint32_t xb[2] = {0u, 0u};
+#pragma unroll
+        for (int u = 0; u < kBPerThread; ++u) xb[u >> 2] += (xlo[u] + 128u) << (8 * (u & 3));
         int8_t* dst = dst0;
 #pragma unroll
         for (int t = 0; t < kMaxMod; ++t) {
@@ -99,12 +103,18 @@ __global__ void __launch_bounds__(128)
                     word = make_uint2(pack_low_bytes(xlo[0], xlo[1], xlo[2], xlo[3]),
                                       pack_low_bytes(xlo[4], xlo[5], xlo[6], xlo[7]));
                 } else {
-                    const uint32_t neg_p = 0u - pt;
-                    uint32_t v[kBPerThread];
+                    // four residues r_u in one word without byte shuffles:
+                    // xlo_u + qlo_u (-p) = r_u (mod 2^32) with |r_u| <= 127, so
+                    // sum_u (xlo_u + 128 + qlo_u (-p)) 2^(8u) = sum_u (r_u + 128) 2^(8u)
+                    // exactly (no carries), and XOR 0x80 per byte leaves r_u mod 256
+                    uint32_t w[2] = {xb[0], xb[1]};
 #pragma unroll
-                    for (int u = 0; u < kBPerThread; ++u)
-                        v[u] = symmetric_residue(static_cast<double>(x[u]), xlo[u], neg_p, c.pinv64[t]);
-                    word = make_uint2(pack_low_bytes(v[0], v[1], v[2], v[3]), pack_low_bytes(v[4], v[5], v[6], v[7]));
+                    for (int u = 0; u < kBPerThread; ++u) {
+                        const uint32_t qlo = static_cast<uint32_t>(
+                            __double2loint(__fma_rn(static_cast<double>(x[u]), c.pinv64[t], kMagic52)));
+                        w[u >> 2] += qlo * c.negp_sh[u & 3][t];
+                    }
+                    word = make_uint2(w[0] ^ 0x80808080u, w[1] ^ 0x80808080u);
                 }
                 *reinterpret_cast<uint2*>(dst) = word;
                 dst += plane_stride;
