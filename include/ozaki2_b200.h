@@ -265,6 +265,14 @@ int64_t ozk_kernel_launches(ozk_handle h);
 int ozk_profile(ozk_handle h, int enable);
 int ozk_profile_read(ozk_handle h, double* ms, int64_t* calls, int reset);
 
+/* K3 diagnostics (extension; no reference counterpart). The tensor-core K3
+ * (FP64 tables) takes C2 from an exact integer dot product and replays the
+ * reference's sequential C2 (emulator.cpp:53) only for elements whose final
+ * rounding the C2 interval cannot decide. ozk_k3_replays enables counting on
+ * the first call (it synchronises the device) and returns the replayed
+ * elements counted since then, optionally resetting the count. */
+int ozk_k3_replays(unsigned long long* count, int reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -32,7 +32,7 @@ EXPORTED_SYMBOLS = (
     "ozk_select_moduli", "ozk_mod_inverse", "ozk_build_constants", "ozk_dump_tables_csv",
     "ozk_gemm", "ozk_gemm_host", "ozk_dgemm", "ozk_sgemm", "ozk_dgemm_ex", "ozk_gemm_strided_batched",
     "ozk_stage_scale", "ozk_plane_ld", "ozk_stage_residues", "ozk_stage_products", "ozk_stage_reconstruct",
-    "ozk_kernel_launches", "ozk_profile", "ozk_profile_read", "ozk_sync",
+    "ozk_kernel_launches", "ozk_profile", "ozk_profile_read", "ozk_k3_replays", "ozk_sync",
     "ozk_shard_begin", "ozk_shard_rowmax", "ozk_shard_end",
     "ozk_shard_stream_begin", "ozk_shard_stream_rows", "ozk_shard_stream_end",
     "ozk_int8_gemm", "ozk_truncate_scale", "ozk_residues", "ozk_mod_u8_array", "ozk_accumulate", "ozk_crt_reduce",
@@ -149,6 +149,7 @@ def load() -> C.CDLL:
     L.ozk_crt_reduce.argtypes = [p, C.POINTER(OzkConfig), i64, p, p, p]
     L.ozk_unscale.argtypes = [p, i64, i64, p, i64, p, p, p, i64]
     L.ozk_profile_read.argtypes = [p, p, p, i32]
+    L.ozk_k3_replays.argtypes = [p, i32]
     _lib = L
     return L
 

@@ -46,6 +46,8 @@ struct Buf {
 
 void set_error(const std::string& msg) { g_error = msg; }
 
+unsigned long long* k3_replay_counter(bool create);  // k3_tc.cu
+
 DevConsts to_dev(const ozk_constants& c) {
     DevConsts d{};
     d.n = c.n_moduli;
@@ -1090,6 +1092,17 @@ int ozk_profile_read(ozk_handle h, double* ms, int64_t* calls, int reset) {
             h->stage_calls[i] = 0;
         }
     }
+    return OZK_OK;
+}
+
+int ozk_k3_replays(unsigned long long* count, int reset) {
+    unsigned long long* d = k3_replay_counter(true);
+    if (!d) return cuda_fail("k3 replay counter", cudaErrorMemoryAllocation);
+    OZK_CUDA(cudaDeviceSynchronize());
+    unsigned long long v = 0;
+    OZK_CUDA(cudaMemcpy(&v, d, sizeof(v), cudaMemcpyDeviceToHost));
+    if (count) *count = v;
+    if (reset) OZK_CUDA(cudaMemset(d, 0, sizeof(v)));
     return OZK_OK;
 }
 

@@ -1,29 +1,35 @@
-// K3 with the C1 sum on the tensor cores (FP64 tables; reference:
-// emulator.cpp:49-53 weighted sums, reconstruct.hpp:51-54, reconstruct.cpp:49-69).
+// K3 on the tensor cores with a verified C2 (FP64 tables; reference:
+// emulator.cpp:49-53 weighted sums, reconstruct.hpp:51-54 crt_reduce_element,
+// reconstruct.cpp:49-69 unscale).
 //
-// With FP64 tables every s1_i is an integer multiple S_i of one power of two
-// 2^E (the head of W_i on the common grid, crt_tables.cpp:165-169), S_i < 2^48,
-// and sum_i S_i (p_i - 1) < 2^53: each product s1_i u and each partial sum of
-// the reference's c1 += s1_i * u is exact, so c1 = 2^E * sum_i S_i u_i for any
-// evaluation order. That integer dot product over the moduli is an int8 GEMM:
-//   [128 rows x 32 moduli] (U tile, u8, MN-major) x [32 moduli x 16] (the
-//   base-256 digits of S_i, u8, K-major) -> [128 x 16] s32 in TMEM,
-// one tcgen05.mma.kind::i8 (M = 128, N = 16, K = 32) per 128-row group, column
-// b holding sum_i D_ib u_i < 2^21 for digit b. The epilogue forms
-//   c1 = fma(Z, 2^(E+32), fma(Y, 2^(E+16), X 2^E)),
-//   X = P0 + 256 P1, Y = P2 + 256 P3, Z = P4 + 256 P5,
-// exact (every partial sum is a multiple of 2^E below 2^53 * 2^E). This takes
-// the C1 chain (DADD + DFMA per element and modulus) off the FP64 pipe; the C2
-// chain keeps the reference's roundings (fl(s2 u) = fma(s2, 2^52 + u, -s2 2^52),
-// then the rounded add), so K3 does 2 instead of 4 FP64 ops per element-modulus.
+// The reference forms, per output element, c1 = sum_i s1_i u_i and
+// c2 = sum_i fl(s2_i u_i) (ascending i, every product and add rounded), then
+// C'' = fma(-P2, Q, fl(fma(-P1, Q, c1) + c2)), Q = rint(P_inv c1).
+// * c1 is exact: every s1_i is S1_i 2^E1 with sum_i S1_i (p_i - 1) < 2^52
+//   (checked per call), so c1 = 2^E1 sum_i S1_i u_i, an integer dot product.
+// * c2 carries roundings, but only its value near a rounding boundary of the
+//   final result matters. s2_i = S2_i 2^E2 with S2_i < 2^64, so the exact sum
+//   S = sum_i s2_i u_i is an integer dot product too, and the reference's
+//   recursive sum of N rounded products satisfies |c2 - S| <= gamma_(N+1) S
+//   (all terms are >= 0). With c2~ = fl(S) the interval
+//   [c2~ - r, c2~ + r], r = (N + 3) 2^-53 c2~ (directed roundings) holds c2.
+//   fl(X + y) and fma(-P2, Q, .) are monotone in y, so when both interval ends
+//   give the same C'' bit pattern that IS the reference's C''. Otherwise (rare:
+//   the interval is ~2^-48 c2 wide and c2 is ~2^-25 of X) the thread replays
+//   the reference's sequential c2 from the planes still in shared memory.
+// Both dot products are one tcgen05.mma.kind::i8 per 128-row group:
+//   [128 rows x 32 moduli] (the U tile, u8, MN-major SW128, landed by one
+//   TMA box {128 rows, P planes}) x [32 moduli x 16] (u8 digits, K-major:
+//   columns 0-5 the base-256 digits of S1_i, 6-13 those of S2_i) -> s32 TMEM,
+// each digit column sum_i D_ib u_i < 2^21. So the per-element FP64 chain of
+// the all-FP64 kernel (4 FP64 ops per element and modulus) becomes a fixed
+// ~15 FP64 ops per element, and K3 streams at the HBM rate.
 //
-// Data movement: one TMA (cp.async.bulk.tensor, 128B swizzle) per 128-row
-// group lands [P planes][128 rows] (P = 16 or 24; planes >= N zero-filled by
-// TMA) — exactly the canonical MN-major SW128 operand of the MMA — into a
-// two-slot ring. The C2 chain reads the same bytes (8 consecutive rows per
-// thread, one 8-byte LDS per plane at the swizzled address); TMEM rows belong
-// to warp (row / 32) % 4, so the exact c1 values cross to the row owners
-// through a (bank-swizzled) shared buffer and one 128-thread named barrier.
+// Warp roles: warp 4 lane 0 issues the TMA boxes into an S-slot ring, lane 1
+// the MMAs into a double-buffered TMEM accumulator (2 x 64
+// columns: 4 groups x 16); warps 0-3 drain TMEM lanes 32w..32w+31 — the row
+// 128 g + 32 w + lane of each group g — so every output row is finished by the
+// thread that holds its digit sums (no exchange), and stores are coalesced.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -37,11 +43,17 @@ namespace ozk {
 namespace {
 
 constexpr int kConsumers = 128;
-constexpr int kThreads = kConsumers + 32;  // + one producer warp
+constexpr int kThreads = kConsumers + 32;  // + one control warp (lane 0 TMA, lane 1 MMA)
+constexpr int kGroups = 4;                 // 128-row MMA groups per tile
+constexpr int kRows = 128 * kGroups;       // rows per tile (one column)
+constexpr int kTmemCols = 2 * 16 * kGroups;  // two accumulator buffers
 
 struct TcParams {
-    unsigned long long s_int[OZK_MAX_MODULI];  // S_i = s1_i / 2^E
-    double sc0, sc0m52;                        // 2^E, -2^(52+E)
+    unsigned long long s1_int[OZK_MAX_MODULI];  // S1_i = s1_i / 2^E1
+    unsigned long long s2_int[OZK_MAX_MODULI];  // S2_i = s2_i / 2^E2
+    double sc1, sc1m;                           // 2^E1, -2^(52+E1)
+    double sc2h, sc2hm, sc2l, sc2lm;            // 2^(32+E2), -2^(84+E2), 2^E2, -2^(52+E2)
+    double rfac;                                // (N + 3) 2^-53
 };
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -96,7 +108,6 @@ __device__ __forceinline__ uint64_t evict_first() {
 }
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
 
 // 128B-swizzled shared-memory descriptor (sm_100 version 1), SBO = 1024 B
 // (8 rows of 128 B); LBO = 16 B (K-major: unused within one atom column;
@@ -118,27 +129,16 @@ __device__ __forceinline__ void mma_u8(uint32_t d, uint64_t a, uint64_t b) {
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-                 : "r"(taddr));
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, "
+        "[%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-__device__ __forceinline__ void ld_nc_v8(const int32_t* p, int* v) {
-    asm volatile("ld.global.nc.v8.s32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-                 : "l"(p));
-}
-__device__ __forceinline__ void st_v4_f64(double* p, const double* v) {
-    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
-                 : "memory");
-}
-__device__ __forceinline__ void st_v8_f32(float* p, const float* v) {
-    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]), "f"(v[1]),
-                 "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
-                 : "memory");
-}
 
 __device__ __forceinline__ double scale_pow2(double x, int e) {
     if (e >= -1022 && e <= 1023) {
@@ -157,80 +157,64 @@ __device__ __forceinline__ double unscale_fast(double x, int e) {
     return scale_pow2(x, e);
 }
 
-template <int R>
-struct RowWord;
-template <>
-struct RowWord<4> {
-    static __device__ __forceinline__ uint2 lds(uint32_t a) {
-        uint2 w;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w.x) : "r"(a));
-        w.y = 0;
-        return w;
-    }
-};
-template <>
-struct RowWord<8> {
-    static __device__ __forceinline__ uint2 lds(uint32_t a) {
-        uint2 w;
-        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w.x), "=r"(w.y) : "r"(a));
-        return w;
-    }
-};
-
-// Tile = 128 R rows of one column (R MMA groups of 128 rows); each consumer
-// thread owns R consecutive rows for the C2 chain and the output.
-template <int R, int S, int P>
+template <int P, int S>
 struct TcCfg {
-    static constexpr int kRows = 128 * R;
     static constexpr int kGroupBytes = P * 128;
-    static constexpr int kStageBytes = R * kGroupBytes;
-    static constexpr int kTmemCols = 16 * R < 32 ? 32 : 16 * R;
-    // [S][R groups][P planes][128 B] | B digits [16][128 B]. The K = 32 MMA
+    static constexpr int kStageBytes = kGroups * kGroupBytes;
+    // [S][4 groups][P planes][128 B] | B digits [16][128 B]. The K = 32 MMA
     // of a stage's last group reads (32 - P) planes past the stage: the next
-    // stage or the digit block, inside the allocation (those bytes meet zero
-    // digit rows). The c1 exchange reuses the consumed stage (kRows doubles).
+    // stage or the digit block (those bytes meet zero digit rows).
     static constexpr int kSmem = 1024 /*align*/ + S * kStageBytes + 2048;
     static_assert((32 - P) * 128 <= 2048, "MMA over-read leaves the allocation");
-    static_assert(kRows * 8 <= kStageBytes, "exchange does not fit the stage");
 };
 
-template <bool kF32Out, bool kPlain, int kMaxMod, int P, int R, int S>
-__global__ void __launch_bounds__(kThreads, R == 4 ? 5 : 4)
+// (2^52 + T) with T < 2^52 given as a 64-bit integer, as a double
+__device__ __forceinline__ double pair52(uint64_t T) {
+    return __hiloint2double(static_cast<int>(static_cast<uint32_t>(T >> 32) | 0x43300000u),
+                            static_cast<int>(static_cast<uint32_t>(T)));
+}
+
+template <bool kF32Out, bool kPlain, bool kExact, int P, int S, int kTmemBatch = 2>
+__global__ void __launch_bounds__(kThreads, 4)
     reconstruct_tc_kernel(const __grid_constant__ CUtensorMap umap, int64_t m, int64_t n, int64_t row_chunks,
                           const int32_t* __restrict__ mu_exp, const int32_t* __restrict__ nu_exp, const DevConsts c,
                           const TcParams tp, double alpha, double beta, void* __restrict__ C, int64_t ldc,
-                          bool vec_ok, int probe) {
-    using Cf = TcCfg<R, S, P>;
-    constexpr int kRows = Cf::kRows, kGroupBytes = Cf::kGroupBytes, kStageBytes = Cf::kStageBytes;
+                          unsigned long long* __restrict__ replays) {
+    using Cf = TcCfg<P, S>;
+    constexpr int kGroupBytes = Cf::kGroupBytes, kStageBytes = Cf::kStageBytes;
     extern __shared__ uint8_t smem_raw[];
-    __shared__ __align__(8) uint64_t full[S], empty[S], mma_bar;
+    __shared__ __align__(8) uint64_t full[S], empty[S], mma_full[2], tmem_empty[2];
     __shared__ uint32_t tmem_slot;
     uint8_t* sbuf = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* bdig = sbuf + S * kStageBytes;
 
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int n_mod = c.n;
     if (tid == 0) {
         for (int st = 0; st < S; ++st) {
             mbar_init(saddr(&full[st]), 1);
             mbar_init(saddr(&empty[st]), kConsumers / 32);
         }
-        mbar_init(saddr(&mma_bar), 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(saddr(&mma_full[b]), 1);
+            mbar_init(saddr(&tmem_empty[b]), kConsumers / 32);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // B operand: row b (digit), K-major 128 B rows, byte k = digit b of S_k,
-    // 16-byte chunk k / 16 XOR-swizzled by b % 8 (the TMA SW128 pattern);
-    // rows 6..15 and moduli >= N are zero
+    // B operand: digit row b (K-major, 128 B rows, 16-byte chunk k / 16
+    // XOR-swizzled by b % 8 as TMA SW128 would): rows 0-5 the digits of S1_k,
+    // rows 6-13 those of S2_k, rows 14-15 and moduli >= N zero
     for (int i = tid; i < 16 * 32; i += kThreads) {
         const int b = i >> 5, k = i & 31;
-        const uint32_t v =
-            (b < 6 && k < n_mod) ? static_cast<uint32_t>((tp.s_int[k] >> (8 * b)) & 0xFFu) : 0u;
+        uint32_t v = 0;
+        if (k < n_mod && b < 6) v = static_cast<uint32_t>((tp.s1_int[k] >> (8 * b)) & 0xFFu);
+        if (k < n_mod && b >= 6 && b < 14) v = static_cast<uint32_t>((tp.s2_int[k] >> (8 * (b - 6))) & 0xFFu);
         bdig[b * 128 + ((((k >> 4) ^ (b & 7)) << 4) | (k & 15))] = static_cast<uint8_t>(v);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (tid < 32) {
+    if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
-                     "n"(Cf::kTmemCols));
+                     "n"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_before();
@@ -250,20 +234,16 @@ __global__ void __launch_bounds__(kThreads, R == 4 ? 5 : 4)
         }
     };
 
-    if (tid >= kConsumers) {  // producer warp: one lane issues the TMA boxes
-        if (tid == kConsumers) {
+    if (warp == 4 && lane == 0) {  // TMA producer
+        {
             const uint64_t pol = evict_first();
             for (int64_t k = 0, tile = blockIdx.x; tile < tiles; ++k, tile += gridDim.x, advance()) {
                 const int st = static_cast<int>(k % S);
                 mbar_wait_backoff(saddr(&empty[st]), static_cast<uint32_t>(((k / S) & 1) ^ 1));
                 const int64_t i0 = chunk * kRows;
                 const int64_t rem = (m - i0 + 127) / 128;
-                const int ng = rem < R ? static_cast<int>(rem) : R;
+                const int ng = rem < kGroups ? static_cast<int>(rem) : kGroups;
                 const uint32_t fb = saddr(&full[st]);
-                if (probe == 2) {  // compute-only probe: stale planes, no loads
-                    mbar_arrive(fb);
-                    continue;
-                }
                 mbar_expect_tx(fb, static_cast<uint32_t>(ng * kGroupBytes));
                 const uint32_t dst = saddr(sbuf) + st * kStageBytes;
                 for (int g = 0; g < ng; ++g)
@@ -273,172 +253,123 @@ __global__ void __launch_bounds__(kThreads, R == 4 ? 5 : 4)
         }
         return;
     }
+    if (warp == 4) {  // lane 1: MMA issuer
+        if (lane == 1) {
+            const uint64_t bd = sdesc_sw128(saddr(bdig));
+            for (int64_t k = 0, tile = blockIdx.x; tile < tiles; ++k, tile += gridDim.x) {
+                const int st = static_cast<int>(k % S), b = static_cast<int>(k & 1);
+                mbar_wait(saddr(&full[st]), static_cast<uint32_t>((k / S) & 1));
+                mbar_wait(saddr(&tmem_empty[b]), static_cast<uint32_t>(((k >> 1) & 1) ^ 1));
+                tc_after();
+                const uint32_t stage = saddr(sbuf) + st * kStageBytes;
+#pragma unroll
+                for (int g = 0; g < kGroups; ++g)
+                    mma_u8(tbase + b * (16 * kGroups) + g * 16, sdesc_sw128(stage + g * kGroupBytes), bd);
+                mma_commit(saddr(&mma_full[b]));
+            }
+        }
+        return;
+    }
 
-    const int warp = tid >> 5, lane = tid & 31;
-    // C2-chain geometry: rows R tid .. R tid + R - 1 = group tid / (128 / R),
-    // bytes o .. o + R - 1 of each 128-byte plane row, o = R (tid % (128 / R)),
-    // at 16-byte chunk o / 16 XOR (plane % 8)
-    constexpr int kPerGroup = 128 / R;
-    const int grp = tid / kPerGroup, o = R * (tid % kPerGroup), chk = o >> 4;
-    const uint32_t row_off = static_cast<uint32_t>(grp * kGroupBytes + (o & 15));
-    // exchange (bytes): owner tid reads its R rows as R/2 16-byte chunks,
-    // chunk jj at 16 ((R/2) tid + (jj ^ sw(tid))), sw(t) = (t >> log2(16/R)) % (R/2),
-    // so 8 consecutive owners hit 8 bank groups; the writer of tile row
-    // 128 g + 32 warp + lane (TMEM lane owner) uses the same map, which is
-    // 1024 g bytes past its g = 0 slot
-    constexpr int kHalf = R / 2, kSwShift = R == 8 ? 1 : 2;
-    const int r0 = 32 * warp + lane, own0 = r0 / R;
-    const uint32_t xw = 8u * static_cast<uint32_t>(R * own0 + 2 * (((r0 >> 1) & (kHalf - 1)) ^
-                                                                  ((own0 >> kSwShift) & (kHalf - 1))) +
-                                                   (r0 & 1));
-    const uint32_t xr = 8u * R * static_cast<uint32_t>(tid), xr_x = static_cast<uint32_t>((tid >> kSwShift) & (kHalf - 1));
-    const uint32_t bdesc_lo = saddr(bdig);
+    // consumers: row 128 g + 32 warp + lane of each group g
+    const int rin = 32 * warp + lane;
+    // swizzled byte of that row in plane t of group g: chunk rin / 16 XOR (t % 8)
+    const uint32_t row_lo = static_cast<uint32_t>(rin & 15), row_chunk = static_cast<uint32_t>(rin >> 4);
+    unsigned long long n_replay = 0;
     for (int64_t k = 0, tile = blockIdx.x; tile < tiles; ++k, tile += gridDim.x, advance()) {
-        const int st = static_cast<int>(k % S);
-        const int64_t i0 = chunk * kRows + tid * R;
-        const bool vec = vec_ok && i0 + R <= m;
-        int me[R];
-        if (vec) {
-            if constexpr (R == 8)
-                ld_nc_v8(mu_exp + i0, me);
-            else
-                asm volatile("ld.global.nc.v4.s32 {%0, %1, %2, %3}, [%4];"
-                             : "=r"(me[0]), "=r"(me[1]), "=r"(me[2]), "=r"(me[3])
-                             : "l"(mu_exp + i0));
-        } else {
+        const int st = static_cast<int>(k % S), b = static_cast<int>(k & 1);
+        const int64_t row0 = chunk * kRows;
+        const int rows_left = m - row0 < kRows ? static_cast<int>(m - row0) : kRows;
+        const int32_t* mu_t = mu_exp + row0 + rin;
+        int me[kGroups];
 #pragma unroll
-            for (int q = 0; q < R; ++q) me[q] = i0 + q < m ? mu_exp[i0 + q] : 0;
-        }
-        const int ne = nu_exp[j];
-        mbar_wait(saddr(&full[st]), static_cast<uint32_t>((k / S) & 1));
-        if (probe == 1) {  // memory-only probe (tools/k3_time.py): planes in, zeros out
-            __syncwarp();
-            if (lane == 0) mbar_arrive(saddr(&empty[st]));
-            if (vec) {
-                double z[R] = {};
-#pragma unroll
-                for (int v = 0; v < R; v += 4) st_v4_f64(static_cast<double*>(C) + i0 + v + j * ldc, z + v);
-            }
-            continue;
-        }
-        const uint32_t stage = saddr(sbuf) + st * kStageBytes;
-        if (tid == 0) {
-            tc_after();
-            const uint64_t bd = sdesc_sw128(bdesc_lo);
-#pragma unroll
-            for (int g = 0; g < R; ++g) mma_u8(tbase + g * 16, sdesc_sw128(stage + g * kGroupBytes), bd);
-            mma_commit(saddr(&mma_bar));
-        }
-        // C2 = sum fl(s2_t u) in ascending t, from the swizzled plane rows
-        double c2[R];
-#pragma unroll
-        for (int q = 0; q < R; ++q) c2[q] = 0.0;
-        const uint32_t rowbase = stage + row_off;
-#pragma unroll
-        for (int t = 0; t < kMaxMod; ++t) {
-            const uint2 w = RowWord<R>::lds(rowbase + t * 128 + ((chk ^ (t & 7)) << 4));
-#pragma unroll
-            for (int q = 0; q < R; ++q) {
-                const uint32_t ub = __byte_perm(q < 4 ? w.x : w.y, 0u, 0x4440u | (q & 3));
-                const double V = __hiloint2double(0x43300000, static_cast<int>(ub));  // 2^52 + u
-                c2[q] = __dadd_rn(c2[q], __fma_rn(c.s2[t], V, c.s2_m52[t]));
-            }
-        }
-        mbar_wait(saddr(&mma_bar), static_cast<uint32_t>(k & 1));
+        for (int g = 0; g < kGroups; ++g) me[g] = 128 * g + rin < rows_left ? __ldg(mu_t + 128 * g) : 0;
+        const int ne = __ldg(nu_exp + j);
+        mbar_wait(saddr(&mma_full[b]), static_cast<uint32_t>((k >> 1) & 1));
         tc_after();
-        // exact c1 of this warp's TMEM rows 128 g + 32 warp + lane, exchanged
-        // through the consumed stage (every warp's LDS of it and the MMA are
-        // done once all consumers pass the first barrier):
-        // T = X + 2^16 Y + 2^32 Z < 2^52 as an integer pair, c1 = T 2^E by one
-        // DFMA on 2^52 + T (exact: (2^52 + T) 2^E - 2^(52+E) is representable)
-        double c1w[R];
-        constexpr int kBatch = R < 4 ? R : 4;
+        double c1[kGroups], c2[kGroups];
 #pragma unroll
-        for (int h = 0; h < R / kBatch; ++h) {
-            uint32_t v[kBatch][8];
+        for (int h = 0; h < kGroups / kTmemBatch; ++h) {
+            uint32_t v[kTmemBatch][16];
+            const uint32_t ta =
+                tbase + (static_cast<uint32_t>(warp * 32) << 16) + b * (16 * kGroups) + h * (16 * kTmemBatch);
 #pragma unroll
-            for (int g = 0; g < kBatch; ++g)
-                tmem_ld8(tbase + (static_cast<uint32_t>(warp * 32) << 16) + (kBatch * h + g) * 16, v[g]);
+            for (int q = 0; q < kTmemBatch; ++q) tmem_ld16(ta + 16 * q, v[q]);
             tmem_wait_ld();
 #pragma unroll
-            for (int g = 0; g < kBatch; ++g) {
-                const uint32_t X = v[g][0] + (v[g][1] << 8), Y = v[g][2] + (v[g][3] << 8), Z = v[g][4] + (v[g][5] << 8);
-                const uint64_t T =
-                    static_cast<uint64_t>(X) + (static_cast<uint64_t>(Y) << 16) + (static_cast<uint64_t>(Z) << 32);
-                const double V = __hiloint2double(static_cast<int>(static_cast<uint32_t>(T >> 32) | 0x43300000u),
-                                                  static_cast<int>(static_cast<uint32_t>(T)));
-                c1w[kBatch * h + g] = __fma_rn(V, tp.sc0, tp.sc0m52);
+            for (int q = 0; q < kTmemBatch; ++q) {
+                const uint32_t* w = v[q];
+                // c1 = 2^E1 (X1 + 2^16 Y1 + 2^32 Z1) exactly: one DFMA on 2^52 + T1
+                const uint64_t T1 = static_cast<uint64_t>(w[0] + (w[1] << 8)) +
+                                    (static_cast<uint64_t>(w[2] + (w[3] << 8)) << 16) +
+                                    (static_cast<uint64_t>(w[4] + (w[5] << 8)) << 32);
+                c1[kTmemBatch * h + q] = __fma_rn(pair52(T1), tp.sc1, tp.sc1m);
+                // S = 2^E2 (H 2^32 + L), H, L < 2^46: both parts exact, one rounding
+                const uint64_t L = static_cast<uint64_t>(w[6] + (w[7] << 8)) +
+                                   (static_cast<uint64_t>(w[8] + (w[9] << 8)) << 16);
+                const uint64_t H = static_cast<uint64_t>(w[10] + (w[11] << 8)) +
+                                   (static_cast<uint64_t>(w[12] + (w[13] << 8)) << 16);
+                c2[kTmemBatch * h + q] =
+                    __dadd_rn(__fma_rn(pair52(H), tp.sc2h, tp.sc2hm), __fma_rn(pair52(L), tp.sc2l, tp.sc2lm));
             }
         }
         tc_before();
-        consumers_sync();
-#pragma unroll
-        for (int g = 0; g < R; ++g)
-            asm volatile("st.shared.f64 [%0], %1;" ::"r"(stage + xw + g * 1024), "d"(c1w[g]) : "memory");
-        consumers_sync();
-        double c1[R];
-#pragma unroll
-        for (int jj = 0; jj < kHalf; ++jj)
-            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
-                         : "=d"(c1[2 * jj]), "=d"(c1[2 * jj + 1])
-                         : "r"(stage + xr + ((jj ^ xr_x) << 4))
-                         : "memory");
-        // slot st back to the producer: order this thread's generic accesses
-        // before the TMA (async proxy) overwrite
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(saddr(&empty[st]));
-        double r[R];
+        if (lane == 0) mbar_arrive(saddr(&tmem_empty[b]));
+        const uint32_t stage = saddr(sbuf) + st * kStageBytes;
+        double* Cd = static_cast<double*>(C) + j * ldc + row0 + rin;
+        float* Cf32 = static_cast<float*>(C) + j * ldc + row0 + rin;
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
-            const double qv = rint(__dmul_rn(c.P_inv, c1[q]));
-            const double cpp = __fma_rn(-c.P2, qv, __dadd_rn(__fma_rn(-c.P1, qv, c1[q]), c2[q]));
-            r[q] = unscale_fast(cpp, -(me[q] + ne));
-        }
-        if (!kPlain) {
-#pragma unroll
-            for (int q = 0; q < R; ++q) {
-                const int64_t i = i0 + q;
-                const double old = (beta != 0.0 && i < m)
-                                       ? (kF32Out ? static_cast<double>(static_cast<float*>(C)[i + j * ldc])
-                                                  : static_cast<double*>(C)[i + j * ldc])
-                                       : 0.0;
-                r[q] = __dadd_rn(__dmul_rn(alpha, r[q]), __dmul_rn(beta, old));
-            }
-        }
-        if (vec) {
-            if constexpr (kF32Out && R == 8) {
-                float f[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) f[q] = __double2float_rn(r[q]);
-                st_v8_f32(static_cast<float*>(C) + i0 + j * ldc, f);
-            } else if constexpr (kF32Out) {
-                asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(static_cast<float*>(C) + i0 + j * ldc),
-                             "f"(__double2float_rn(r[0])), "f"(__double2float_rn(r[1])), "f"(__double2float_rn(r[2])),
-                             "f"(__double2float_rn(r[3]))
-                             : "memory");
+        for (int g = 0; g < kGroups; ++g) {
+            const bool live = 128 * g + rin < rows_left;
+            const double qv = rint(__dmul_rn(c.P_inv, c1[g]));
+            const double X = __fma_rn(-c.P1, qv, c1[g]);
+            double cpp;
+            if constexpr (kExact) {  // c2 exact: no interval
+                cpp = __fma_rn(-c.P2, qv, __dadd_rn(X, c2[g]));
             } else {
-#pragma unroll
-                for (int v = 0; v < R; v += 4) st_v4_f64(static_cast<double*>(C) + i0 + v + j * ldc, r + v);
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < R; ++q) {
-                const int64_t i = i0 + q;
-                if (i < m) {
-                    if (kF32Out)
-                        static_cast<float*>(C)[i + j * ldc] = __double2float_rn(r[q]);
-                    else
-                        static_cast<double*>(C)[i + j * ldc] = r[q];
+                const double rad = __dmul_ru(c2[g], tp.rfac);
+                cpp = __fma_rn(-c.P2, qv, __dadd_rn(X, __dsub_rd(c2[g], rad)));
+                const double zhi = __fma_rn(-c.P2, qv, __dadd_rn(X, __dadd_ru(c2[g], rad)));
+                if (__double_as_longlong(cpp) != __double_as_longlong(zhi) && live) {
+                    // replay the reference's c2 (emulator.cpp:53) from the planes
+                    const uint32_t line = stage + g * kGroupBytes + row_lo;
+                    double c2r = 0.0;
+#pragma unroll 1
+                    for (int t = 0; t < n_mod; ++t) {
+                        uint32_t ub;
+                        asm volatile("ld.shared.u8 %0, [%1];"
+                                     : "=r"(ub)
+                                     : "r"(line + t * 128 + ((row_chunk ^ static_cast<uint32_t>(t & 7)) << 4)));
+                        c2r = __dadd_rn(c2r, __fma_rn(c.s2[t], __hiloint2double(0x43300000, static_cast<int>(ub)),
+                                                      c.s2_m52[t]));
+                    }
+                    cpp = __fma_rn(-c.P2, qv, __dadd_rn(X, c2r));
+                    ++n_replay;
                 }
             }
+            double r = unscale_fast(cpp, -(me[g] + ne));
+            if (live) {
+                if (!kPlain) {
+                    const double old = beta != 0.0 ? (kF32Out ? static_cast<double>(Cf32[128 * g]) : Cd[128 * g]) : 0.0;
+                    r = __dadd_rn(__dmul_rn(alpha, r), __dmul_rn(beta, old));
+                }
+                if (kF32Out)
+                    Cf32[128 * g] = __double2float_rn(r);
+                else
+                    Cd[128 * g] = r;
+            }
         }
+        // slot st: the MMA has read it (mma_full) and any replay is done
+        __syncwarp();
+        if (lane == 0) mbar_arrive(saddr(&empty[st]));
     }
+    if (replays && n_replay) atomicAdd(replays, n_replay);
     tc_before();
-    consumers_sync();
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
     if (warp == 0) {
         tc_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(Cf::kTmemCols));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols));
     }
 }
 
@@ -454,12 +385,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <bool kF32Out, bool kPlain, int kMaxMod, int P, int R, int S>
+template <bool kF32Out, bool kPlain, bool kExact, int P, int S>
 bool launch_t(const CUtensorMap& map, int num_sms, cudaStream_t s, int64_t m, int64_t n, const int32_t* mu_exp,
               const int32_t* nu_exp, const DevConsts& c, const TcParams& tp, double alpha, double beta, void* C,
-              int64_t ldc, bool vec_ok) {
-    using Cf = TcCfg<R, S, P>;
-    auto kern = reconstruct_tc_kernel<kF32Out, kPlain, kMaxMod, P, R, S>;
+              int64_t ldc, unsigned long long* replays) {
+    using Cf = TcCfg<P, S>;
+    auto kern = reconstruct_tc_kernel<kF32Out, kPlain, kExact, P, S>;
     constexpr int smem = Cf::kSmem;
     static bool attr = false;
     if (!attr) {
@@ -479,96 +410,122 @@ bool launch_t(const CUtensorMap& map, int num_sms, cudaStream_t s, int64_t m, in
         const int by_smem = smem_sm / (smem + static_cast<int>(fa.sharedSizeBytes) + 1024);
         const int regs_warp = (fa.numRegs * 32 + 255) / 256 * 256;
         const int by_regs = regs_sm / (regs_warp * (kThreads / 32));
-        return std::min(std::min(by_smem, by_regs), 512 / Cf::kTmemCols);
+        return std::min(std::min(by_smem, by_regs), 512 / kTmemCols);
     }();
     if (per_sm < 1) return false;
-    const int64_t row_chunks = (m + Cf::kRows - 1) / Cf::kRows;
+    const int64_t row_chunks = (m + kRows - 1) / kRows;
     const int64_t grid = std::min<int64_t>(row_chunks * n, static_cast<int64_t>(num_sms) * per_sm);
-    static const int probe = std::getenv("OZK_K3_PROBE") ? std::atoi(std::getenv("OZK_K3_PROBE")) : 0;
     kern<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(map, m, n, row_chunks, mu_exp, nu_exp, c, tp, alpha, beta,
-                                                             C, ldc, vec_ok, kF32Out ? 0 : probe);
+                                                             C, ldc, replays);
     return true;
-}
-
-int k3_tc_rows() {
-    static const int r = [] {
-        const char* e = std::getenv("OZK_K3_TC_ROWS");
-        return e && std::atoi(e) == 4 ? 4 : 8;
-    }();
-    return r;
 }
 
 template <bool kF32Out, bool kPlain>
 bool launch_variant(const CUtensorMap& map, int sms, cudaStream_t s, int64_t m, int64_t n, const int32_t* mu_exp,
                     const int32_t* nu_exp, const DevConsts& c, const TcParams& tp, double alpha, double beta, void* C,
-                    int64_t ldc, bool vec_ok) {
-#define OZK_K3T(MAXN, P)                                                                                     \
-    (k3_tc_rows() == 8                                                                                           \
-         ? launch_t<kF32Out, kPlain, MAXN, P, 8, P == 16 ? 3 : 2>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc, \
-                                                    vec_ok)                                                    \
-         : launch_t<kF32Out, kPlain, MAXN, P, 4, 4>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc, \
-                                                    vec_ok))
-    if (c.n <= 8) return OZK_K3T(8, 16);
-    if (c.n <= 12) return OZK_K3T(12, 16);
-    if (c.n <= 14) return OZK_K3T(14, 16);
-    if (c.n <= 16) return OZK_K3T(16, 16);
-    return OZK_K3T(OZK_MAX_MODULI, 24);
-#undef OZK_K3T
+                    int64_t ldc, unsigned long long* replays) {
+    if (tp.rfac == 0.0)  // c2 exact (N <= 10): no interval, never a replay
+        return launch_t<kF32Out, kPlain, true, 16, 4>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc,
+                                                      replays);
+    if (c.n <= 16)
+        return launch_t<kF32Out, kPlain, false, 16, 4>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc,
+                                                       replays);
+    return launch_t<kF32Out, kPlain, false, 24, 4>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc,
+                                                   replays);
 }
 
-// opt-in (OZK_K3_TC=1): measured slower than the all-FP64 bulk kernel at
-// every N, so the production path does not take it
+// OZK_K3_TC=0 selects the all-FP64 bulk kernel (A/B timing)
 bool k3_tc_enabled() {
     static const bool b = [] {
         const char* e = std::getenv("OZK_K3_TC");
-        return e && std::atoi(e) == 1;
+        return !(e && std::atoi(e) == 0);
     }();
     return b;
 }
 
+// lowest set bit exponent of a positive finite double
+int lsb_exponent(double v) {
+    int ex = 0;
+    const double fr = std::frexp(v, &ex);
+    unsigned long long mant = static_cast<unsigned long long>(std::ldexp(fr, 53));
+    int lsb = ex - 53;
+    while ((mant & 1ull) == 0) {
+        mant >>= 1;
+        ++lsb;
+    }
+    return lsb;
+}
+
+// S_i = v_i / 2^E on the common grid of the table (E = the lowest set bit);
+// false if a value is negative / non-finite or an integer exceeds `max_bits`
+bool integer_table(const double* v, int n, int max_bits, int* E_out, unsigned long long* out) {
+    int E = 1 << 30;
+    for (int t = 0; t < n; ++t) {
+        if (!(v[t] >= 0.0) || std::isinf(v[t])) return false;
+        if (v[t] != 0.0) E = std::min(E, lsb_exponent(v[t]));
+    }
+    if (E == (1 << 30)) E = 0;
+    for (int t = 0; t < n; ++t) {
+        const double q = std::ldexp(v[t], -E);
+        if (q >= std::ldexp(1.0, max_bits)) return false;
+        out[t] = static_cast<unsigned long long>(q);
+        if (static_cast<double>(out[t]) != q) return false;
+    }
+    *E_out = E;
+    return true;
+}
+
 }  // namespace
 
+// device counter of replayed elements (tests / tools read it through
+// ozk_k3_replays); nullptr until first asked for
+static unsigned long long* g_replays = nullptr;
+unsigned long long* k3_replay_counter(bool create) {
+    if (!g_replays && create) {
+        if (cudaMalloc(&g_replays, sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+        cudaMemset(g_replays, 0, sizeof(unsigned long long));
+    }
+    return g_replays;
+}
+
 // The tensor-core K3 for FP64 tables (see the header comment); returns false
-// (nothing launched) when its preconditions do not hold, and the caller takes
-// the all-FP64 kernel: FP32 tables (full-width s1, rounded products), an s1
-// table that is not on a common grid below 2^48 / 2^53, a U layout TMA cannot
-// describe, or OZK_K3_TC=0.
+// (nothing launched) when its preconditions do not hold and the caller takes
+// the all-FP64 kernel: FP32 tables (full-width s1, rounded products), tables
+// off the integer grids checked here, a U layout TMA cannot describe, or
+// OZK_K3_TC=0.
 bool launch_reconstruct_tc(const uint8_t* u, int64_t ldu, int64_t stride, int64_t m, int64_t n, const int32_t* mu_exp,
                            const int32_t* nu_exp, const DevConsts& c, double alpha, double beta, void* C, int64_t ldc,
                            int c_is_f32, cudaStream_t s) {
     if (!k3_tc_enabled() || c.precision != OZK_FP64 || c.n < 1 || c.n > OZK_MAX_MODULI) return false;
     if (m < 1 || n < 1 || m > (int64_t(1) << 31) - 1024 || n > (int64_t(1) << 31) - 1) return false;
     if (reinterpret_cast<uintptr_t>(u) % 16 || ldu % 16 || stride % 16 || ldu < m) return false;
-    // common grid 2^E of the s1 table and the exactness bound
-    int E = 1 << 30;
-    for (int t = 0; t < c.n; ++t) {
-        const double v = c.s1[t];
-        if (!(v >= 0.0) || std::isinf(v)) return false;
-        if (v == 0.0) continue;
-        int ex = 0;
-        double fr = std::frexp(v, &ex);  // v = fr 2^ex, fr in [0.5, 1)
-        unsigned long long mant = static_cast<unsigned long long>(std::ldexp(fr, 53));
-        int lsb = ex - 53;
-        while ((mant & 1ull) == 0) {
-            mant >>= 1;
-            ++lsb;
-        }
-        E = std::min(E, lsb);
-    }
-    if (E == (1 << 30)) E = 0;
-    if (E < -1000 || E > 1023 - 52) return false;
     TcParams tp{};
-    unsigned __int128 total = 0;
-    for (int t = 0; t < c.n; ++t) {
-        const double q = std::ldexp(c.s1[t], -E);
-        if (q >= 0x1p48) return false;
-        tp.s_int[t] = static_cast<unsigned long long>(q);
-        if (static_cast<double>(tp.s_int[t]) != q) return false;
-        total += static_cast<unsigned __int128>(tp.s_int[t]) * static_cast<unsigned>(c.p[t] - 1);
-    }
-    if (total >= (static_cast<unsigned __int128>(1) << 52)) return false;  // T < 2^52: one-DFMA conversion
-    tp.sc0 = std::ldexp(1.0, E);
-    tp.sc0m52 = -std::ldexp(1.0, E + 52);
+    int E1 = 0, E2 = 0;
+    if (!integer_table(c.s1, c.n, 48, &E1, tp.s1_int)) return false;
+    if (!integer_table(c.s2, c.n, 64, &E2, tp.s2_int)) return false;
+    unsigned __int128 total = 0;  // c1 exact and T1 < 2^52 (one-DFMA conversion)
+    for (int t = 0; t < c.n; ++t) total += static_cast<unsigned __int128>(tp.s1_int[t]) * static_cast<unsigned>(c.p[t] - 1);
+    if (total >= (static_cast<unsigned __int128>(1) << 52)) return false;
+    if (E1 < -1000 || E1 > 1023 - 52 || E2 < -1000 || E2 > 1023 - 84) return false;
+    tp.sc1 = std::ldexp(1.0, E1);
+    tp.sc1m = -std::ldexp(1.0, E1 + 52);
+    tp.sc2h = std::ldexp(1.0, E2 + 32);
+    tp.sc2hm = -std::ldexp(1.0, E2 + 84);
+    tp.sc2l = std::ldexp(1.0, E2);
+    tp.sc2lm = -std::ldexp(1.0, E2 + 52);
+    // with every s2_i u_i and every partial sum on the 2^E2 grid below 2^53
+    // the reference's c2 is exact (= S), so the interval collapses
+    unsigned __int128 total2 = 0;
+    for (int t = 0; t < c.n; ++t)
+        total2 += static_cast<unsigned __int128>(tp.s2_int[t]) * static_cast<unsigned>(c.p[t] - 1);
+    tp.rfac = total2 < (static_cast<unsigned __int128>(1) << 53) ? 0.0 : (c.n + 3) * 0x1p-53;
+    // test hook: a radius of c2 itself sends (almost) every element through
+    // the replay of the reference's sequential c2
+    static const bool replay_all = [] {
+        const char* e = std::getenv("OZK_K3_REPLAY_ALL");
+        return e && std::atoi(e) == 1;
+    }();
+    if (replay_all) tp.rfac = 1.0;
 
     auto enc = encode_fn();
     if (!enc) return false;
@@ -583,19 +540,17 @@ bool launch_reconstruct_tc(const uint8_t* u, int64_t ldu, int64_t stride, int64_
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
 
-    const int esz = c_is_f32 ? 4 : 8;
-    const bool vec_ok = (reinterpret_cast<uintptr_t>(mu_exp) % 32 == 0) && (reinterpret_cast<uintptr_t>(C) % 32 == 0) &&
-                        ((ldc * esz) % 32 == 0);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    unsigned long long* replays = k3_replay_counter(false);
     const bool plain = alpha == 1.0 && beta == 0.0;
     if (c_is_f32)
-        return plain ? launch_variant<true, true>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc, vec_ok)
+        return plain ? launch_variant<true, true>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc, replays)
                      : launch_variant<true, false>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc,
-                                                   vec_ok);
-    return plain ? launch_variant<false, true>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc, vec_ok)
-                 : launch_variant<false, false>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc, vec_ok);
+                                                   replays);
+    return plain ? launch_variant<false, true>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc, replays)
+                 : launch_variant<false, false>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc, replays);
 }
 
 }  // namespace ozk

@@ -149,6 +149,13 @@ class Context:
         _lib.check(self._lib.ozk_profile_read(self.handle, ms, calls, int(reset)))
         return {name: (ms[i], calls[i]) for i, name in enumerate(_lib.PROFILE_SLOTS)}
 
+    def k3_replays(self, reset: bool = True) -> int:
+        """elements whose C2 the tensor-core K3 replayed sequentially since
+        counting began (the first call starts it)"""
+        n = C.c_ulonglong(0)
+        _lib.check(self._lib.ozk_k3_replays(C.byref(n), int(reset)))
+        return int(n.value)
+
     # ---- host (reference-facing) GEMM ----------------------------------------------
     def gemm_host(self, a: np.ndarray, b: np.ndarray, cfg: EmuConfig, alpha: float = 1.0, beta: float = 0.0,
                   c: np.ndarray | None = None, c_dtype=np.float64, constants=None, trans_a: bool = False,

@@ -1,12 +1,17 @@
-"""The opt-in tensor-core K3 (OZK_K3_TC=1, csrc/k3_tc.cu: C1 = sum s1_i u_i as a
-u8 x u8 tcgen05 MMA against the base-256 digits of the FP64 s1 table) is held to
-the same bar as the production kernel: the randomised parity sweep, run in a
-child process because the library reads the switch once per process, in both
-tile shapes (8 and 4 rows per thread)."""
+"""K3 variants held to the production bar. The default K3 for FP64 tables
+(csrc/k3_tc.cu) takes C1 and an interval for C2 from one u8 x u8 tcgen05 MMA
+and replays the reference's sequential C2 only where the interval cannot
+decide the final rounding; the all-FP64 kernel (csrc/k3_reconstruct.cu) takes
+FP32 tables and OZK_K3_TC=0. The library reads both switches once per process,
+so the sweeps run in child processes:
+  * OZK_K3_REPLAY_ALL=1 widens the interval so (almost) every element takes the
+    replay path — the path the default run reaches only ~100 times per 16384^2;
+  * OZK_K3_TC=0 runs every FP64 case through the all-FP64 kernel."""
 import os
 import subprocess
 import sys
 
+import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -14,10 +19,31 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("rows", ["8", "4"])
-def test_k3_tc_random_sweep(rows):
-    env = dict(os.environ, OZK_K3_TC="1", OZK_K3_TC_ROWS=rows)
+@pytest.mark.parametrize("env", [{"OZK_K3_REPLAY_ALL": "1"}, {"OZK_K3_TC": "0"}], ids=["replay_all", "fp64_kernel"])
+def test_k3_variant_random_sweep(env):
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
-                        os.path.join(ROOT, "tests", "test_gpu_random.py")],
-                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+                        os.path.join(ROOT, "tests", "test_gpu_random.py"), os.path.join(ROOT, "tests", "test_gpu_parity.py")],
+                       cwd=ROOT, env=dict(os.environ, **env), capture_output=True, text=True, timeout=1500)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_k3_replays_are_rare_and_exact(oracle):
+    """N = 14 at a size where the interval fails for a handful of elements:
+    the count is small and the result still equals the oracle bit for bit."""
+    torch = pytest.importorskip("torch")
+    from paper_2508_03984_b200 import Context, EmuConfig, gen_matrix
+
+    ctx = Context(0)
+    m, n, k = 1024, 1024, 512
+    a = gen_matrix(m, k, 0.5, 11)
+    b = gen_matrix(k, n, 0.5, 12)
+    ctx.k3_replays(reset=True)
+    A = torch.from_numpy(np.ascontiguousarray(a.T)).cuda().t()
+    B = torch.from_numpy(np.ascontiguousarray(b.T)).cuda().t()
+    C = torch.empty((n, m), dtype=torch.float64, device="cuda").t()
+    ctx.gemm(A, B, EmuConfig(n_moduli=14), C)
+    replays = ctx.k3_replays(reset=True)
+    want = oracle.gemm(a, b, 14, 0)
+    got = C.cpu().numpy()
+    assert np.array_equal(got.view(np.int64), want.view(np.int64))
+    assert replays < m * n // 1000

@@ -26,6 +26,7 @@ def main():
         cfg = EmuConfig(n_moduli=N, precision=Precision(prec))
         ctx.stage_reconstruct(cfg, n, n, U, ldu, mu, mu, C)
         torch.cuda.synchronize()
+        ctx.k3_replays(reset=True)  # start counting
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(reps):
@@ -34,6 +35,7 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
         out[f"N{N}_ms"] = round(ms, 3)
+        out[f"N{N}_replays_per_call"] = ctx.k3_replays(reset=True) / reps
         out[f"N{N}_TBs"] = round((N + (4 if prec else 8)) * n * n / ms / 1e9, 2)
         del U
     print(json.dumps(out))
