@@ -173,6 +173,15 @@ __device__ __forceinline__ double pair52(uint64_t T) {
     return __hiloint2double(static_cast<int>(static_cast<uint32_t>(T >> 32) | 0x43300000u),
                             static_cast<int>(static_cast<uint32_t>(T)));
 }
+// 2^52 + x + 2^16 y (+ 2^32 z) for x, y, z < 2^30 without 64-bit arithmetic:
+// low word x + (y << 16) with carry, high word 0x43300000 + (y >> 16) + z + carry
+__device__ __forceinline__ double pair52_xyz(uint32_t x, uint32_t y, uint32_t z) {
+    uint32_t lo, hi;
+    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
+        : "=r"(lo), "=r"(hi)
+        : "r"(x), "r"(y << 16), "r"(y >> 16), "r"(z + 0x43300000u));
+    return __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
+}
 
 template <bool kF32Out, bool kPlain, bool kExact, int P, int S, int kTmemBatch = 2>
 __global__ void __launch_bounds__(kThreads, 4)
@@ -300,17 +309,12 @@ __global__ void __launch_bounds__(kThreads, 4)
             for (int q = 0; q < kTmemBatch; ++q) {
                 const uint32_t* w = v[q];
                 // c1 = 2^E1 (X1 + 2^16 Y1 + 2^32 Z1) exactly: one DFMA on 2^52 + T1
-                const uint64_t T1 = static_cast<uint64_t>(w[0] + (w[1] << 8)) +
-                                    (static_cast<uint64_t>(w[2] + (w[3] << 8)) << 16) +
-                                    (static_cast<uint64_t>(w[4] + (w[5] << 8)) << 32);
-                c1[kTmemBatch * h + q] = __fma_rn(pair52(T1), tp.sc1, tp.sc1m);
+                c1[kTmemBatch * h + q] = __fma_rn(
+                    pair52_xyz(w[0] + (w[1] << 8), w[2] + (w[3] << 8), w[4] + (w[5] << 8)), tp.sc1, tp.sc1m);
                 // S = 2^E2 (H 2^32 + L), H, L < 2^46: both parts exact, one rounding
-                const uint64_t L = static_cast<uint64_t>(w[6] + (w[7] << 8)) +
-                                   (static_cast<uint64_t>(w[8] + (w[9] << 8)) << 16);
-                const uint64_t H = static_cast<uint64_t>(w[10] + (w[11] << 8)) +
-                                   (static_cast<uint64_t>(w[12] + (w[13] << 8)) << 16);
-                c2[kTmemBatch * h + q] =
-                    __dadd_rn(__fma_rn(pair52(H), tp.sc2h, tp.sc2hm), __fma_rn(pair52(L), tp.sc2l, tp.sc2lm));
+                const double Lp = pair52_xyz(w[6] + (w[7] << 8), w[8] + (w[9] << 8), 0u);
+                const double Hp = pair52_xyz(w[10] + (w[11] << 8), w[12] + (w[13] << 8), 0u);
+                c2[kTmemBatch * h + q] = __dadd_rn(__fma_rn(Hp, tp.sc2h, tp.sc2hm), __fma_rn(Lp, tp.sc2l, tp.sc2lm));
             }
         }
         tc_before();
@@ -325,14 +329,26 @@ __global__ void __launch_bounds__(kThreads, 4)
             const double qv = rint(__dmul_rn(c.P_inv, c1[g]));
             const double X = __fma_rn(-c.P1, qv, c1[g]);
             double cpp;
+            bool decided = true;
             if constexpr (kExact) {  // c2 exact: no interval
                 cpp = __fma_rn(-c.P2, qv, __dadd_rn(X, c2[g]));
             } else {
                 const double rad = __dmul_ru(c2[g], tp.rfac);
                 cpp = __fma_rn(-c.P2, qv, __dadd_rn(X, __dsub_rd(c2[g], rad)));
                 const double zhi = __fma_rn(-c.P2, qv, __dadd_rn(X, __dadd_ru(c2[g], rad)));
-                if (__double_as_longlong(cpp) != __double_as_longlong(zhi) && live) {
-                    // replay the reference's c2 (emulator.cpp:53) from the planes
+                decided = __double_as_longlong(cpp) == __double_as_longlong(zhi) || !live;
+            }
+            // unscale by moving the exponent field (x and the result normal)
+            const int e = -(me[g] + ne);
+            const int hi = __double2hiint(cpp);
+            const int ex = (hi >> 20) & 0x7ff;
+            const bool normal = ex != 0 && static_cast<unsigned>(ex + e - 1) < 2046u;
+            double r = __hiloint2double(hi + static_cast<int>(static_cast<unsigned>(e) << 20), __double2loint(cpp));
+            // rare paths, taken warp-uniformly: the interval did not decide
+            // (replay the reference's c2, emulator.cpp:53, from the planes) or
+            // the unscale leaves the normal range (general ldexp)
+            if (!__all_sync(0xffffffffu, decided && normal)) {
+                if (!decided) {
                     const uint32_t line = stage + g * kGroupBytes + row_lo;
                     double c2r = 0.0;
 #pragma unroll 1
@@ -347,8 +363,8 @@ __global__ void __launch_bounds__(kThreads, 4)
                     cpp = __fma_rn(-c.P2, qv, __dadd_rn(X, c2r));
                     ++n_replay;
                 }
+                r = unscale_fast(cpp, e);
             }
-            double r = unscale_fast(cpp, -(me[g] + ne));
             if (live) {
                 if (!kPlain) {
                     const double old = beta != 0.0 ? (kF32Out ? static_cast<double>(Cf32[128 * g]) : Cd[128 * g]) : 0.0;
