@@ -33,11 +33,6 @@ __device__ __forceinline__ uint32_t bound_entry(double x, int e) {
     return static_cast<uint32_t>(__double2loint(__dadd_ru(v, 0x1.0p52))) & 0xffu;
 }
 
-template <typename T>
-__device__ __forceinline__ uint32_t literal_byte(T x, const DevConsts& c, int t) {
-    return static_cast<uint32_t>(static_cast<uint8_t>(rmod_fast(x, c.p[t], c.pinv64[t], c.pinv32[t], c.n)));
-}
-
 // Column-major rows x cols input -> N column-major int8 planes (ld bytes per
 // column, plane_stride bytes apart). ROW_EXP: the scale exponent is per row
 // (A: mu), else per column (B: nu). Each thread handles 8 consecutive rows of
@@ -83,53 +78,7 @@ __global__ void __launch_bounds__(128)
                                                      pack_low_bytes(v[4], v[5], v[6], v[7]));
         return;
     }
-    uint32_t xlo[kBPerThread];
-#pragma unroll
-    for (int u = 0; u < kBPerThread; ++u)
-        xlo[u] = static_cast<uint32_t>(__double2loint(__dadd_rn(static_cast<double>(x[u]), kMagic52)));
-    // the fast/literal choice is warp-uniform: branch once, outside the modulus loop
-    if (fast) {
-        // modulus-independent half of the packed residue words (see below)
-        uint32_t xb[2] = {0u, 0u};
-#pragma unroll
-        for (int u = 0; u < kBPerThread; ++u) xb[u >> 2] += (xlo[u] + 128u) << (8 * (u & 3));
-        int8_t* dst = dst0;
-#pragma unroll
-        for (int t = 0; t < kMaxMod; ++t) {
-            if (t < c.n) {  // uniform
-                const uint32_t pt = static_cast<uint32_t>(c.p[t]);
-                uint2 word;
-                if (pt == 256) {  // p = 256: the residue is the low byte of x
-                    word = make_uint2(pack_low_bytes(xlo[0], xlo[1], xlo[2], xlo[3]),
-                                      pack_low_bytes(xlo[4], xlo[5], xlo[6], xlo[7]));
-                } else {
-                    // four residues r_u in one word without byte shuffles:
-                    // xlo_u + qlo_u (-p) = r_u (mod 2^32) with |r_u| <= 127, so
-                    // sum_u (xlo_u + 128 + qlo_u (-p)) 2^(8u) = sum_u (r_u + 128) 2^(8u)
-                    // exactly (no carries), and XOR 0x80 per byte leaves r_u mod 256
-                    uint32_t w[2] = {xb[0], xb[1]};
-#pragma unroll
-                    for (int u = 0; u < kBPerThread; ++u) {
-                        const uint32_t qlo = static_cast<uint32_t>(
-                            __double2loint(__fma_rn(static_cast<double>(x[u]), c.pinv64[t], kMagic52)));
-                        w[u >> 2] += qlo * c.negp_sh[u & 3][t];
-                    }
-                    word = make_uint2(w[0] ^ 0x80808080u, w[1] ^ 0x80808080u);
-                }
-                *reinterpret_cast<uint2*>(dst) = word;
-                dst += plane_stride;
-            }
-        }
-    } else {
-#pragma unroll 1
-        for (int t = 0; t < c.n; ++t) {
-            uint32_t v[kBPerThread];
-#pragma unroll
-            for (int u = 0; u < kBPerThread; ++u) v[u] = literal_byte(x[u], c, t);
-            *reinterpret_cast<uint2*>(dst0 + t * plane_stride) =
-                make_uint2(pack_low_bytes(v[0], v[1], v[2], v[3]), pack_low_bytes(v[4], v[5], v[6], v[7]));
-        }
-    }
+    residue_planes8<T, kMaxMod>(x, fast, dst0, plane_stride, c);
 }
 
 __global__ void round_to_f32_kernel(const double* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,

@@ -73,6 +73,69 @@ __device__ __forceinline__ uint32_t pack_low_bytes(uint32_t r0, uint32_t r1, uin
     return __byte_perm(__byte_perm(r0, r1, 0x0040), __byte_perm(r2, r3, 0x0040), 0x5410);
 }
 
+template <typename T>
+__device__ __forceinline__ uint32_t literal_byte(T x, const DevConsts& c, int t) {
+    return static_cast<uint32_t>(static_cast<uint8_t>(rmod_fast(x, c.p[t], c.pinv64[t], c.pinv32[t], c.n)));
+}
+
+// K1b core (residue.cpp:24-42): the N residue bytes of 8 consecutive
+// truncated-scaled elements x of one column, one 8-byte word per plane at
+// dst0 + t * plane_stride. fast (warp-uniform): every x of the warp lies in
+// the symmetric-residue domain (one DFMA + one IMAD per element and modulus,
+// bytes packed by IMADs); else the literal rmod_fast sequence.
+template <typename T, int kMaxMod>
+__device__ __forceinline__ void residue_planes8(const T (&x)[8], bool fast, int8_t* dst0, int64_t plane_stride,
+                                                const DevConsts& c) {
+    constexpr int kBPerThread = 8;
+    uint32_t xlo[kBPerThread];
+#pragma unroll
+    for (int u = 0; u < kBPerThread; ++u)
+        xlo[u] = static_cast<uint32_t>(__double2loint(__dadd_rn(static_cast<double>(x[u]), kMagic52)));
+    // the fast/literal choice is warp-uniform: branch once, outside the modulus loop
+    if (fast) {
+        // modulus-independent half of the packed residue words (see below)
+        uint32_t xb[2] = {0u, 0u};
+#pragma unroll
+        for (int u = 0; u < kBPerThread; ++u) xb[u >> 2] += (xlo[u] + 128u) << (8 * (u & 3));
+        int8_t* dst = dst0;
+#pragma unroll
+        for (int t = 0; t < kMaxMod; ++t) {
+            if (t < c.n) {  // uniform
+                const uint32_t pt = static_cast<uint32_t>(c.p[t]);
+                uint2 word;
+                if (pt == 256) {  // p = 256: the residue is the low byte of x
+                    word = make_uint2(pack_low_bytes(xlo[0], xlo[1], xlo[2], xlo[3]),
+                                      pack_low_bytes(xlo[4], xlo[5], xlo[6], xlo[7]));
+                } else {
+                    // four residues r_u in one word without byte shuffles:
+                    // xlo_u + qlo_u (-p) = r_u (mod 2^32) with |r_u| <= 127, so
+                    // sum_u (xlo_u + 128 + qlo_u (-p)) 2^(8u) = sum_u (r_u + 128) 2^(8u)
+                    // exactly (no carries), and XOR 0x80 per byte leaves r_u mod 256
+                    uint32_t w[2] = {xb[0], xb[1]};
+#pragma unroll
+                    for (int u = 0; u < kBPerThread; ++u) {
+                        const uint32_t qlo = static_cast<uint32_t>(
+                            __double2loint(__fma_rn(static_cast<double>(x[u]), c.pinv64[t], kMagic52)));
+                        w[u >> 2] += qlo * c.negp_sh[u & 3][t];
+                    }
+                    word = make_uint2(w[0] ^ 0x80808080u, w[1] ^ 0x80808080u);
+                }
+                *reinterpret_cast<uint2*>(dst) = word;
+                dst += plane_stride;
+            }
+        }
+    } else {
+#pragma unroll 1
+        for (int t = 0; t < c.n; ++t) {
+            uint32_t v[kBPerThread];
+#pragma unroll
+            for (int u = 0; u < kBPerThread; ++u) v[u] = literal_byte(x[u], c, t);
+            *reinterpret_cast<uint2*>(dst0 + t * plane_stride) =
+                make_uint2(pack_low_bytes(v[0], v[1], v[2], v[3]), pack_low_bytes(v[4], v[5], v[6], v[7]));
+        }
+    }
+}
+
 // mod_u8 (reconstruct.hpp:31-37): high-half multiply by floor(2^32/p - 1)
 // then two one-sided corrections. The true y lies in (-p, 2p), so the 32-bit
 // wrapping difference is exact.
