@@ -268,10 +268,11 @@ int ozk_profile_read(ozk_handle h, double* ms, int64_t* calls, int reset);
 /* K3 diagnostics (extension; no reference counterpart). The tensor-core K3
  * (FP64 tables) takes C2 from an exact integer dot product and replays the
  * reference's sequential C2 (emulator.cpp:53) only for elements whose final
- * rounding the C2 interval cannot decide. ozk_k3_replays enables counting on
- * the first call (it synchronises the device) and returns the replayed
- * elements counted since then, optionally resetting the count. */
-int ozk_k3_replays(unsigned long long* count, int reset);
+ * rounding the C2 interval cannot decide. ozk_k3_replays counts per device
+ * (the handle's): the first call enables counting there; each call
+ * synchronises that device and returns the elements replayed on it since
+ * then (by any handle on the device), optionally resetting the count. */
+int ozk_k3_replays(ozk_handle h, unsigned long long* count, int reset);
 
 #ifdef __cplusplus
 }

@@ -149,7 +149,7 @@ def load() -> C.CDLL:
     L.ozk_crt_reduce.argtypes = [p, C.POINTER(OzkConfig), i64, p, p, p]
     L.ozk_unscale.argtypes = [p, i64, i64, p, i64, p, p, p, i64]
     L.ozk_profile_read.argtypes = [p, p, p, i32]
-    L.ozk_k3_replays.argtypes = [p, i32]
+    L.ozk_k3_replays.argtypes = [p, p, i32]
     _lib = L
     return L
 

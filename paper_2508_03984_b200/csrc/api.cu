@@ -1095,7 +1095,9 @@ int ozk_profile_read(ozk_handle h, double* ms, int64_t* calls, int reset) {
     return OZK_OK;
 }
 
-int ozk_k3_replays(unsigned long long* count, int reset) {
+int ozk_k3_replays(ozk_handle h, unsigned long long* count, int reset) {
+    if (!h) return OZK_INPUT_ERROR;
+    OZK_CUDA(cudaSetDevice(h->device));
     unsigned long long* d = k3_replay_counter(true);
     if (!d) return cuda_fail("k3 replay counter", cudaErrorMemoryAllocation);
     OZK_CUDA(cudaDeviceSynchronize());

@@ -493,15 +493,22 @@ bool integer_table(const double* v, int n, int max_bits, int* E_out, unsigned lo
 
 }  // namespace
 
-// device counter of replayed elements (tests / tools read it through
-// ozk_k3_replays); nullptr until first asked for
-static unsigned long long* g_replays = nullptr;
+// per-device counters of replayed elements (tests / tools read them through
+// ozk_k3_replays); nullptr until first asked for on that device
+namespace {
+constexpr int kMaxDevices = 64;
+unsigned long long* g_replays[kMaxDevices] = {};
+}  // namespace
 unsigned long long* k3_replay_counter(bool create) {
-    if (!g_replays && create) {
-        if (cudaMalloc(&g_replays, sizeof(unsigned long long)) != cudaSuccess) return nullptr;
-        cudaMemset(g_replays, 0, sizeof(unsigned long long));
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+    if (!g_replays[dev] && create) {
+        unsigned long long* p = nullptr;
+        if (cudaMalloc(&p, sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+        cudaMemset(p, 0, sizeof(unsigned long long));
+        g_replays[dev] = p;
     }
-    return g_replays;
+    return g_replays[dev];
 }
 
 // The tensor-core K3 for FP64 tables (see the header comment); returns false

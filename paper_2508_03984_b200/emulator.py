@@ -150,10 +150,10 @@ class Context:
         return {name: (ms[i], calls[i]) for i, name in enumerate(_lib.PROFILE_SLOTS)}
 
     def k3_replays(self, reset: bool = True) -> int:
-        """elements whose C2 the tensor-core K3 replayed sequentially since
-        counting began (the first call starts it)"""
+        """elements whose C2 the tensor-core K3 replayed sequentially on this
+        context's device since counting began there (the first call starts it)"""
         n = C.c_ulonglong(0)
-        _lib.check(self._lib.ozk_k3_replays(C.byref(n), int(reset)))
+        _lib.check(self._lib.ozk_k3_replays(self.handle, C.byref(n), int(reset)))
         return int(n.value)
 
     # ---- host (reference-facing) GEMM ----------------------------------------------
