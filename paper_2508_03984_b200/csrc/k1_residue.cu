@@ -33,6 +33,26 @@ __device__ __forceinline__ uint32_t bound_entry(double x, int e) {
     return static_cast<uint32_t>(__double2loint(__dadd_ru(v, 0x1.0p52))) & 0xffu;
 }
 
+// 8 consecutive values from a 32-byte aligned address (read-only path)
+__device__ __forceinline__ void load8(const double* p, double (&v)[8]) {
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                 : "l"(p));
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(v[4]), "=d"(v[5]), "=d"(v[6]), "=d"(v[7])
+                 : "l"(p + 4));
+}
+__device__ __forceinline__ void load8(const float* p, float (&v)[8]) {
+    asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(p));
+}
+__device__ __forceinline__ void load8(const int32_t* p, int (&v)[8]) {
+    asm volatile("ld.global.nc.v8.s32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "l"(p));
+}
+
 // Column-major rows x cols input -> N column-major int8 planes (ld bytes per
 // column, plane_stride bytes apart). ROW_EXP: the scale exponent is per row
 // (A: mu), else per column (B: nu). Each thread handles 8 consecutive rows of
@@ -52,12 +72,22 @@ __global__ void __launch_bounds__(128)
     T x[kBPerThread];
     int ex[ROW_EXP ? kBPerThread : 1];
     bool fast = true;
+    // whole, 32-byte aligned runs: 256-bit loads of the 8 elements (and of
+    // their 8 row exponents) instead of 8 + 8 scalar ones
+    T vin[kBPerThread];
+    int ein[kBPerThread];
+    const bool vec = active && i0 + kBPerThread <= k && (reinterpret_cast<uintptr_t>(col + i0) & 31) == 0 &&
+                     (!ROW_EXP || (reinterpret_cast<uintptr_t>(exps + i0) & 31) == 0);
+    if (vec) {
+        load8(col + i0, vin);
+        if constexpr (ROW_EXP) load8(exps + i0, ein);
+    }
 #pragma unroll
     for (int u = 0; u < kBPerThread; ++u) {
         const int64_t i = i0 + u;
         const bool ok = active && i < k;
-        const T v = ok ? col[i] : T(0);
-        const int eu = ROW_EXP ? (ok ? exps[i] : 0) : e;
+        const T v = vec ? vin[u] : (ok ? col[i] : T(0));
+        const int eu = ROW_EXP ? (vec ? ein[u] : (ok ? exps[i] : 0)) : e;
         if constexpr (ROW_EXP) ex[u] = eu;
         if constexpr (KIND == 0) {
             x[u] = trunc_scaled(v, eu);
