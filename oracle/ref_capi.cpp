@@ -138,6 +138,26 @@ int ref_dump_tables_csv(int n, int prec, char* buf, int buflen) {
 REF_GEMM(ref_gemm_f64, double)
 REF_GEMM(ref_gemm_f32, float)
 
+// the explicit-constants overloads (emulator.hpp:29-32): cfg.precision and the
+// table's precision chosen independently
+#define REF_GEMM_TBL(NAME, T)                                                                            \
+    int NAME(int64_t m, int64_t n, int64_t k, const T* a, const T* b, int n_moduli, int mode, int prec,    \
+             int table_prec, int64_t block_k, int threads, double* c) {                                   \
+        return guarded([&] {                                                                             \
+            EmuConfig cfg;                                                                               \
+            cfg.n_moduli = n_moduli;                                                                     \
+            cfg.mode = mode_of(mode);                                                                    \
+            cfg.precision = prec_of(prec);                                                               \
+            cfg.block_k = block_k;                                                                       \
+            cfg.threads = threads;                                                                       \
+            const CrtConstants& cs = build_constants(n_moduli, prec_of(table_prec));                     \
+            EmulationResult r = gemm_emulated(wrap(a, m, k), wrap(b, k, n), cfg, cs);                    \
+            unwrap(r.c, c);                                                                              \
+        });                                                                                              \
+    }
+REF_GEMM_TBL(ref_gemm_tbl_f64, double)
+REF_GEMM_TBL(ref_gemm_tbl_f32, float)
+
 #define REF_SCALE(NAME, T)                                                                               \
     int NAME(int64_t m, int64_t n, int64_t k, const T* a, const T* b, int n_moduli, int mode, int prec,    \
              int64_t block_k, int threads, double* mu, double* nu) {                                      \

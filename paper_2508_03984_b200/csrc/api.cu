@@ -154,8 +154,10 @@ int cuda_fail(const char* what, cudaError_t e) {
         if (st_ != OZK_OK) return st_; \
     } while (0)
 
-// entries of Abar*Bbar are <= 64 * 64 * k: int32 holds them up to k = 2^19
+// entries of Abar*Bbar are <= 64 * 64 * k (an Abar entry is ceil of a value in
+// (63, 64] at most): int32 holds them for k < 2^19 (at k = 2^19, 2^31 wraps)
 constexpr int64_t kBoundInt32K = int64_t(1) << 19;
+inline bool bound_needs_int64(int64_t k) { return k >= kBoundInt32K; }
 
 int ensure(Buf& b, size_t bytes) {
     if (bytes <= b.bytes && b.p) return OZK_OK;
@@ -222,7 +224,8 @@ int resolve(const ozk_config* cfg, ozk_constants& c) {
 // validate_inputs (emulator.cpp:12-23) minus the finite scan, which runs on the device
 int validate(const ozk_config* cfg, const ozk_constants& c, int64_t m, int64_t n, int64_t k, int64_t lda,
              int64_t ldb) {
-    if (c.precision == OZK_FP64 && cfg->a_type == OZK_R32F) {
+    // the configuration's precision (not the table's) decides, as in emulator.cpp:96-99
+    if (cfg->precision != OZK_FP32 && cfg->a_type == OZK_R32F) {
         set_error("gemm_emulated: FP32 inputs require cfg.precision == Fp32");
         return OZK_CONFIG_ERROR;
     }
@@ -302,7 +305,7 @@ int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c,
     J.nb = J.ma + m;
     J.rowmax = J.nb + n;
     J.colmax = J.rowmax + m;
-    J.wide_bound = cfg->mode == OZK_ACCURATE && k > kBoundInt32K;
+    J.wide_bound = cfg->mode == OZK_ACCURATE && bound_needs_int64(k);
     if (J.wide_bound) {
         OZK_TRY(ensure(h->wide, sizeof(unsigned long long) * (m + n)));
         J.rowmax64 = static_cast<unsigned long long*>(h->wide.p);
@@ -325,8 +328,10 @@ int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c,
 
 // FP32 precision on FP64 storage (emulator.cpp:84-91): the operands are rounded
 // into FP32 staging buffers (A whole, B by column range) before any stage reads them.
-bool rounds_inputs(const Job& J, const ozk_config* cfg) {
-    return J.c.precision == OZK_FP32 && cfg->a_type == OZK_R64F;
+// cfg.precision decides, as in the reference; the constant table (which may be
+// passed separately, of either precision) only supplies the arithmetic.
+bool rounds_inputs(const Job&, const ozk_config* cfg) {
+    return cfg->precision == OZK_FP32 && cfg->a_type == OZK_R64F;
 }
 
 int round_a(ozk_context* h, Job& J, const ozk_config* cfg) {
@@ -770,14 +775,16 @@ int region_products(ozk_context* h, Job& J, int64_t r0, int64_t mr, int64_t c0, 
 }
 
 // C[r0:r0+mr, c0:c0+nc] from the planes (K2 + K3), then its D2H on the copy stream
+// (the device staging C is m x n with pitch m; the caller's C has pitch ldc)
 int stream_region(ozk_context* h, Job& J, int64_t r0, int64_t mr, int64_t c0, int64_t nc, double alpha, int c_f32,
                   void* C_host, int64_t ldc, cudaEvent_t done) {
-    OZK_TRY(region_products(h, J, r0, mr, c0, nc, alpha, 0.0, h->host_c.p, ldc, c_f32));
+    const int64_t ldd = J.m;
+    OZK_TRY(region_products(h, J, r0, mr, c0, nc, alpha, 0.0, h->host_c.p, ldd, c_f32));
     const size_t cs = c_f32 ? 4 : 8;
-    const char* cdev = static_cast<const char*>(h->host_c.p) + cs * (c0 * ldc + r0);
+    const char* cdev = static_cast<const char*>(h->host_c.p) + cs * (c0 * ldd + r0);
     OZK_CUDA(cudaEventRecord(done, h->stream));
     OZK_CUDA(cudaStreamWaitEvent(h->d2h, done, 0));
-    OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(C_host) + cs * (c0 * ldc + r0), cs * ldc, cdev, cs * ldc, cs * mr,
+    OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(C_host) + cs * (c0 * ldc + r0), cs * ldc, cdev, cs * ldd, cs * mr,
                                nc, cudaMemcpyDeviceToHost, h->d2h));
     return OZK_OK;
 }
@@ -808,16 +815,16 @@ int gemm_host_streamed(ozk_context* h, Job& J, double alpha, const void* A, int6
     for (int s = 0; s < na || s < nb; ++s) {
         if (s < na) {
             const int64_t r0 = blocks_a[s].first, mr = blocks_a[s].second;
-            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(h->host_a.p) + es * r0, es * lda,
+            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(h->host_a.p) + es * r0, es * m,
                                        static_cast<const char*>(A) + es * r0, es * lda, es * mr, k,
                                        cudaMemcpyHostToDevice, h->h2d));
             OZK_CUDA(cudaEventRecord(ev_a(s), h->h2d));
         }
         if (s < nb) {
             const int64_t c0 = blocks_b[s].first, nc = blocks_b[s].second;
-            OZK_CUDA(cudaMemcpyAsync(static_cast<char*>(h->host_b.p) + es * ldb * c0,
-                                     static_cast<const char*>(B) + es * ldb * c0, es * ldb * nc,
-                                     cudaMemcpyHostToDevice, h->h2d));
+            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(h->host_b.p) + es * k * c0, es * k,
+                                       static_cast<const char*>(B) + es * ldb * c0, es * ldb, es * k, nc,
+                                       cudaMemcpyHostToDevice, h->h2d));
             OZK_CUDA(cudaEventRecord(ev_b(s), h->h2d));
         }
     }
@@ -871,12 +878,15 @@ int gemm_host(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int
     if (!h->d2h) OZK_CUDA(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
     const size_t es = cfg->a_type == OZK_R32F ? 4 : 8, cs = cfg->c_type == OZK_R32F ? 4 : 8;
     const bool ta = (cfg->flags & OZK_FLAG_TRANS_A) != 0, tb = (cfg->flags & OZK_FLAG_TRANS_B) != 0;
-    const size_t a_bytes = es * lda * (ta ? m : k);
-    OZK_TRY(ensure(h->host_a, a_bytes));
-    OZK_TRY(ensure(h->host_b, es * ldb * (tb ? k : n)));
-    OZK_TRY(ensure(h->host_c, cs * ldc * n));
+    // device staging is dense (pitch = stored rows); every transfer is a pitched
+    // copy of the stored rows only, so a caller's ld > rows (a submatrix view)
+    // is neither over-read nor, for C, written outside its rows
+    const int64_t rows_a = ta ? k : m, cols_a = ta ? m : k, rows_b = tb ? n : k;
+    OZK_TRY(ensure(h->host_a, es * rows_a * cols_a));
+    OZK_TRY(ensure(h->host_b, es * rows_b * (tb ? k : n)));
+    OZK_TRY(ensure(h->host_c, cs * m * n));
     Job J{};
-    OZK_TRY(setup(h, J, cfg, c, m, n, k, h->host_a.p, lda, h->host_b.p, ldb, true));
+    OZK_TRY(setup(h, J, cfg, c, m, n, k, h->host_a.p, rows_a, h->host_b.p, rows_b, true));
     const void* b_src = h->host_b.p;
     const int c_f32 = cfg->c_type == OZK_R32F;
     if (use_streamed(J, cfg, beta)) {
@@ -906,23 +916,24 @@ int gemm_host(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int
     OZK_CUDA(cudaEventRecord(evStart, h->stream));
     OZK_CUDA(cudaStreamWaitEvent(h->h2d, evStart, 0));
     OZK_CUDA(cudaStreamWaitEvent(h->d2h, evStart, 0));
-    OZK_CUDA(cudaMemcpyAsync(h->host_a.p, A, a_bytes, cudaMemcpyHostToDevice, h->h2d));
+    OZK_CUDA(cudaMemcpy2DAsync(h->host_a.p, es * rows_a, A, es * lda, es * rows_a, cols_a, cudaMemcpyHostToDevice,
+                               h->h2d));
     OZK_CUDA(cudaEventRecord(evA, h->h2d));
     for (int b = 0; b < nblk; ++b) {
         int64_t j0, nj;
         block(b, j0, nj);
-        if (tb)  // op(B) columns = rows j0.. of the stored n x k B: a pitched copy
-            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(h->host_b.p) + es * j0, es * ldb,
+        if (tb)  // op(B) columns = rows j0.. of the stored n x k B
+            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(h->host_b.p) + es * j0, es * rows_b,
                                        static_cast<const char*>(B) + es * j0, es * ldb, es * nj, k,
                                        cudaMemcpyHostToDevice, h->h2d));
         else
-            OZK_CUDA(cudaMemcpyAsync(static_cast<char*>(h->host_b.p) + es * ldb * j0,
-                                     static_cast<const char*>(B) + es * ldb * j0, es * ldb * nj,
-                                     cudaMemcpyHostToDevice, h->h2d));
+            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(h->host_b.p) + es * rows_b * j0, es * rows_b,
+                                       static_cast<const char*>(B) + es * ldb * j0, es * ldb, es * rows_b, nj,
+                                       cudaMemcpyHostToDevice, h->h2d));
         if (beta != 0.0)
-            OZK_CUDA(cudaMemcpyAsync(static_cast<char*>(h->host_c.p) + cs * ldc * j0,
-                                     static_cast<const char*>(C) + cs * ldc * j0, cs * ldc * nj,
-                                     cudaMemcpyHostToDevice, h->h2d));
+            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(h->host_c.p) + cs * m * j0, cs * m,
+                                       static_cast<const char*>(C) + cs * ldc * j0, cs * ldc, cs * m, nj,
+                                       cudaMemcpyHostToDevice, h->h2d));
         OZK_CUDA(cudaEventRecord(ev_b(b), h->h2d));
     }
     {
@@ -938,7 +949,7 @@ int gemm_host(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int
                 int64_t j0, nj;
                 block(b, j0, nj);
                 OZK_CUDA(cudaStreamWaitEvent(h->stream, ev_b(b), 0));
-                OZK_TRY(round_b(h, J, cfg, b_src, ldb, j0, nj));
+                OZK_TRY(round_b(h, J, cfg, b_src, rows_b, j0, nj));
                 StageTimer t(h, OZK_PROFILE_SCALE);
                 OZK_TRY(stage_cols(h, J, j0, nj));
             }
@@ -954,16 +965,16 @@ int gemm_host(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int
             block(b, j0, nj);
             if (J.mode == OZK_FAST) {
                 OZK_CUDA(cudaStreamWaitEvent(h->stream, ev_b(b), 0));
-                OZK_TRY(round_b(h, J, cfg, b_src, ldb, j0, nj));
+                OZK_TRY(round_b(h, J, cfg, b_src, rows_b, j0, nj));
                 StageTimer t(h, OZK_PROFILE_SCALE);
                 OZK_TRY(stage_cols(h, J, j0, nj));
             }
-            OZK_TRY(compute_block(h, J, j0, nj, alpha, beta, h->host_c.p, ldc, c_f32));
+            OZK_TRY(compute_block(h, J, j0, nj, alpha, beta, h->host_c.p, m, c_f32));
             OZK_CUDA(cudaEventRecord(ev_c(b), h->stream));
             OZK_CUDA(cudaStreamWaitEvent(h->d2h, ev_c(b), 0));
-            OZK_CUDA(cudaMemcpyAsync(static_cast<char*>(C) + cs * ldc * j0,
-                                     static_cast<const char*>(h->host_c.p) + cs * ldc * j0, cs * ldc * nj,
-                                     cudaMemcpyDeviceToHost, h->d2h));
+            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(C) + cs * ldc * j0, cs * ldc,
+                                       static_cast<const char*>(h->host_c.p) + cs * m * j0, cs * m, cs * m, nj,
+                                       cudaMemcpyDeviceToHost, h->d2h));
         }
     }
     OZK_CUDA(cudaStreamSynchronize(h->d2h));
@@ -1196,9 +1207,9 @@ int ozk_shard_begin(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, i
     ozk_constants c;
     OZK_TRY(resolve(cfg, c));
     OZK_TRY(validate(cfg, c, m, n, k, lda, ldb));
-    if (cfg->mode == OZK_ACCURATE && k > kBoundInt32K) {
+    if (cfg->mode == OZK_ACCURATE && bound_needs_int64(k)) {
         // ozk_shard_rowmax exchanges int32 maxima
-        set_error("column-shard accurate mode supports k <= 2^19");
+        set_error("column-shard accurate mode supports k < 2^19");
         return OZK_INPUT_ERROR;
     }
     OZK_CUDA(cudaSetDevice(h->device));
@@ -1255,7 +1266,7 @@ int ozk_shard_stream_begin(ozk_handle h, const ozk_config* cfg, int64_t m, int64
     OZK_TRY(resolve(cfg, c));
     OZK_TRY(validate(cfg, c, m, n, k, m, ldb));
     if (cfg->mode != OZK_FAST || (cfg->flags & (OZK_FLAG_TRANS_A | OZK_FLAG_TRANS_B)) ||
-        (c.precision == OZK_FP32 && cfg->a_type == OZK_R64F)) {
+        (cfg->precision == OZK_FP32 && cfg->a_type == OZK_R64F)) {
         // accurate-mode mu needs every column's bound first; rounding / transposed
         // operands keep the whole-A path (ozk_shard_begin)
         set_error("row-streamed shard: fast mode, untransposed operands stored in the compute precision only");

@@ -121,7 +121,9 @@ template <typename T>
 EmulationResult run(const Matrix<T>& a, const Matrix<T>& b, const EmuConfig& cfg, const CrtConstants& consts) {
     validate_host(a, b, cfg);
     ozk_constants oc = to_c(consts);
-    ozk_config c = ozk_default_config(consts.n(), mode_code(cfg.mode), prec_code(consts.precision));
+    // cfg.precision decides the FP32 rounding and the FP32-input check
+    // (emulator.cpp:84-99); the table supplies the arithmetic
+    ozk_config c = ozk_default_config(consts.n(), mode_code(cfg.mode), prec_code(cfg.precision));
     c.a_type = sizeof(T) == 4 ? OZK_R32F : OZK_R64F;
     c.c_type = OZK_R64F;
     c.block_k = cfg.block_k;

@@ -91,7 +91,9 @@ __global__ void __launch_bounds__(128)
         if constexpr (ROW_EXP) ex[u] = eu;
         if constexpr (KIND == 0) {
             x[u] = trunc_scaled(v, eu);
-            fast &= symmetric_residue_domain(static_cast<double>(x[u]), c.precision, c.n);
+            // the residue sequence follows the element type (residue.hpp:39-53 overloads
+            // rmod_fast on T), the tables may be of either precision
+            fast &= symmetric_residue_domain(static_cast<double>(x[u]), sizeof(T) == 4 ? OZK_FP32 : OZK_FP64, c.n);
         } else {
             x[u] = v;
         }

@@ -74,6 +74,7 @@ struct K2Params {
     int sync_every;        // mode 2: check every this many k-blocks
     unsigned int* done;    // mode 1: completed (cluster, tile) count
     unsigned int* progress;  // mode 2: issued k-blocks per cluster
+    unsigned long long sync_timeout_ns;  // a lockstep wait longer than this abandons the lockstep
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -173,6 +174,11 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
     unsigned int v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
@@ -350,14 +356,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t pol_b = (P.hints & 2) ? policy_evict_last()
                                              : ((P.hints & 8) ? policy_evict_first() : policy_evict_normal());
         const bool kstep = P.sync_mode == 2 && leader;
+        bool lockstep = P.sync_mode == 1 && leader;
         int lt = 0;
         for (int t = cluster_id; t < total; t += nclusters, ++lt) {
-            if (P.sync_mode == 1 && leader && lt >= 1 && lane == 0) {
+            if (lockstep && lt >= 1 && lane == 0) {
                 // tile lockstep: every cluster's producer must have issued its tile
                 // lt - 1. Counting producers (not MMA completion) lets this cluster
                 // keep its ring full while it waits, so the MMA pipe does not drain.
+                // The grid is capped at the co-resident cluster count, but other
+                // work (another stream, NCCL, MPS limits) can still hold SMs a
+                // cluster of this launch is waiting for: a wait longer than the
+                // timeout (many tile durations) drops the lockstep for the rest
+                // of this launch instead of deadlocking.
                 const unsigned int need = static_cast<unsigned int>(min(total, lt * nclusters));
-                while (ld_acquire(P.done) < need) __nanosleep(128);
+                const unsigned long long t0 = globaltimer_ns();
+                while (ld_acquire(P.done) < need) {
+                    __nanosleep(128);
+                    if (globaltimer_ns() - t0 > P.sync_timeout_ns) {
+                        lockstep = false;
+                        break;
+                    }
+                }
             }
             __syncwarp();
             int mod, tm, tn;
@@ -651,6 +670,7 @@ int launch_impl(const K2Launch& L, cudaStream_t s) {
     P.sync_window = env_int("OZK_K2_SYNC_WINDOW", 32);
     P.sync_every = env_int("OZK_K2_SYNC_EVERY", 8);
     if (P.sync_every < 1) P.sync_every = 1;
+    P.sync_timeout_ns = 1000ull * static_cast<unsigned long long>(env_int("OZK_K2_SYNC_TIMEOUT_US", 20000));
     P.done = L.sync_counter;
     P.progress = L.sync_counter ? L.sync_counter + 16 : nullptr;
     // the lockstep words start at zero (the handle clears its flag buffer once)
@@ -661,10 +681,12 @@ int launch_impl(const K2Launch& L, cudaStream_t s) {
     if (clusters < 1) clusters = 1;
 
     auto kern = residue_gemm_kernel<CG, KIND, A_MN, B_MN>;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<unsigned long long> attr_set{0};  // per instantiation and device
+    static std::atomic<int> resident[64];                // co-resident clusters per device
+    const int dev = current_device() & 63;
+    if (needs_setup(attr_set)) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-        attr_set = true;
+        mark_setup(attr_set);
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
@@ -678,6 +700,20 @@ int launch_impl(const K2Launch& L, cudaStream_t s) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // the persistent grid never exceeds the clusters the device can hold at once
+    // (the lockstep waits on every cluster of the launch)
+    int fit = resident[dev].load(std::memory_order_relaxed);
+    if (!fit) {
+        if (cudaOccupancyMaxActiveClusters(&fit, kern, &cfg) != cudaSuccess || fit < 1) {
+            cudaGetLastError();
+            fit = L.num_sms / CG;
+        }
+        resident[dev].store(fit, std::memory_order_relaxed);
+    }
+    if (clusters > fit) {
+        clusters = fit;
+        cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
+    }
     const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, P);
     if (e != cudaSuccess) {
         set_error(std::string("residue_gemm launch: ") + cudaGetErrorString(e));

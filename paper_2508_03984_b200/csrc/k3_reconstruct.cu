@@ -333,11 +333,11 @@ void launch_bulk_t(int num_sms, cudaStream_t s, const uint8_t* u, int64_t ldu, i
     constexpr int kBulkThreads = kConsumers + 32;  // + one producer warp
     auto kern = reconstruct_bulk_kernel<kF32Out, kPlain, kC1, kMaxMod, R, kConsumers, kStages>;
     const int smem = kStages * kMaxMod * kTile;
-    static bool attr = false;  // per instantiation
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};  // per instantiation and device
+    if (needs_setup(attr)) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        attr = true;
+        mark_setup(attr);
     }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBulkThreads, smem);

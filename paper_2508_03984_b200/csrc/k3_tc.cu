@@ -408,17 +408,19 @@ bool launch_t(const CUtensorMap& map, int num_sms, cudaStream_t s, int64_t m, in
     using Cf = TcCfg<P, S>;
     auto kern = reconstruct_tc_kernel<kF32Out, kPlain, kExact, P, S>;
     constexpr int smem = Cf::kSmem;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};  // per instantiation and device
+    static std::atomic<int> per_sm_dev[64];
+    const int dev = current_device() & 63;
+    if (needs_setup(attr)) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        attr = true;
+        mark_setup(attr);
     }
     // blocks per SM from the resources (the occupancy API reports 1 for
     // kernels that allocate TMEM): shared memory, registers, TMEM columns
-    static int per_sm = [&] {
-        int dev = 0, smem_sm = 0, regs_sm = 0;
-        cudaGetDevice(&dev);
+    int per_sm = per_sm_dev[dev].load(std::memory_order_relaxed);
+    if (!per_sm) per_sm = [&] {
+        int smem_sm = 0, regs_sm = 0;
         cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
         cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
         cudaFuncAttributes fa{};
@@ -426,7 +428,9 @@ bool launch_t(const CUtensorMap& map, int num_sms, cudaStream_t s, int64_t m, in
         const int by_smem = smem_sm / (smem + static_cast<int>(fa.sharedSizeBytes) + 1024);
         const int regs_warp = (fa.numRegs * 32 + 255) / 256 * 256;
         const int by_regs = regs_sm / (regs_warp * (kThreads / 32));
-        return std::min(std::min(by_smem, by_regs), 512 / kTmemCols);
+        const int v = std::min(std::min(by_smem, by_regs), 512 / kTmemCols);
+        per_sm_dev[dev].store(v < 1 ? -1 : v, std::memory_order_relaxed);
+        return v < 1 ? -1 : v;
     }();
     if (per_sm < 1) return false;
     const int64_t row_chunks = (m + kRows - 1) / kRows;

@@ -3,6 +3,7 @@
 // k3_reconstruct.cu). Not part of the public ABI.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <string>
 
@@ -34,6 +35,22 @@ struct DevConsts {
 };
 
 DevConsts to_dev(const ozk_constants& c);
+
+// Kernel attributes (dynamic shared memory opt-in, carveout) and launch
+// geometry are per device: a process may drive several GPUs (one handle per
+// device). `done` holds one bit per device ordinal; the attribute is set before
+// the bit, so a racing thread at worst sets it twice.
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+inline bool needs_setup(const std::atomic<unsigned long long>& done) {
+    return !(done.load(std::memory_order_acquire) & (1ull << (current_device() & 63)));
+}
+inline void mark_setup(std::atomic<unsigned long long>& done) {
+    done.fetch_or(1ull << (current_device() & 63), std::memory_order_release);
+}
 
 // Column pitch of the int8 planes: a multiple of 16 bytes (TMA global strides
 // must be 16-byte multiples). A planes use plane_ld(m), B planes plane_ld(k).

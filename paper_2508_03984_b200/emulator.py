@@ -164,17 +164,20 @@ class Context:
         passed as stored, e.g. a is k x m for trans_a; nothing is transposed)."""
         _validate_threads(a.T if trans_a else a, b.T if trans_b else b, cfg)
         dt = np.float32 if a.dtype == np.float32 else np.float64
-        a = np.asfortranarray(a, dtype=dt)
-        b = np.asfortranarray(b, dtype=dt)
+        # column-major views with a leading dimension > rows (e.g. big[:m, :])
+        # pass through as (pointer, ld), like a BLAS submatrix
+        a, lda = _host_colmajor(a, dt)
+        b, ldb = _host_colmajor(b, dt)
         m, k = (a.shape[1], a.shape[0]) if trans_a else a.shape
         n = b.shape[0] if trans_b else b.shape[1]
         out = np.zeros((m, n), dtype=c_dtype, order="F") if c is None else c
-        if not (out.flags.f_contiguous and out.shape == (m, n)):
-            raise InputError("c must be an m x n Fortran-ordered array")
+        ldc = _host_ld(out)
+        if ldc is None or out.shape != (m, n):
+            raise InputError("c must be an m x n column-major array (Fortran order, or a column-major view)")
         conf = _config(cfg, _lib.OZK_R32F if dt == np.float32 else _lib.OZK_R64F,
                        _lib.OZK_R32F if out.dtype == np.float32 else _lib.OZK_R64F, constants, trans_a, trans_b)
         _lib.check(self._lib.ozk_gemm_host(self.handle, C.byref(conf), m, n, k, float(alpha), a.ctypes.data,
-                                           a.shape[0], b.ctypes.data, b.shape[0], float(beta), out.ctypes.data, m))
+                                           lda, b.ctypes.data, ldb, float(beta), out.ctypes.data, ldc))
         return out
 
     def synchronize(self) -> None:
@@ -288,6 +291,29 @@ class Context:
         _lib.check(self._lib.ozk_stage_reconstruct(self.handle, C.byref(conf), m, n, U.data_ptr(), int(ldu),
                                                    mu_exp.data_ptr(), nu_exp.data_ptr(), float(alpha), float(beta),
                                                    C_out.data_ptr(), _colmajor_ld(C_out)))
+
+
+def _host_ld(x: np.ndarray):
+    """leading dimension of a column-major host matrix or view, else None"""
+    if x.ndim != 2:
+        return None
+    it = x.itemsize
+    if x.shape[1] <= 1 and (x.shape[0] <= 1 or x.strides[0] == it):
+        return max(x.shape[0], 1)
+    if x.strides[0] != it and x.shape[0] > 1:
+        return None
+    if x.strides[1] % it or x.strides[1] < it * x.shape[0]:
+        return None
+    return max(x.strides[1] // it, x.shape[0], 1)
+
+
+def _host_colmajor(x: np.ndarray, dt):
+    """(array, ld): x itself when it is a column-major matrix/view of dtype dt, else a Fortran copy"""
+    ld = _host_ld(x) if x.dtype == dt else None
+    if ld is None:
+        x = np.asfortranarray(x, dtype=dt)
+        ld = max(x.shape[0], 1)
+    return x, ld
 
 
 def _dtype_code(t) -> int:

@@ -267,6 +267,8 @@ class RefLib:
         L.ref_constants.argtypes = [C.c_int, C.c_int] + [_p] * 11
         for nm in ("ref_gemm_f64", "ref_gemm_f32"):
             getattr(L, nm).argtypes = [_i64, _i64, _i64, _p, _p, C.c_int, C.c_int, C.c_int, _i64, C.c_int, _p]
+        for nm in ("ref_gemm_tbl_f64", "ref_gemm_tbl_f32"):
+            getattr(L, nm).argtypes = [_i64, _i64, _i64, _p, _p, C.c_int, C.c_int, C.c_int, C.c_int, _i64, C.c_int, _p]
         for nm in ("ref_scale_f64", "ref_scale_f32"):
             getattr(L, nm).argtypes = [_i64, _i64, _i64, _p, _p, C.c_int, C.c_int, C.c_int, _i64, C.c_int, _p, _p]
         for nm in ("ref_residues_f64", "ref_residues_f32"):
@@ -327,6 +329,17 @@ class RefLib:
         c = np.zeros((m, n), np.float64, order="F")
         fn = self.lib.ref_gemm_f64 if in_prec == 0 else self.lib.ref_gemm_f32
         self._check(fn(m, n, k, _ptr(a), _ptr(b), n_moduli, mode, prec, block_k, threads, _ptr(c)))
+        return c
+
+    def gemm_tables(self, a, b, n_moduli, mode, prec, table_prec, block_k=1 << 17, threads=1):
+        """gemm_emulated(a, b, cfg, build_constants(n, table_prec)) with cfg.precision = prec
+        (emulator.hpp:29-32); a/b keep their dtype (float64 or float32)"""
+        fn = self.lib.ref_gemm_tbl_f32 if a.dtype == np.float32 else self.lib.ref_gemm_tbl_f64
+        a, b = _f(a, a.dtype), _f(b, b.dtype)
+        m, k = a.shape
+        n = b.shape[1]
+        c = np.zeros((m, n), np.float64, order="F")
+        self._check(fn(m, n, k, _ptr(a), _ptr(b), n_moduli, mode, prec, table_prec, block_k, threads, _ptr(c)))
         return c
 
     def scale(self, a, b, n_moduli, mode, prec=0, block_k=1 << 17, threads=1):

@@ -343,7 +343,7 @@ def test_long_k_blocked_path(oracle, k, mode):
         np.testing.assert_array_equal(_bits(got), _bits(want))
 
 
-@pytest.mark.parametrize("k", [(1 << 19) + 1000, (1 << 20) + 17])
+@pytest.mark.parametrize("k", [1 << 19, (1 << 19) + 1000, (1 << 20) + 17])
 def test_accurate_long_k_int64_bound(oracle, k):
     """accurate mode beyond k = 2^19: entries of the bound product Abar*Bbar reach
     64*64*k > 2^31, so it accumulates in int64 (scaling.cpp:118-148 keeps it in
@@ -366,6 +366,70 @@ def test_shard_accurate_long_k_rejected(ctx):
     B = _dev_colmajor(np.zeros((k, 2)))
     with pytest.raises(InputError):
         ctx.shard_begin(A, B, EmuConfig(n_moduli=8, mode=ScaleMode.Accurate))
+
+
+@pytest.mark.parametrize("mode", [ScaleMode.Fast, ScaleMode.Accurate])
+@pytest.mark.parametrize("m,n,k", [(70, 50, 90), (2100, 2060, 64)])
+def test_host_leading_dimensions(ctx, oracle, mode, m, n, k):
+    """ozk_gemm_host on BLAS submatrix views (lda > m, ldb > k, ldc > m): the
+    result equals the oracle and the rows of C past m are never written (the
+    second shape takes the streamed fast-mode pipeline)."""
+    a = gen_matrix(m, k, 0.5, 81)
+    b = gen_matrix(k, n, 0.5, 82)
+    A = np.full((m + 7, k), 7.5, order="F")
+    A[:m] = a
+    B = np.full((k + 5, n), -3.5, order="F")
+    B[:k] = b
+    Cbig = np.full((m + 3, n), 123.25, order="F")
+    ctx.gemm_host(A[:m], B[:k], EmuConfig(n_moduli=14, mode=mode), c=Cbig[:m])
+    np.testing.assert_array_equal(_bits(np.asfortranarray(Cbig[:m])), _bits(oracle.gemm(a, b, 14, int(mode))))
+    assert (Cbig[m:] == 123.25).all()
+
+
+@pytest.mark.parametrize("trans", [False, True])
+def test_host_leading_dimensions_alpha_beta(ctx, trans):
+    """the column pipeline (beta != 0, transposes) on submatrix views equals
+    the same call on dense copies, and leaves C's padding rows alone"""
+    m, n, k = 300, 260, 130
+    a = gen_matrix(m, k, 0.5, 83)
+    b = gen_matrix(k, n, 0.5, 84)
+    c0 = gen_matrix(m, n, 0.0, 85)
+    sa = np.asfortranarray(a.T) if trans else a  # stored operand
+    A = np.full((sa.shape[0] + 9, sa.shape[1]), 1.0, order="F")
+    A[:sa.shape[0]] = sa
+    B = np.full((k + 3, n), 2.0, order="F")
+    B[:k] = b
+    Cbig = np.full((m + 5, n), -1.0, order="F")
+    Cbig[:m] = c0
+    cfg = EmuConfig(n_moduli=14)
+    ctx.gemm_host(A[:sa.shape[0]], B[:k], cfg, alpha=1.5, beta=-0.5, c=Cbig[:m], trans_a=trans)
+    want = ctx.gemm_host(np.asfortranarray(sa), b, cfg, alpha=1.5, beta=-0.5, c=np.asfortranarray(c0.copy()),
+                         trans_a=trans)
+    np.testing.assert_array_equal(_bits(np.asfortranarray(Cbig[:m])), _bits(want))
+    assert (Cbig[m:] == -1.0).all()
+
+
+@pytest.mark.parametrize("in_dt,prec,table_prec", [(np.float64, Precision.Fp64, Precision.Fp32),
+                                                   (np.float64, Precision.Fp32, Precision.Fp64),
+                                                   (np.float32, Precision.Fp32, Precision.Fp64)])
+@pytest.mark.parametrize("mode", [ScaleMode.Fast, ScaleMode.Accurate])
+def test_config_precision_vs_table_precision(in_dt, prec, table_prec, mode):
+    """the explicit-constants overloads (emulator.hpp:29-32) with a table of the
+    other precision: cfg.precision decides the FP32 rounding and the FP32-input
+    check (emulator.cpp:84-99), the table the arithmetic; equal to the reference."""
+    from paper_2508_03984_b200 import build_constants
+    from _oracle import RefLib
+
+    if not RefLib.available():
+        pytest.skip("oracle/_ref not built")
+    ref = RefLib()
+    a = gen_matrix(90, 400, 1.0, 86).astype(in_dt)
+    b = gen_matrix(400, 70, 1.0, 87).astype(in_dt)
+    for N in (8, 10):
+        cs = build_constants(N, table_prec)
+        got = gemm_emulated(a, b, EmuConfig(n_moduli=N, mode=mode, precision=prec), constants=cs).c
+        want = ref.gemm_tables(a, b, N, int(mode), int(prec), int(table_prec))
+        np.testing.assert_array_equal(_bits(got), _bits(want))
 
 
 @pytest.mark.parametrize("m,n,k,prec,c32", [(2050, 2600, 77, Precision.Fp64, False),
