@@ -274,6 +274,29 @@ int ozk_profile_read(ozk_handle h, double* ms, int64_t* calls, int reset);
  * then (by any handle on the device), optionally resetting the count. */
 int ozk_k3_replays(ozk_handle h, unsigned long long* count, int reset);
 
+/* ---- device workspace (extension; no reference counterpart) ---------------
+ * The reference needs one modulus's int32 product live at a time
+ * (emulator.cpp:42-48). Here a call holds N int8 residue planes of A and of B
+ * and the N uint8 product residues U of C in handle-owned device buffers,
+ * reused across calls. When that workspace (about N bytes per element of A, B
+ * and C) exceeds the handle's limit, ozk_gemm / ozk_gemm_host run in panels:
+ * row panels of A and C times column panels of B and C, each panel's planes
+ * written into the same buffers, in the loop order (and panel shape) that
+ * re-derives the fewest residues. Results do not depend on the panelling
+ * (every stage after the O(m + n) exponents is row/column-local).
+ *   ozk_set_workspace_limit  bytes; 0 = automatic: the free device memory plus
+ *                            what the handle already holds, minus
+ *                            max(1 GiB, 10 % of the device) (env
+ *                            OZK_WORKSPACE_GB overrides the automatic value)
+ *   ozk_workspace_bytes      device bytes the handle holds now
+ *   ozk_last_plan            the last ozk_gemm / ozk_gemm_host plan: out[0] row
+ *                            panel height, out[1] column panel width, out[2]
+ *                            panels, out[3] operand residue passes beyond one
+ *                            per operand */
+int ozk_set_workspace_limit(ozk_handle h, int64_t bytes);
+int64_t ozk_workspace_bytes(ozk_handle h);
+int ozk_last_plan(ozk_handle h, int64_t out[4]);
+
 #ifdef __cplusplus
 }
 #endif

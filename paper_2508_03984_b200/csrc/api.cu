@@ -106,6 +106,16 @@ struct Job {
     int32_t *cnt_a, *cnt_b;  // last-block counters of the row-stat reductions (A side / B side)
     int8_t *pa, *pb;
     uint8_t* u;
+    bool need_products;
+};
+
+// a panel plan (make_plan): row panels of op(A)/C, column panels of op(B)/C
+struct Plan {
+    int64_t mr = 0, nc = 0;
+    bool col_outer = true;
+    int64_t panels = 1, extra_passes = 0;
+    size_t pa = 0, pb = 0, u = 0;
+    bool single = true;  // one panel: the whole problem (the two-stream K1 path)
 };
 }  // namespace
 
@@ -128,12 +138,17 @@ struct ozk_context {
     bool shard_open = false;
     ozk_config shard_cfg{};
     Job shard{};  // plain pointers into this handle's workspace
+    Plan shard_plan{};
     // the row-streamed shard (ozk_shard_stream_*): output and progress
     bool stream_open = false;
     double stream_alpha = 1.0, stream_beta = 0.0;
     void* stream_c = nullptr;
     int64_t stream_ldc = 0, stream_rows = 0;
     int stream_c_f32 = 0;
+    int64_t stream_ldu = 0;  // U pitch of the row-streamed shard's per-block products
+    // device workspace limit (0: automatic) and the last call's panel plan
+    int64_t ws_limit = 0;
+    int64_t last_plan[4] = {0, 0, 0, 0};
 };
 
 namespace {
@@ -284,11 +299,11 @@ int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c,
         J.cnt_a = static_cast<int32_t*>(h->counters.p);
         J.cnt_b = J.cnt_a + row_stat_groups(m) + 1;
     }
-    if (need_products) {
-        OZK_TRY(ensure(h->planes_a, static_cast<size_t>(N * J.pa_stride)));
-        OZK_TRY(ensure(h->planes_b, static_cast<size_t>(N * J.pb_stride)));
-        OZK_TRY(ensure(h->u, static_cast<size_t>(N * n * J.ldu)));
-    } else if (cfg->mode == OZK_ACCURATE) {  // the bound operands Abar/Bbar
+    (void)N;
+    // the residue planes and U are sized by the caller's panel plan
+    // (alloc_plan); without products only the accurate-mode bound operands
+    // Abar / Bbar (one plane each, whole problem) are needed here
+    if (!need_products && cfg->mode == OZK_ACCURATE) {
         OZK_TRY(ensure(h->planes_a, static_cast<size_t>(J.pa_stride)));
         OZK_TRY(ensure(h->planes_b, static_cast<size_t>(J.pb_stride)));
     }
@@ -314,6 +329,7 @@ int setup(ozk_context* h, Job& J, const ozk_config* cfg, const ozk_constants& c,
     J.pa = static_cast<int8_t*>(h->planes_a.p);
     J.pb = static_cast<int8_t*>(h->planes_b.p);
     J.u = static_cast<uint8_t*>(h->u.p);
+    J.need_products = need_products;
     J.a = A;
     J.b = B;
     J.lda = lda;
@@ -458,13 +474,11 @@ int stage_cols(ozk_context* h, Job& J, int64_t j0, int64_t nj, int part = 0) {
     OZK_TRY(check_launch(h, 1));
     if (J.mode == OZK_FAST) return OZK_OK;
     b_planes(h, J, j0, nj, J.nb, 1, J.pb, J.pb_stride);
-    if (J.wide_bound) {
-        OZK_CUDA(cudaMemsetAsync(J.colmax64 + j0, 0, sizeof(unsigned long long) * nj, h->stream));
-        OZK_TRY(ensure(h->cbar, sizeof(long long) * J.m * nj));
-    }
+    if (J.wide_bound) OZK_CUDA(cudaMemsetAsync(J.colmax64 + j0, 0, sizeof(unsigned long long) * nj, h->stream));
     OZK_TRY(check_launch(h, 2));
     if (part == 1) return OZK_OK;
 bound_gemm:
+    if (J.wide_bound) OZK_TRY(ensure(h->cbar, sizeof(long long) * J.m * nj));
     K2Launch L{};
     L.a_planes = J.pa;
     L.b_planes = bbar;
@@ -594,6 +608,217 @@ int scale_all(ozk_context* h, Job& J, const ozk_config* cfg) {
     return OZK_OK;
 }
 
+// ---- panel plan (bounded workspace) -------------------------------------------
+// The N residue planes of A, of B and the N uint8 product residues U take
+// about N bytes per element of A, B and C (60 GB each at 65536^2, N = 14). A
+// problem whose workspace exceeds the handle's limit runs in panels: row
+// panels of op(A)/C (mr rows) times column panels of op(B)/C (nc columns), the
+// planes of one A panel and one B panel and the U of one region live at a
+// time. With column panels outside, A's residues are derived once per column
+// panel (none extra when one row panel holds all of A), and vice versa; the
+// plan takes the shape and order with the fewest extra residue passes that
+// fits. Results do not depend on it: after the O(m + n) exponents every stage
+// is row/column-local.
+
+// one plane of an op(A) row panel / op(B) column panel, in K2's operand layouts
+int64_t a_panel_ld(const Job& J, int64_t mr) { return J.ta ? plane_ld(J.k) : plane_ld(mr); }
+int64_t a_panel_plane(const Job& J, int64_t mr) { return J.ta ? mr * a_panel_ld(J, mr) : J.k * a_panel_ld(J, mr); }
+int64_t b_panel_ld(const Job& J, int64_t nc) { return J.tb ? plane_ld(nc) : plane_ld(J.k); }
+int64_t b_panel_plane(const Job& J, int64_t nc) { return J.tb ? J.k * b_panel_ld(J, nc) : nc * b_panel_ld(J, nc); }
+
+int64_t env_workspace_limit() {
+    const char* e = std::getenv("OZK_WORKSPACE_GB");
+    return e && *e ? static_cast<int64_t>(std::atof(e) * 1e9) : 0;
+}
+
+// bytes the plan may use for planes_a + planes_b + u
+int64_t workspace_limit(ozk_context* h) {
+    if (h->ws_limit > 0) return h->ws_limit;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
+        return INT64_MAX;
+    }
+    const int64_t held = static_cast<int64_t>(h->planes_a.bytes + h->planes_b.bytes + h->u.bytes);
+    const int64_t reserve = std::max<int64_t>(int64_t(1) << 30, static_cast<int64_t>(total_b / 10));
+    int64_t lim = static_cast<int64_t>(free_b) + held - reserve;
+    const int64_t env = env_workspace_limit();
+    if (env > 0) lim = env;
+    return lim;
+}
+
+std::vector<int64_t> panel_candidates(int64_t x) {
+    std::vector<int64_t> v{x};
+    for (int s = 1; s < 40; ++s) {
+        int64_t c = (x + (int64_t(1) << s) - 1) >> s;
+        c = (c + 255) / 256 * 256;  // whole 256-wide GEMM tiles
+        if (c >= v.back()) continue;
+        v.push_back(c);
+        if (c <= 256) break;
+    }
+    return v;
+}
+
+Plan make_plan(ozk_context* h, const Job& J, int64_t extra_bytes = 0) {
+    const int N = J.c.n_moduli;
+    const bool acc = J.mode == OZK_ACCURATE;
+    const int64_t es = J.in_f32 ? 4 : 8;
+    const int64_t limit = workspace_limit(h) - extra_bytes;
+    const double pass_a = double(es + N) * J.m * J.k, pass_b = double(es + N) * J.k * J.n;
+    const double region_cost = 256e6;  // ~40 us of HBM per region (launches, partial last waves)
+    Plan best;
+    double best_cost = 0;
+    bool found = false;
+    Plan smallest;
+    for (int64_t mr : panel_candidates(J.m)) {
+        for (int64_t nc : panel_candidates(J.n)) {
+            Plan P;
+            P.mr = mr;
+            P.nc = nc;
+            P.pa = static_cast<size_t>(std::max<int64_t>(N * a_panel_plane(J, mr), acc ? J.pa_stride : 0));
+            P.pb = static_cast<size_t>(std::max<int64_t>(N * b_panel_plane(J, nc), acc ? J.pb_stride : 0));
+            P.u = static_cast<size_t>(N * nc * u_ld(mr));
+            const int64_t I = (J.m + mr - 1) / mr, Jn = (J.n + nc - 1) / nc;
+            P.panels = I * Jn;
+            P.single = I == 1 && Jn == 1;
+            const double col = I > 1 ? double(Jn - 1) * pass_a : 0.0;
+            const double row = Jn > 1 ? double(I - 1) * pass_b : 0.0;
+            P.col_outer = col <= row;
+            P.extra_passes = P.col_outer ? (I > 1 ? Jn - 1 : 0) : (Jn > 1 ? I - 1 : 0);
+            smallest = P;  // candidates shrink: the last one is the smallest
+            if (static_cast<int64_t>(P.pa + P.pb + P.u) > limit) continue;
+            const double cost = std::min(col, row) + region_cost * double(P.panels);
+            if (!found || cost < best_cost) {
+                best = P;
+                best_cost = cost;
+                found = true;
+            }
+        }
+    }
+    return found ? best : smallest;
+}
+
+int alloc_plan(ozk_context* h, Job& J, const Plan& P) {
+    OZK_TRY(ensure(h->planes_a, P.pa));
+    OZK_TRY(ensure(h->planes_b, P.pb));
+    OZK_TRY(ensure(h->u, P.u));
+    J.pa = static_cast<int8_t*>(h->planes_a.p);
+    J.pb = static_cast<int8_t*>(h->planes_b.p);
+    J.u = static_cast<uint8_t*>(h->u.p);
+    h->last_plan[0] = P.mr;
+    h->last_plan[1] = P.nc;
+    h->last_plan[2] = P.panels;
+    h->last_plan[3] = P.extra_passes;
+    return OZK_OK;
+}
+
+// residue planes of op(A)'s rows [r0, r0+mr) at pa (panel layout, offset 0)
+int a_panel_residues(ozk_context* h, Job& J, int64_t r0, int64_t mr, int8_t* pa) {
+    const int64_t es = J.in_f32 ? 4 : 8;
+    const int64_t ld = a_panel_ld(J, mr), stride = a_panel_plane(J, mr);
+    if (J.ta)  // K-major: columns r0.. of the stored k x m A^T
+        launch_b_planes(static_cast<const char*>(J.a) + es * r0 * J.lda, J.in_f32, J.k, mr, J.lda, J.mu + r0, J.dc, 0,
+                        pa, ld, stride, h->stream);
+    else
+        launch_a_planes(static_cast<const char*>(J.a) + es * r0, J.in_f32, mr, J.k, J.lda, J.mu + r0, J.dc, 0, pa,
+                        ld, stride, h->stream);
+    return check_launch(h, 1);
+}
+
+// residue planes of op(B)'s columns [c0, c0+nc) at pb (panel layout, offset 0)
+int b_panel_residues(ozk_context* h, Job& J, int64_t c0, int64_t nc, int8_t* pb) {
+    const int64_t ld = b_panel_ld(J, nc), stride = b_panel_plane(J, nc);
+    if (J.tb)  // MN-major: rows c0.. of the stored n x k B^T
+        launch_a_planes(b_block(J, c0), J.in_f32, nc, J.k, J.ldb, J.nu + c0, J.dc, 0, pb, ld, stride, h->stream);
+    else
+        launch_b_planes(b_block(J, c0), J.in_f32, J.k, nc, J.ldb, J.nu + c0, J.dc, 0, pb, ld, stride, h->stream);
+    return check_launch(h, 1);
+}
+
+// C[r0:r0+mr, c0:c0+nc] from an A panel and a B panel: K2 into U, then K3
+int panel_region(ozk_context* h, Job& J, int64_t r0, int64_t mr, int64_t c0, int64_t nc, double alpha, double beta,
+                 void* C, int64_t ldc, int c_f32) {
+    const int64_t ldu = u_ld(mr), ustride = nc * ldu;
+    {
+        StageTimer t(h, OZK_PROFILE_PRODUCTS);
+        K2Launch L{};
+        L.a_planes = J.pa;
+        L.b_planes = J.pb;
+        L.m = mr;
+        L.n = nc;
+        L.k = J.k;
+        L.lda = a_panel_ld(J, mr);
+        L.ld = b_panel_ld(J, nc);
+        L.a_mn = !J.ta;
+        L.b_mn = J.tb;
+        L.a_stride = a_panel_plane(J, mr);
+        L.b_stride = b_panel_plane(J, nc);
+        L.n_mod = J.c.n_moduli;
+        L.kind = K2_U8;
+        L.out = J.u;
+        L.ldo = ldu;
+        L.out_stride = ustride;
+        L.c = &J.dc;
+        L.num_sms = h->num_sms;
+        L.sync_counter = reinterpret_cast<unsigned int*>(J.flags + 4);
+        OZK_TRY(launch_k2(L, h->stream));
+        OZK_TRY(check_launch(h, 1));
+    }
+    const size_t cs = c_f32 ? 4 : 8;
+    StageTimer t(h, OZK_PROFILE_RECONSTRUCT);
+    launch_reconstruct(J.u, ldu, ustride, mr, nc, J.mu + r0, J.nu + c0, J.dc, alpha, beta,
+                       static_cast<char*>(C) + cs * (c0 * ldc + r0), ldc, c_f32, h->stream);
+    return check_launch(h, 1);
+}
+
+// every panel once the exponents are known (on the handle's stream)
+int run_panels(ozk_context* h, Job& J, const Plan& P, double alpha, double beta, void* C, int64_t ldc, int c_f32) {
+    const int64_t I = (J.m + P.mr - 1) / P.mr, Jn = (J.n + P.nc - 1) / P.nc;
+    auto a_res = [&](int64_t r0, int64_t mr) {
+        StageTimer t(h, OZK_PROFILE_RESIDUES);
+        return a_panel_residues(h, J, r0, mr, J.pa);
+    };
+    auto b_res = [&](int64_t c0, int64_t nc) {
+        StageTimer t(h, OZK_PROFILE_RESIDUES);
+        return b_panel_residues(h, J, c0, nc, J.pb);
+    };
+    if (P.col_outer) {
+        for (int64_t jb = 0; jb < Jn; ++jb) {
+            const int64_t c0 = jb * P.nc, nc = std::min(P.nc, J.n - c0);
+            OZK_TRY(b_res(c0, nc));
+            for (int64_t ib = 0; ib < I; ++ib) {
+                const int64_t r0 = ib * P.mr, mr = std::min(P.mr, J.m - r0);
+                if (I > 1 || jb == 0) OZK_TRY(a_res(r0, mr));
+                OZK_TRY(panel_region(h, J, r0, mr, c0, nc, alpha, beta, C, ldc, c_f32));
+            }
+        }
+    } else {
+        for (int64_t ib = 0; ib < I; ++ib) {
+            const int64_t r0 = ib * P.mr, mr = std::min(P.mr, J.m - r0);
+            OZK_TRY(a_res(r0, mr));
+            for (int64_t jb = 0; jb < Jn; ++jb) {
+                const int64_t c0 = jb * P.nc, nc = std::min(P.nc, J.n - c0);
+                if (Jn > 1 || ib == 0) OZK_TRY(b_res(c0, nc));
+                OZK_TRY(panel_region(h, J, r0, mr, c0, nc, alpha, beta, C, ldc, c_f32));
+            }
+        }
+    }
+    return OZK_OK;
+}
+
+// accurate mode: the bound GEMM Abar * Bbar (row maxima accumulate across
+// column blocks; the int64 product of k >= 2^19 is formed per block of at
+// most ~2 GB) and the budgets
+int bound_and_budget(ozk_context* h, Job& J) {
+    StageTimer t(h, OZK_PROFILE_SCALE);
+    int64_t nb = J.n;
+    if (J.wide_bound) nb = std::min<int64_t>(J.n, std::max<int64_t>(256, ((int64_t(1) << 31) / (8 * J.m)) / 256 * 256));
+    for (int64_t j0 = 0; j0 < J.n; j0 += nb) OZK_TRY(stage_cols(h, J, j0, std::min(nb, J.n - j0), 2));
+    return stage_budget(h, J);
+}
+
+int single_panel(ozk_context* h, Job& J, double alpha, double beta, void* C, int64_t ldc, int c_f32);
+
 int gemm_device(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int64_t m, int64_t n, int64_t k,
                 double alpha, const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C,
                 int64_t ldc) {
@@ -605,6 +830,9 @@ int gemm_device(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, i
     OZK_CUDA(cudaSetDevice(h->device));
     Job J{};
     OZK_TRY(setup(h, J, cfg, c, m, n, k, A, lda, B, ldb, true));
+    const int64_t f32_bytes = rounds_inputs(J, cfg) ? 4 * (m * k + k * n) : 0;
+    const Plan P = make_plan(h, J, f32_bytes);
+    OZK_TRY(alloc_plan(h, J, P));
     const int c_f32 = cfg->c_type == OZK_R32F;
     const bool fast = J.mode == OZK_FAST;
     {
@@ -619,7 +847,7 @@ int gemm_device(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, i
             OZK_TRY(round_a(h, J, cfg));
             OZK_TRY(stage_rows(h, J));
         }
-        if (fast) {
+        if (fast && P.single) {
             StageTimer t(h, OZK_PROFILE_RESIDUES);
             OZK_TRY(stage_row_residues(h, J, J.mu, J.pa));
         }
@@ -630,19 +858,30 @@ int gemm_device(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, i
                 OZK_TRY(round_b(h, J, cfg, J.b, J.ldb, 0, n));
                 OZK_TRY(stage_cols(h, J, 0, n, fast ? 0 : 1));
             }
-            if (fast) {
+            if (fast && P.single) {
                 StageTimer t(h, OZK_PROFILE_RESIDUES);
                 OZK_TRY(stage_col_residues(h, J, 0, n, J.nu, J.pb, J.pb_stride));
             }
             OZK_CUDA(cudaEventRecord(h->ev_join, h->stream));
         }
         OZK_CUDA(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
-        if (!fast) {  // the bound GEMM needs both bound operands, mu and nu need its maxima
-            {
-                StageTimer t(h, OZK_PROFILE_SCALE);
-                OZK_TRY(stage_cols(h, J, 0, n, 2));
-                OZK_TRY(stage_budget(h, J));
-            }
+        // the bound GEMM needs both bound operands, mu and nu need its maxima
+        if (!fast) OZK_TRY(bound_and_budget(h, J));
+        if (!P.single) {
+            OZK_TRY(run_panels(h, J, P, alpha, beta, C, ldc, c_f32));
+        } else {
+            OZK_TRY(single_panel(h, J, alpha, beta, C, ldc, c_f32));
+        }
+    }
+    return finish_check(h, J, h->stream);
+}
+
+// the whole problem as one panel (the residues of fast mode are already issued
+// on the two K1 streams): residues (accurate mode), K2, K3
+int single_panel(ozk_context* h, Job& J, double alpha, double beta, void* C, int64_t ldc, int c_f32) {
+    const int64_t n = J.n;
+    {
+        if (J.mode != OZK_FAST) {
             // both residue passes at once again (A on this stream, B on the side stream)
             OZK_CUDA(cudaEventRecord(h->ev_fork, h->stream));
             OZK_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
@@ -666,7 +905,7 @@ int gemm_device(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, i
         StageTimer t(h, OZK_PROFILE_RECONSTRUCT);
         OZK_TRY(stage_reconstruct(h, J, 0, n, J.u, J.ldu, J.n * J.ldu, J.mu, J.nu, alpha, beta, C, ldc, c_f32));
     }
-    return finish_check(h, J, h->stream);
+    return OZK_OK;
 }
 
 int64_t host_block_cols(int64_t n) {
@@ -724,14 +963,19 @@ bool use_streamed(const Job& J, const ozk_config* cfg, double beta) {
 
 // rows [r0, r0+mr) of A, stored as an mr x k column-major block at `a` with
 // leading dimension lda: stats, mu, residue planes (fast mode: all row-local)
-int rows_block(ozk_context* h, Job& J, int64_t r0, int64_t mr, const void* a, int64_t lda) {
+int row_block_stats(ozk_context* h, Job& J, int64_t r0, int64_t mr, const void* a, int64_t lda) {
     int splits = row_stats_splits(mr, J.k);
     const int64_t cap = J.splits * J.m / mr;  // the [split][rows] partials live in J.amax / J.asum
     if (splits > cap) splits = static_cast<int>(cap < 1 ? 1 : cap);
     launch_row_stats(a, J.in_f32, mr, J.k, lda, splits, J.amax, J.asum, J.flags, J.cnt_a,
                      line_final(J, J.mu + r0, nullptr, a, 1, lda), h->stream);
+    return check_launch(h, 1);
+}
+
+int rows_block(ozk_context* h, Job& J, int64_t r0, int64_t mr, const void* a, int64_t lda) {
+    OZK_TRY(row_block_stats(h, J, r0, mr, a, lda));
     launch_a_planes(a, J.in_f32, mr, J.k, lda, J.mu + r0, J.dc, 0, J.pa + r0, J.lda_p, J.pa_stride, h->stream);
-    return check_launch(h, 2);
+    return check_launch(h, 1);
 }
 
 int stream_a_block(ozk_context* h, Job& J, int64_t r0, int64_t mr) {
@@ -887,6 +1131,24 @@ int gemm_host(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int
     OZK_TRY(ensure(h->host_c, cs * m * n));
     Job J{};
     OZK_TRY(setup(h, J, cfg, c, m, n, k, h->host_a.p, rows_a, h->host_b.p, rows_b, true));
+    const Plan P = make_plan(h, J, rounds_inputs(J, cfg) ? 4 * (m * k + k * n) : 0);
+    if (!P.single) {
+        // too large for one panel: the operands go to the device whole, the
+        // panelled device call runs, C comes back (no copy/compute overlap)
+        const int64_t cols_b = tb ? k : n;
+        OZK_CUDA(cudaMemcpy2DAsync(h->host_a.p, es * rows_a, A, es * lda, es * rows_a, cols_a, cudaMemcpyHostToDevice,
+                                   h->stream));
+        OZK_CUDA(cudaMemcpy2DAsync(h->host_b.p, es * rows_b, B, es * ldb, es * rows_b, cols_b, cudaMemcpyHostToDevice,
+                                   h->stream));
+        if (beta != 0.0)
+            OZK_CUDA(cudaMemcpy2DAsync(h->host_c.p, cs * m, C, cs * ldc, cs * m, n, cudaMemcpyHostToDevice, h->stream));
+        OZK_TRY(gemm_device(h, cfg, c, m, n, k, alpha, h->host_a.p, rows_a, h->host_b.p, rows_b, beta, h->host_c.p,
+                            m));
+        OZK_CUDA(cudaMemcpy2DAsync(C, cs * ldc, h->host_c.p, cs * m, cs * m, n, cudaMemcpyDeviceToHost, h->stream));
+        OZK_CUDA(cudaStreamSynchronize(h->stream));
+        return OZK_OK;
+    }
+    OZK_TRY(alloc_plan(h, J, P));
     const void* b_src = h->host_b.p;
     const int c_f32 = cfg->c_type == OZK_R32F;
     if (use_streamed(J, cfg, beta)) {
@@ -1121,6 +1383,27 @@ int ozk_k3_replays(ozk_handle h, unsigned long long* count, int reset) {
 
 int64_t ozk_plane_ld(int64_t k) { return plane_ld(k); }
 
+int ozk_set_workspace_limit(ozk_handle h, int64_t bytes) {
+    if (!h || bytes < 0) return OZK_INPUT_ERROR;
+    h->ws_limit = bytes;
+    return OZK_OK;
+}
+
+int64_t ozk_workspace_bytes(ozk_handle h) {
+    if (!h) return 0;
+    int64_t total = 0;
+    for (const Buf* b : {&h->wide, &h->cbar, &h->counters, &h->planes_a, &h->planes_b, &h->u, &h->stats, &h->ints,
+                         &h->flags, &h->f32a, &h->f32b, &h->host_a, &h->host_b, &h->host_c})
+        total += static_cast<int64_t>(b->bytes);
+    return total;
+}
+
+int ozk_last_plan(ozk_handle h, int64_t out[4]) {
+    if (!h || !out) return OZK_INPUT_ERROR;
+    for (int i = 0; i < 4; ++i) out[i] = h->last_plan[i];
+    return OZK_OK;
+}
+
 int ozk_sync(ozk_handle h) {
     if (!h) return OZK_INPUT_ERROR;
     OZK_CUDA(cudaSetDevice(h->device));
@@ -1216,6 +1499,8 @@ int ozk_shard_begin(ozk_handle h, const ozk_config* cfg, int64_t m, int64_t n, i
     Job& J = h->shard;
     J = Job{};
     OZK_TRY(setup(h, J, cfg, c, m, n, k, A, lda, B, ldb, true));
+    h->shard_plan = make_plan(h, J, rounds_inputs(J, cfg) ? 4 * (m * k + k * n) : 0);
+    OZK_TRY(alloc_plan(h, J, h->shard_plan));
     h->shard_cfg = *cfg;
     h->shard_cfg.constants = nullptr;  // resolved into J.c
     {
@@ -1251,11 +1536,16 @@ int ozk_shard_end(ozk_handle h, double alpha, double beta, void* C, int64_t ldc)
         StageTimer t(h, OZK_PROFILE_SCALE);
         OZK_TRY(stage_budget(h, J));
     }
+    const int c_f32 = h->shard_cfg.c_type == OZK_R32F;
+    if (!h->shard_plan.single) {
+        OZK_TRY(run_panels(h, J, h->shard_plan, alpha, beta, C, ldc, c_f32));
+        return finish_check(h, J, h->stream);
+    }
     {
         StageTimer t(h, OZK_PROFILE_RESIDUES);
         OZK_TRY(stage_row_residues(h, J, J.mu, J.pa));
     }
-    OZK_TRY(compute_block(h, J, 0, J.n, alpha, beta, C, ldc, h->shard_cfg.c_type == OZK_R32F));
+    OZK_TRY(compute_block(h, J, 0, J.n, alpha, beta, C, ldc, c_f32));
     return finish_check(h, J, h->stream);
 }
 
@@ -1280,6 +1570,10 @@ int ozk_shard_stream_begin(ozk_handle h, const ozk_config* cfg, int64_t m, int64
     Job& J = h->shard;
     J = Job{};
     OZK_TRY(setup(h, J, cfg, c, m, n, k, nullptr, m, B, ldb, true));
+    // the shard's B planes live for the whole call; A's planes and U are per
+    // row block (sized, and reused, in ozk_shard_stream_rows)
+    OZK_TRY(ensure(h->planes_b, static_cast<size_t>(c.n_moduli * J.pb_stride)));
+    J.pb = static_cast<int8_t*>(h->planes_b.p);
     h->shard_cfg = *cfg;
     h->shard_cfg.constants = nullptr;
     h->stream_alpha = alpha;
@@ -1311,13 +1605,26 @@ int ozk_shard_stream_rows(ozk_handle h, int64_t r0, int64_t mr, const void* A_ro
         return OZK_INPUT_ERROR;
     }
     OZK_CUDA(cudaSetDevice(h->device));
+    // this block's planes and U at offset 0 of buffers sized for the block: the
+    // blocks run in stream order, so one buffer of each serves them all
+    const int N = J.c.n_moduli;
+    OZK_TRY(ensure(h->planes_a, static_cast<size_t>(N * a_panel_plane(J, mr))));
+    OZK_TRY(ensure(h->u, static_cast<size_t>(N * J.n * u_ld(mr))));
+    J.pa = static_cast<int8_t*>(h->planes_a.p);
+    J.u = static_cast<uint8_t*>(h->u.p);
     {
         StageTimer t(h, OZK_PROFILE_SCALE);
-        OZK_TRY(rows_block(h, J, r0, mr, A_rows, lda_rows));
+        OZK_TRY(row_block_stats(h, J, r0, mr, A_rows, lda_rows));
+    }
+    {
+        StageTimer t(h, OZK_PROFILE_RESIDUES);
+        launch_a_planes(A_rows, J.in_f32, mr, J.k, lda_rows, J.mu + r0, J.dc, 0, J.pa, a_panel_ld(J, mr),
+                        a_panel_plane(J, mr), h->stream);
+        OZK_TRY(check_launch(h, 1));
     }
     h->stream_rows += mr;
-    return region_products(h, J, r0, mr, 0, J.n, h->stream_alpha, h->stream_beta, h->stream_c, h->stream_ldc,
-                           h->stream_c_f32);
+    return panel_region(h, J, r0, mr, 0, J.n, h->stream_alpha, h->stream_beta, h->stream_c, h->stream_ldc,
+                        h->stream_c_f32);
 }
 
 int ozk_shard_stream_end(ozk_handle h) {

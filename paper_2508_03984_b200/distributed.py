@@ -16,13 +16,17 @@ block's broadcast lands, and the broadcast of A overlaps the residue GEMMs of
 the blocks before it (engine calls shard_stream_begin / _rows / _end, backed
 by ozk_shard_stream_*). Blocks travel packed (mr x k, contiguous) because a
 row block of a column-major A is strided; the source packs them on a side
-stream and computes on its own A directly.
+stream and computes on its own A directly. A ring of three pack buffers bounds
+the copies of A in flight, so per-rank memory is A (on the source), this
+rank's B and C blocks, its B residue planes and O(row_block x k) more.
 
 ``engine`` is anything with shard_begin(A, B_local, cfg), shard_rowmax() ->
 tensor and shard_end(C_local, alpha, beta): the GPU ``Context`` here, or the
 CPU stand-in the gloo tests use to exercise exactly this exchange logic.
 """
 from __future__ import annotations
+
+import contextlib
 
 import torch
 import torch.distributed as dist
@@ -82,7 +86,8 @@ def _storage(t: torch.Tensor) -> torch.Tensor:
     raise ValueError("A must be a dense column-major (or row-major) matrix")
 
 
-def _gemm_streamed(engine, A, B_local, cfg, C_local, alpha, beta, group, src, broadcast, row_block):
+def _gemm_streamed(engine, A, B_local, cfg, C_local, alpha, beta, group, src, broadcast, row_block,
+                   ring: int = 3):
     m, k = A.shape
     blocks = row_blocks(m, row_block)
     engine.shard_stream_begin(m, k, B_local, cfg, C_local, alpha, beta)
@@ -92,32 +97,48 @@ def _gemm_streamed(engine, A, B_local, cfg, C_local, alpha, beta, group, src, br
         engine.shard_stream_end()
         return
     is_src = dist.get_rank() == src
-    # packed (mr x k column-major) block buffers; every broadcast is issued up
-    # front, so the comm stream runs ahead of the compute that waits on it
-    packs = [A.new_empty((k, mr)).t() for _, mr in blocks]
-    works = []
-    side = None
-    if A.is_cuda and is_src:
-        side = torch.cuda.Stream(device=A.device)
-        side.wait_stream(torch.cuda.current_stream(A.device))
-    for (r0, mr), pack in zip(blocks, packs):
-        if is_src:
-            if side is not None:
-                with torch.cuda.stream(side):
-                    pack.copy_(A[r0:r0 + mr])
-                    works.append(dist.broadcast(_storage(pack), src=src, group=group, async_op=True))
-            else:
-                pack.copy_(A[r0:r0 + mr])
-                works.append(dist.broadcast(_storage(pack), src=src, group=group, async_op=True))
-        else:
-            works.append(dist.broadcast(_storage(pack), src=src, group=group, async_op=True))
-    for (r0, mr), pack, work in zip(blocks, packs, works):
-        if is_src:
-            engine.shard_stream_rows(r0, A[r0:r0 + mr])  # the root's own rows need no wait
-        else:
-            work.wait()  # the compute stream waits for this block only
-            engine.shard_stream_rows(r0, pack)
-    engine.shard_stream_end()
+    # A ring of `ring` packed block buffers (mr x k column-major, contiguous: a
+    # row block of a column-major A is strided): at most `ring` blocks of A are
+    # in flight, whatever m is (the whole of A never exists twice on a rank).
+    cap = max(mr for _, mr in blocks)
+    slots = [A.new_empty((k, cap)) for _ in range(min(ring, len(blocks)))]
+
+    def pack_of(i):  # block i's (mr x k) column-major view into its slot
+        mr = blocks[i][1]
+        return slots[i % len(slots)].view(-1)[:k * mr].view(k, mr).t()
+
+    works = [None] * len(blocks)
     if is_src:
-        for work in works:  # the packs stay alive until their sends are done
-            work.wait()
+        # the root packs block i into its slot once the send of block i - ring
+        # from that slot is done, then sends it; all of this is issued up front
+        # on a side stream (CUDA) and the root computes on its own A meanwhile
+        side = None
+        if A.is_cuda:
+            side = torch.cuda.Stream(device=A.device)
+            side.wait_stream(torch.cuda.current_stream(A.device))
+        for i, (r0, mr) in enumerate(blocks):
+            pack = pack_of(i)
+            with torch.cuda.stream(side) if side is not None else contextlib.nullcontext():
+                if i >= len(slots):
+                    works[i - len(slots)].wait()
+                pack.copy_(A[r0:r0 + mr])
+                works[i] = dist.broadcast(_storage(pack), src=src, group=group, async_op=True)
+        for r0, mr in blocks:
+            engine.shard_stream_rows(r0, A[r0:r0 + mr])  # the root's own rows need no wait
+        engine.shard_stream_end()
+        for w in works:  # the slots stay alive until their sends are done
+            w.wait()
+        return
+    # receivers: the first `ring` receives are posted up front; the receive of
+    # block i + ring is posted after block i's compute was issued, so (on the
+    # compute stream's order) it cannot overwrite a slot still being read
+    for i in range(len(slots)):
+        works[i] = dist.broadcast(_storage(pack_of(i)), src=src, group=group, async_op=True)
+    for i, (r0, mr) in enumerate(blocks):
+        works[i].wait()  # the compute stream waits for this block only
+        engine.shard_stream_rows(r0, pack_of(i))
+        nxt = i + len(slots)
+        if nxt < len(blocks):
+            works[nxt] = dist.broadcast(_storage(pack_of(nxt)), src=src, group=group, async_op=True)
+    engine.shard_stream_end()
+

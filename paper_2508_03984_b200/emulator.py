@@ -132,6 +132,21 @@ class Context:
         except Exception:
             pass
 
+    def set_workspace_limit(self, nbytes: int) -> None:
+        """device workspace cap in bytes (0: automatic); larger problems run in panels"""
+        _lib.check(self._lib.ozk_set_workspace_limit(self.handle, int(nbytes)))
+
+    @property
+    def workspace_bytes(self) -> int:
+        return int(self._lib.ozk_workspace_bytes(self.handle))
+
+    @property
+    def last_plan(self) -> dict:
+        """the panel plan of the last gemm: row panel height, column panel width, panels, extra residue passes"""
+        out = (C.c_int64 * 4)()
+        _lib.check(self._lib.ozk_last_plan(self.handle, out))
+        return {"rows": out[0], "cols": out[1], "panels": out[2], "extra_passes": out[3]}
+
     def set_stream(self, stream_ptr: int) -> None:
         _lib.check(self._lib.ozk_set_stream(self.handle, C.c_void_p(stream_ptr)))
 

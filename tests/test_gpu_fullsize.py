@@ -86,6 +86,18 @@ CASES = [
     (16384, 16384, 16384, 10, ScaleMode.Accurate, 1.0, Precision.Fp32),
     (8192, 8192, 65536, 14, ScaleMode.Fast, 0.5, Precision.Fp64),
     (32768, 32768, 32768, 14, ScaleMode.Fast, 0.5, Precision.Fp64),  # configs[3] per-GPU problem at 1 GPU
+    # every other point bench.py times (round 2)
+    (16384, 16384, 16384, 15, ScaleMode.Fast, 0.5, Precision.Fp64),
+    (16384, 16384, 16384, 15, ScaleMode.Accurate, 0.5, Precision.Fp64),
+    (16384, 16384, 16384, 16, ScaleMode.Fast, 0.5, Precision.Fp64),
+    (16384, 16384, 16384, 16, ScaleMode.Accurate, 0.5, Precision.Fp64),
+    (16384, 16384, 16384, 18, ScaleMode.Fast, 0.5, Precision.Fp64),
+    (16384, 16384, 16384, 18, ScaleMode.Accurate, 0.5, Precision.Fp64),
+    (16384, 16384, 16384, 6, ScaleMode.Fast, 0.5, Precision.Fp32),
+    (16384, 16384, 16384, 7, ScaleMode.Accurate, 0.5, Precision.Fp32),
+    (16384, 16384, 16384, 9, ScaleMode.Fast, 0.5, Precision.Fp32),
+    (16384, 16384, 16384, 9, ScaleMode.Accurate, 0.5, Precision.Fp32),
+    (8192, 8192, 65536, 14, ScaleMode.Accurate, 0.5, Precision.Fp64),
 ]
 
 
@@ -117,3 +129,62 @@ def test_full_size_sampled_parity(ctx, oracle, m, n, k, N, mode, phi, prec):
     got = Cg[torch.from_numpy(rows).cuda()][:, torch.from_numpy(cols).cuda()].cpu().numpy()
     assert got.size >= 4096
     np.testing.assert_array_equal(_bits(got), _bits(want))
+
+
+def _gen_chunked(rows, cols, phi, seed, chunk=2048):
+    """the paper's generator drawn column block by column block into one
+    preallocated column-major FP64 matrix (no full-size temporaries)"""
+    out = torch.empty((cols, rows), dtype=torch.float64, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    for j0 in range(0, cols, chunk):
+        j1 = min(cols, j0 + chunk)
+        blk = out[j0:j1]
+        torch.rand(blk.shape, generator=g, device="cuda", dtype=torch.float64, out=blk)
+        blk.neg_().add_(0.5)  # (1 - r) - 0.5 with r in [0, 1)
+        if phi:
+            blk.mul_(torch.exp(phi * torch.randn(blk.shape, generator=g, device="cuda", dtype=torch.float64)))
+    return out.t()
+
+
+def test_65536_single_gpu_sampled_parity(ctx, oracle):
+    """BASELINE configs[3] at one GPU: DGEMM 65536^3, N = 14, fast mode. A, B and
+    C alone take 103 GB, the full workspace would take 180 GB more, so the call
+    runs in panels under the automatic workspace limit. Fast-mode mu_i depends
+    on row i of A only and nu_j on column j of B only (scaling.cpp:58-99), so
+    the reference exponents of sampled rows/columns come from those rows and
+    columns alone; C is compared bit for bit on 64 x 64 sampled entries."""
+    n = 65536
+    N = 14
+    torch.cuda.empty_cache()
+    A = _gen_chunked(n, n, 0.5, 1)
+    B = _gen_chunked(n, n, 0.5, 2)
+    C = torch.empty((n, n), dtype=torch.float64, device="cuda").t()
+    torch.cuda.empty_cache()
+    cfg = EmuConfig(n_moduli=N, mode=ScaleMode.Fast)
+    ctx.set_workspace_limit(0)
+    ctx.gemm(A, B, cfg, C)
+    torch.cuda.synchronize()
+    plan = ctx.last_plan
+    # this call's footprint: the caller's A, B, C plus the handle's workspace
+    # (other handles of the test session may hold memory of their own)
+    used_gb = (torch.cuda.memory_allocated() + ctx.workspace_bytes) / 1e9
+    print(f"65536^3 N=14 fast: plan {plan}, A+B+C+workspace {used_gb:.1f} GB "
+          f"(workspace {ctx.workspace_bytes / 1e9:.1f} GB)")
+    assert plan["panels"] > 1
+    assert used_gb <= 160.0
+    mu = torch.zeros(n, dtype=torch.int32, device="cuda")
+    nu = torch.zeros(n, dtype=torch.int32, device="cuda")
+    ctx.stage_scale(A, B, cfg, mu, nu)
+    rng = np.random.default_rng(65536)
+    rows, cols = _sample(64, n, rng), _sample(64, n, rng)
+    ri, ci = torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda()
+    a_rows = _host(A[ri, :])
+    b_cols = _host(B[:, ci])
+    wmu, wnu = oracle.scale(a_rows, b_cols, N, 0, 0)  # row/column-local in fast mode
+    np.testing.assert_array_equal(mu[ri].cpu().numpy(), wmu)
+    np.testing.assert_array_equal(nu[ci].cpu().numpy(), wnu)
+    want = oracle.gemm_scaled(a_rows, b_cols, N, wmu, wnu)
+    got = C[ri][:, ci].cpu().numpy()
+    np.testing.assert_array_equal(_bits(got), _bits(want))
+    del A, B, C
+    torch.cuda.empty_cache()
