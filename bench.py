@@ -15,12 +15,15 @@ exceed the 126 MB L2, so no explicit flush is needed between steps.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
 
-Multi-GPU (torchrun, one rank per GPU): weak scaling by column blocks of B/C
-(SURVEY §8e); every rank owns an n = 16384 column block, rank 0's A is
-broadcast over NCCL inside each step (the north star's A broadcast) — in fast
-mode as row blocks that each rank starts computing on as they land
-(ozk_shard_stream_*, --row-block) — and "value" is the aggregate
-2 m n_total k / max-over-ranks time.
+Multi-GPU (torchrun, one rank per GPU), column blocks of B/C:
+rank 0's A is broadcast over NCCL inside each step (the north star's A
+broadcast) — in fast mode as row blocks that each rank starts computing on as
+they land (ozk_shard_stream_*, --row-block) — and "value" is the aggregate
+2 m n_total k / max-over-ranks time. --scaling weak (default): every rank owns
+an n-column block; --scaling strong: the n columns are split over the ranks
+(BASELINE configs[3]: --n 65536 --scaling strong; at one GPU the problem
+runs in workspace panels, with the footprint capped by
+--footprint-gb).
 """
 from __future__ import annotations
 
@@ -57,6 +60,12 @@ def parse():
                         "multi-rank run on one GPU; its timing means nothing)")
     p.add_argument("--row-block", type=int, default=2048,
                    help="fast mode, N > 1: A streams to the ranks in row blocks of this many rows (0: whole A)")
+    p.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                   help="weak: n columns per rank; strong: n columns in total, split over the ranks")
+    p.add_argument("--footprint-gb", type=float, default=160.0,
+                   help="cap on A + B + C + workspace per GPU (the workspace limit is set from it)")
+    p.add_argument("--e2e", dest="e2e_force", action="store_true",
+                   help="run the host-buffer e2e leg also above n = 32768 (needs 3 x 8 n^2 bytes of pinned host memory)")
     return p.parse_args()
 
 
@@ -179,17 +188,22 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ GPU helpers
-def gen_device(rows, cols, phi, seed, dtype, device):
-    """paper generator on the device: column-major (rows x cols) tensor"""
+def gen_device(rows, cols, phi, seed, dtype, device, chunk=2048):
+    """paper generator on the device: column-major (rows x cols) tensor, drawn
+    column block by column block (no full-size temporaries at n = 65536)"""
     import torch
 
     g = torch.Generator(device=device)
     g.manual_seed(seed)
-    x = torch.rand((cols, rows), generator=g, device=device, dtype=torch.float64)
-    x = (1.0 - x) - 0.5  # rand in (0, 1]
-    if phi:
-        x.mul_(torch.exp(phi * torch.randn((cols, rows), generator=g, device=device, dtype=torch.float64)))
-    return x.to(dtype).t()
+    out = torch.empty((cols, rows), dtype=dtype, device=device)
+    for j0 in range(0, cols, chunk):
+        j1 = min(cols, j0 + chunk)
+        x = torch.rand((j1 - j0, rows), generator=g, device=device, dtype=torch.float64)
+        x = (1.0 - x) - 0.5  # rand in (0, 1]
+        if phi:
+            x.mul_(torch.exp(phi * torch.randn((j1 - j0, rows), generator=g, device=device, dtype=torch.float64)))
+        out[j0:j1].copy_(x)
+    return out.t()
 
 
 def load_peaks():
@@ -267,8 +281,15 @@ def main():
         else:
             dist.init_process_group("gloo")
 
-    n = args.n
-    m = k = n
+    from paper_2508_03984_b200.distributed import column_shard
+
+    n_total = args.n
+    m = k = args.n
+    if args.scaling == "strong":
+        j0, n = column_shard(n_total, world, rank)  # this rank's share of the n columns
+        n_done = n_total
+    else:
+        n, n_done = args.n, args.n * world
     mode = ScaleMode.Fast if args.mode == "fast" else ScaleMode.Accurate
     cfg = EmuConfig(n_moduli=args.moduli, mode=mode, precision=Precision.Fp64)
     stream = torch.cuda.current_stream()
@@ -278,6 +299,10 @@ def main():
     A = gen_device(m, k, args.phi, 1, torch.float64, dev)
     B = gen_device(k, n, args.phi, 2 + rank, torch.float64, dev)  # this rank's column block
     C = torch.empty((n, m), dtype=torch.float64, device=dev).t()
+    torch.cuda.empty_cache()
+    # footprint cap: the caller's operands + the handle's workspace
+    ws_cap = int(args.footprint_gb * 1e9) - torch.cuda.memory_allocated(dev) - (1 << 30)
+    ctx.set_workspace_limit(max(ws_cap, 1 << 30))
 
     def step():
         if world > 1:
@@ -314,42 +339,64 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
-    flop = 2.0 * m * n * k
-    value = flop * world / (ms * 1e-3) / 1e12
+    flop = 2.0 * m * n * k  # this rank's share
+    value = 2.0 * m * n_done * k / (ms * 1e-3) / 1e12
+    free_b, total_b = torch.cuda.mem_get_info(dev)
+    memory = {"abc_gb": torch.cuda.memory_allocated(dev) / 1e9, "workspace_gb": ctx.workspace_bytes / 1e9,
+              "device_used_gb": (total_b - free_b) / 1e9, "device_total_gb": total_b / 1e9,
+              "plan": ctx.last_plan}
 
-    # ---- roofline of the dominant kernel (K2, tensor-bound) ------------------------
+    # ---- roofline of the dominant kernel (K2, tensor-bound) and of K1 / K3 (HBM) ----
     peaks = load_peaks()
-    # per step: the streamed multi-GPU path launches K2 once per row block of A
+    # per step: the streamed multi-GPU path launches K2 once per row block of A,
+    # the panelled path once per panel
     k2_ms = prof["products"][0] / args.steps
     k2_ops = args.moduli * 2.0 * m * n * k  # algorithmic int8 ops per step
     achieved = k2_ops / (k2_ms * 1e-3) / 1e12
     bf16 = peaks.get("bf16_tflops")
     peak = 2.0 * bf16 if bf16 else 2.0 * 1590.0
-    traffic = load_traffic().get(f"products_n{n}_N{args.moduli}_{args.mode}")
+    traffic = load_traffic().get(f"products_n{args.n}_N{args.moduli}_{args.mode}") if world == 1 else None
+    hbm = peaks.get("hbm_gbs") or 7700.0
+    # K1 / K3 in the step: K1's two streams overlap, so its wall time is the
+    # step's total minus K2 and K3 (which run after the join on one stream)
+    tot_ms = prof["total"][0] / args.steps
+    k3_ms = prof["reconstruct"][0] / args.steps
+    k1_ms = max(tot_ms - k2_ms - k3_ms, 1e-9)
+    es = 8
+    k1_bytes = (m * k + k * n) * (es + args.moduli)  # compulsory: read A, B; write N planes each
+    k3_bytes = m * n * (args.moduli + 8)             # read N residues, write C per element
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "residue_gemm_kernel (K2, tcgen05.mma kind::i8)",
                 "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (dense INT8 = 2 x dense BF16 on sm_100)"
                                 if bf16 else "2 x fallback 1.59 PFLOP/s bf16 (B200_PROFILING.md)"),
-                # per stage and step, summed over launches; the A-side and B-side K1
-                # chains run on two streams (overlapping), so scale + residues can
-                # exceed their wall-clock share
-                "stage_ms": {kname: v[0] / args.steps for kname, v in prof.items()},
-                "k2_launches_per_step": prof["products"][1] / args.steps}
+                "traffic_source": "profiles/roofline_traffic.json (ncu --set full, dram__bytes_read+write per launch)",
+                "k2_launches_per_step": prof["products"][1] / args.steps, "k2_ms": k2_ms,
+                # the memory-bound stages against MEASURED_PEAKS.json hbm_gbs, in the step
+                "k1_ms": k1_ms, "k1_gbps": k1_bytes / (k1_ms * 1e-3) / 1e9,
+                "k1_frac_hbm": k1_bytes / (k1_ms * 1e-3) / 1e9 / hbm,
+                "k3_ms": k3_ms, "k3_gbps": k3_bytes / (k3_ms * 1e-3) / 1e9,
+                "k3_frac_hbm": k3_bytes / (k3_ms * 1e-3) / 1e9 / hbm,
+                "hbm_peak_gbps": hbm,
+                "stage_ms": {kname: v[0] / args.steps for kname, v in prof.items()}}
     if peaks.get("bf16_tflops_sustained"):
         # K2 runs inside a long step: the sustained-clock denominator, for reference
         roofline["peak_sustained"] = 2.0 * peaks["bf16_tflops_sustained"]
         roofline["frac_sustained"] = achieved / roofline["peak_sustained"]
 
     out = {
-        "metric": f"emulated DGEMM TFLOPS (2mnk/s) at n={n}, {args.moduli} moduli, {args.mode} mode",
+        "metric": f"emulated DGEMM TFLOPS (2mnk/s) at n={args.n}, {args.moduli} moduli, {args.mode} mode",
         "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (rand-0.5)*exp(phi*randn), phi={args.phi}, generated on device",
-        "config": {"workload": f"DGEMM m=n=k={n} per GPU (column block of B/C), {args.moduli} moduli, {args.mode}",
-                   "l2": "inputs (2 x 2.1 GB) larger than L2; no flush", "parallelism": f"colshard{world}",
+        "config": {"workload": (f"DGEMM m=n=k={args.n} per GPU (column block of B/C), {args.moduli} moduli, {args.mode}"
+                                if args.scaling == "weak" else
+                                f"DGEMM m=n=k={args.n} split by columns over {world} GPU(s), {args.moduli} moduli, "
+                                f"{args.mode}"),
+                   "l2": "inputs (2 x 8 n^2 bytes) larger than L2; no flush", "parallelism": f"colshard{world}",
                    "a_broadcast": (f"row blocks of {args.row_block}" if world > 1 and args.row_block
-                                   and args.mode == "fast" else ("whole" if world > 1 else "none"))},
-        "gpu_launches": int(launches), "roofline": roofline, "clocks": clk.summary(),
+                                   and args.mode == "fast" else ("whole" if world > 1 else "none")),
+                   "footprint_cap_gb": args.footprint_gb},
+        "gpu_launches": int(launches), "roofline": roofline, "clocks": clk.summary(), "memory": memory,
     }
 
     # ---- end to end through the host-pointer C ABI (ozk_gemm_host) ----------------

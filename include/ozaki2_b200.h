@@ -289,12 +289,15 @@ int ozk_k3_replays(ozk_handle h, unsigned long long* count, int reset);
  *                            max(1 GiB, 10 % of the device) (env
  *                            OZK_WORKSPACE_GB overrides the automatic value)
  *   ozk_workspace_bytes      device bytes the handle holds now
+ *   ozk_release_workspace    frees the planes, U and staging buffers (the
+ *                            next call allocates what its plan needs)
  *   ozk_last_plan            the last ozk_gemm / ozk_gemm_host plan: out[0] row
  *                            panel height, out[1] column panel width, out[2]
  *                            panels, out[3] operand residue passes beyond one
  *                            per operand */
 int ozk_set_workspace_limit(ozk_handle h, int64_t bytes);
 int64_t ozk_workspace_bytes(ozk_handle h);
+int ozk_release_workspace(ozk_handle h);
 int ozk_last_plan(ozk_handle h, int64_t out[4]);
 
 #ifdef __cplusplus

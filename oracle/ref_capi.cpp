@@ -266,6 +266,20 @@ int ref_unscale(int n_moduli, int prec, int64_t m, int64_t n, const double* cpp,
 REF_COMPARE(ref_exact_compare_f64, double)
 REF_COMPARE(ref_exact_compare_f32, float)
 
+// the exact product (oracle.cpp exact_gemm) rounded to the nearest FP64 per
+// entry (ExactMatrix::value_rounded): compare()'s denominator, so one exact
+// GEMM serves the error of many candidate results
+#define REF_EXACT_ROUNDED(NAME, T)                                                                       \
+    int NAME(int64_t m, int64_t n, int64_t k, const T* a, const T* b, double* out) {                     \
+        return guarded([&] {                                                                             \
+            const ExactMatrix ex = exact_gemm(wrap(a, m, k), wrap(b, k, n));                             \
+            for (int64_t j = 0; j < n; ++j)                                                              \
+                for (int64_t i = 0; i < m; ++i) out[i + j * m] = ex.value_rounded(i, j);                 \
+        });                                                                                              \
+    }
+REF_EXACT_ROUNDED(ref_exact_rounded_f64, double)
+REF_EXACT_ROUNDED(ref_exact_rounded_f32, float)
+
 int ref_plain_gemm_f64(int64_t m, int64_t n, int64_t k, const double* a, const double* b, double* c) {
     return guarded([&] { unwrap(plain_gemm(wrap(a, m, k), wrap(b, k, n)), c); });
 }

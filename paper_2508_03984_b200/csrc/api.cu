@@ -698,7 +698,21 @@ Plan make_plan(ozk_context* h, const Job& J, int64_t extra_bytes = 0) {
     return found ? best : smallest;
 }
 
+void release(Buf& b) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+}
+
 int alloc_plan(ozk_context* h, Job& J, const Plan& P) {
+    // the plan counted what the handle holds as available: if any of the three
+    // buffers must grow, all three are released first (growing one while the
+    // others keep their old sizes could need more than the limit)
+    if (P.pa > h->planes_a.bytes || P.pb > h->planes_b.bytes || P.u > h->u.bytes) {
+        release(h->planes_a);
+        release(h->planes_b);
+        release(h->u);
+    }
     OZK_TRY(ensure(h->planes_a, P.pa));
     OZK_TRY(ensure(h->planes_b, P.pb));
     OZK_TRY(ensure(h->u, P.u));
@@ -1396,6 +1410,20 @@ int64_t ozk_workspace_bytes(ozk_handle h) {
                          &h->flags, &h->f32a, &h->f32b, &h->host_a, &h->host_b, &h->host_c})
         total += static_cast<int64_t>(b->bytes);
     return total;
+}
+
+int ozk_release_workspace(ozk_handle h) {
+    if (!h) return OZK_INPUT_ERROR;
+    if (h->shard_open || h->stream_open) {
+        set_error("ozk_release_workspace: a shard is open on this handle");
+        return OZK_INPUT_ERROR;
+    }
+    OZK_CUDA(cudaSetDevice(h->device));
+    OZK_CUDA(cudaDeviceSynchronize());
+    for (Buf* b : {&h->wide, &h->cbar, &h->planes_a, &h->planes_b, &h->u, &h->f32a, &h->f32b, &h->host_a, &h->host_b,
+                   &h->host_c})
+        release(*b);
+    return OZK_OK;
 }
 
 int ozk_last_plan(ozk_handle h, int64_t out[4]) {

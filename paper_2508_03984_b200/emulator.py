@@ -136,6 +136,10 @@ class Context:
         """device workspace cap in bytes (0: automatic); larger problems run in panels"""
         _lib.check(self._lib.ozk_set_workspace_limit(self.handle, int(nbytes)))
 
+    def release_workspace(self) -> None:
+        """free the handle's device workspace (planes, U, staging)"""
+        _lib.check(self._lib.ozk_release_workspace(self.handle))
+
     @property
     def workspace_bytes(self) -> int:
         return int(self._lib.ozk_workspace_bytes(self.handle))

@@ -282,6 +282,8 @@ class RefLib:
         L.ref_unscale.argtypes = [C.c_int, C.c_int, _i64, _i64, _p, _p, _p, _p]
         for nm in ("ref_exact_compare_f64", "ref_exact_compare_f32"):
             getattr(L, nm).argtypes = [_i64, _i64, _i64, _p, _p, _p, _p]
+        for nm in ("ref_exact_rounded_f64", "ref_exact_rounded_f32"):
+            getattr(L, nm).argtypes = [_i64, _i64, _i64, _p, _p, _p]
         L.ref_plain_gemm_f64.argtypes = [_i64, _i64, _i64, _p, _p, _p]
         L.ref_plain_gemm_f32.argtypes = [_i64, _i64, _i64, _p, _p, _p]
         L.ref_dump_tables_csv.argtypes = [C.c_int, C.c_int, C.c_char_p, C.c_int]
@@ -382,6 +384,28 @@ class RefLib:
         fn = self.lib.ref_exact_compare_f64 if prec == 0 else self.lib.ref_exact_compare_f32
         self._check(fn(m, n, k, _ptr(a), _ptr(b), _ptr(c), _ptr(rep)))
         return {"max_rel_err": rep[0], "median_rel_err": rep[1], "exact_match": bool(rep[2])}
+
+    def exact_rounded(self, a, b, prec=0):
+        """the exact product a b (GMP, oracle.cpp exact_gemm), each entry rounded to FP64"""
+        dt = np.float64 if prec == 0 else np.float32
+        a, b = _f(a, dt), _f(b, dt)
+        m, k = a.shape
+        n = b.shape[1]
+        out = np.zeros((m, n), order="F")
+        fn = self.lib.ref_exact_rounded_f64 if prec == 0 else self.lib.ref_exact_rounded_f32
+        self._check(fn(m, n, k, _ptr(a), _ptr(b), _ptr(out)))
+        return out
+
+    @staticmethod
+    def rel_errors(c, rounded_exact):
+        """compare()'s componentwise |c - r| / |r| (oracle.cpp:116-157) against
+        rounded exact values: 0 where equal, +inf where r = 0 != c"""
+        c = np.asarray(c, np.float64)
+        r = np.asarray(rounded_exact, np.float64)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            e = np.abs(c - r) / np.abs(r)
+        e = np.where(c == r, 0.0, e)
+        return np.where((r == 0) & (c != 0), np.inf, e)
 
     def plain_gemm(self, a, b, prec=0):
         dt = np.float64 if prec == 0 else np.float32

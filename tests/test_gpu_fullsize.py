@@ -153,15 +153,22 @@ def test_65536_single_gpu_sampled_parity(ctx, oracle):
     on row i of A only and nu_j on column j of B only (scaling.cpp:58-99), so
     the reference exponents of sampled rows/columns come from those rows and
     columns alone; C is compared bit for bit on 64 x 64 sampled entries."""
+    import gc
+
     n = 65536
     N = 14
+    gc.collect()  # contexts of earlier tests release their workspace
+    ctx.release_workspace()
     torch.cuda.empty_cache()
     A = _gen_chunked(n, n, 0.5, 1)
     B = _gen_chunked(n, n, 0.5, 2)
     C = torch.empty((n, n), dtype=torch.float64, device="cuda").t()
     torch.cuda.empty_cache()
     cfg = EmuConfig(n_moduli=N, mode=ScaleMode.Fast)
-    ctx.set_workspace_limit(0)
+    # the footprint target (VERDICT r1): caller's A, B, C + workspace <= 160 GB
+    ctx.set_workspace_limit(int(158e9) - torch.cuda.memory_allocated())
+    free, total = torch.cuda.mem_get_info()
+    print(f"before the call: {free / 1e9:.1f} of {total / 1e9:.1f} GB free")
     ctx.gemm(A, B, cfg, C)
     torch.cuda.synchronize()
     plan = ctx.last_plan
@@ -186,5 +193,7 @@ def test_65536_single_gpu_sampled_parity(ctx, oracle):
     want = oracle.gemm_scaled(a_rows, b_cols, N, wmu, wnu)
     got = C[ri][:, ci].cpu().numpy()
     np.testing.assert_array_equal(_bits(got), _bits(want))
+    ctx.set_workspace_limit(0)
+    ctx.release_workspace()
     del A, B, C
     torch.cuda.empty_cache()

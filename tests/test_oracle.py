@@ -271,3 +271,28 @@ def test_rmod_fast_is_symmetric_in_domain(oracle, n, prec, lim):
         p = c.moduli[i]
         for x, r in zip(xs, planes[i].ravel()):
             assert int(r) == _symmetric(int(x), p), (n, prec, p, int(x), int(r))
+
+
+def test_exact_rounded_reproduces_reference_compare(ref):
+    """bench.py's exact-error leg: one exact GEMM (oracle.cpp exact_gemm) rounded
+    per entry, then compare()'s error formula in numpy, equals the reference's
+    compare() (oracle.cpp:116-157) on the same candidate."""
+    from _oracle import RefLib
+
+    from paper_2508_03984_b200 import gen_matrix
+
+    a = gen_matrix(24, 700, 2.0, 41)
+    b = gen_matrix(700, 20, 2.0, 42)
+    b[:, 3] = 0.0  # exact zeros: error 0 (candidate 0) / inf (candidate != 0)
+    ex = ref.exact_rounded(a, b)
+    for c in (np.asfortranarray(a @ b), np.asfortranarray(ex.copy())):
+        c[0, 3] = 1e-300
+        e = RefLib.rel_errors(c, ex)
+        rep = ref.exact_compare(a, b, c)
+        assert np.isinf(e[0, 3])
+        finite = np.isfinite(e)
+        e2 = RefLib.rel_errors(np.where(finite, c, 0.0), ex)
+        rep2 = ref.exact_compare(a, b, np.asfortranarray(np.where(finite, c, 0.0)))
+        assert e2.max() == rep2["max_rel_err"]
+        assert np.median(e2) == rep2["median_rel_err"]
+        assert rep["max_rel_err"] == np.inf
