@@ -400,7 +400,8 @@ def main():
     }
 
     # ---- end to end through the host-pointer C ABI (ozk_gemm_host) ----------------
-    if not args.no_e2e and world == 1:
+    big = args.n > 32768 and not args.e2e_force  # 3 x 8 n^2 bytes of pinned host memory
+    if not args.no_e2e and world == 1 and not big:
         import numpy as np
 
         Ah = torch.empty((k, m), dtype=torch.float64, pin_memory=True)
@@ -419,7 +420,24 @@ def main():
         out["e2e"] = {"value": flop / e_s / 1e12, "unit": "TFLOPS", "h2d_bytes_per_step": 2 * 8 * m * k,
                       "d2h_bytes_per_step": 8 * m * n, "ms_per_step": e_s * 1e3,
                       "path": "ozk_gemm_host (pinned host A, B, C)"}
-    elif not args.no_e2e:
+        del Ah, Bh, Ch, an, bn, cn
+        # the same call from pageable host memory (what a crtgemm Matrix<T>, a
+        # std::vector, hands over): the handle's pinned staging ring
+        ap = np.asfortranarray(A.cpu().numpy())
+        bp = np.asfortranarray(B.cpu().numpy())
+        cp = np.zeros((m, n), order="F")
+        ctx.gemm_host(ap, bp, cfg, c=cp)
+        t0 = time.perf_counter()
+        for _ in range(2):
+            ctx.gemm_host(ap, bp, cfg, c=cp)
+        e_p = (time.perf_counter() - t0) / 2
+        out["e2e_pageable"] = {"value": flop / e_p / 1e12, "unit": "TFLOPS", "ms_per_step": e_p * 1e3,
+                               "path": "ozk_gemm_host (pageable numpy A, B, C)"}
+        del ap, bp, cp
+        dropin = dropin_e2e(args.n, args.moduli, args.mode)
+        if dropin:
+            out["e2e_dropin"] = dropin
+    elif not args.no_e2e and world > 1 and not big:
         # N > 1: host buffers on every rank (A on the source rank only): H2D of A
         # (rank 0) and of each rank's B block, the column-sharded GEMM with A's
         # row-streamed broadcast, D2H of each C block; wall clock, max over ranks
@@ -447,17 +465,21 @@ def main():
         t = torch.tensor([e_s], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e_s = float(t.item())
-        out["e2e"] = {"value": flop * world / e_s / 1e12, "unit": "TFLOPS",
+        out["e2e"] = {"value": 2.0 * m * n_done * k / e_s / 1e12, "unit": "TFLOPS",
                       "h2d_bytes_per_step": 8 * (m * k + k * n * world), "d2h_bytes_per_step": 8 * m * n * world,
                       "ms_per_step": e_s * 1e3,
                       "path": "pinned host A (rank 0), B and C blocks (every rank) -> H2D -> gemm_sharded -> D2H"}
+    elif not args.no_e2e:
+        out["e2e_note"] = f"host-buffer leg skipped at n={args.n} (needs {3 * 8 * args.n ** 2 / 1e9:.0f} GB pinned; --e2e)"
 
     # ---- extras: native FP64/FP32, moduli sweep, accuracy, int8 library -----------
-    if not args.no_extra and world == 1:
+    if not args.no_extra and world == 1 and args.n <= 16384:
         extra = {}
         extra["native_fp64_tflops"] = native_gemm_tflops(n, torch.float64, 3)
         extra["native_fp32_tflops"] = native_gemm_tflops(n, torch.float32, 3)
         extra["int8_cublaslt_tops"] = int8_library_tops(n)
+        exact = ExactPool()
+
         def timed(Ax, Bx, c2, Cx, reps=2, **kw):
             ctx.gemm(Ax, Bx, c2, Cx, **kw)
             torch.cuda.synchronize()
@@ -471,10 +493,19 @@ def main():
             kk = Ax.shape[0] if kw.get("trans_a") else Ax.shape[1]
             return 2.0 * mm * nn * kk / (s0.elapsed_time(s1) / reps * 1e-3) / 1e12
 
-        sweep = {}
-        for N in (12, 14, 16, 18, 20):
+        # accuracy at the bench size against the reference's exact GMP oracle
+        # (oracle.cpp exact_gemm / compare) on 64 x 64 sampled entries of C, full k
+        rows, cols = sample_idx(m, 64, 7), sample_idx(n, 64, 8)
+        exact.submit("main", A, B, rows, cols)
+        sweep, acc = {}, {}
+        for N in (12, 14, 15, 16, 18, 20):
             for md in (ScaleMode.Fast, ScaleMode.Accurate):
-                sweep[f"{md.name.lower()}{N}"] = timed(A, B, EmuConfig(n_moduli=N, mode=md), C)
+                key = f"{md.name.lower()}{N}"
+                sweep[key] = timed(A, B, EmuConfig(n_moduli=N, mode=md), C)
+                acc[key] = C[rows][:, cols].cpu().numpy()
+        Cn = torch.mm(A, B)
+        acc["native_fp64"] = Cn[rows][:, cols].cpu().numpy()
+        del Cn
         extra["dgemm_sweep_tflops"] = sweep
         # BLAS transposes (square problem: the stored operands are read as op(X) = X^T)
         extra["transposes_tflops"] = {"TN"[not ta] + "TN"[not tb]: timed(A, B, cfg, C, trans_a=ta, trans_b=tb)
@@ -482,31 +513,48 @@ def main():
         # SGEMM emulation (BASELINE configs[2]): FP32 inputs, FP32 C, N = 6..10, vs native FP32
         A32, B32 = A.float(), B.float()
         C32 = torch.empty((n, m), dtype=torch.float32, device=dev).t()
-        extra["sgemm_sweep_tflops"] = {
-            f"{md.name.lower()}{N}": timed(A32, B32, EmuConfig(n_moduli=N, mode=md, precision=Precision.Fp32), C32)
-            for N in (6, 7, 8, 9, 10) for md in (ScaleMode.Fast, ScaleMode.Accurate)}
-        extra["sgemm_accuracy"] = accuracy_probe(ctx, A32, B32, EmuConfig(n_moduli=8, mode=ScaleMode.Fast,
-                                                                          precision=Precision.Fp32))
+        exact.submit("sgemm", A32, B32, rows, cols)
+        ssweep, sacc = {}, {}
+        for N in (6, 7, 8, 9, 10):
+            for md in (ScaleMode.Fast, ScaleMode.Accurate):
+                key = f"{md.name.lower()}{N}"
+                ssweep[key] = timed(A32, B32, EmuConfig(n_moduli=N, mode=md, precision=Precision.Fp32), C32)
+                sacc[key] = C32[rows][:, cols].double().cpu().numpy()
+        sacc["native_fp32"] = torch.mm(A32, B32)[rows][:, cols].double().cpu().numpy()
+        extra["sgemm_sweep_tflops"] = ssweep
         del A32, B32, C32
-        # input dynamic range (BASELINE configs[4]): phi sweep accuracy on a 1024^2 block, full k
-        extra["phi_sweep"] = {}
+        # input dynamic range (BASELINE configs[4]): phi sweep, 1024^2 outputs with full k,
+        # exact errors on 64 x 64 sampled entries
+        phi_acc = {}
+        r1, c1 = sample_idx(1024, 64, 9), sample_idx(1024, 64, 10)
         for phi in (0.5, 1.0, 1.5, 2.0, 3.0, 4.0):
             Ap = gen_device(1024, k, phi, 11, torch.float64, dev)
             Bp = gen_device(k, 1024, phi, 12, torch.float64, dev)
-            extra["phi_sweep"][str(phi)] = {
-                f"{md.name.lower()}{N}": accuracy_probe(ctx, Ap, Bp, EmuConfig(n_moduli=N, mode=md), short=True)
-                for N in (14, 16, 18) for md in (ScaleMode.Fast, ScaleMode.Accurate)}
-            extra["phi_sweep"][str(phi)]["native_fp64"] = accuracy_probe(ctx, Ap, Bp, None, short=True)
-            del Ap, Bp
+            exact.submit(f"phi{phi}", Ap, Bp, r1, c1)
+            Cp = torch.empty((1024, 1024), dtype=torch.float64, device=dev).t()
+            d = {}
+            for N in (14, 16, 18):
+                for md in (ScaleMode.Fast, ScaleMode.Accurate):
+                    ctx.gemm(Ap, Bp, EmuConfig(n_moduli=N, mode=md), Cp)
+                    d[f"{md.name.lower()}{N}"] = Cp[r1][:, c1].cpu().numpy()
+            d["native_fp64"] = torch.mm(Ap, Bp)[r1][:, c1].cpu().numpy()
+            phi_acc[str(phi)] = d
+            del Ap, Bp, Cp
         # rectangular m = n = 8192, k = 65536 (configs[4]) and n = 32768 (configs[3] per-GPU problem)
         del C
         torch.cuda.empty_cache()
         Ar = gen_device(8192, 65536, args.phi, 21, torch.float64, dev)
         Br = gen_device(65536, 8192, args.phi, 22, torch.float64, dev)
         Cr = torch.empty((8192, 8192), dtype=torch.float64, device=dev).t()
-        extra["rect_8192x8192x65536_tflops"] = {f"{md.name.lower()}{args.moduli}": timed(
-            Ar, Br, EmuConfig(n_moduli=args.moduli, mode=md), Cr) for md in (ScaleMode.Fast, ScaleMode.Accurate)}
-        extra["rect_accuracy"] = accuracy_probe(ctx, Ar, Br, cfg)
+        r2, c2 = sample_idx(8192, 64, 11), sample_idx(8192, 64, 12)
+        exact.submit("rect", Ar, Br, r2, c2)
+        rect, racc = {}, {}
+        for md in (ScaleMode.Fast, ScaleMode.Accurate):
+            key = f"{md.name.lower()}{args.moduli}"
+            rect[key] = timed(Ar, Br, EmuConfig(n_moduli=args.moduli, mode=md), Cr)
+            racc[key] = Cr[r2][:, c2].cpu().numpy()
+        racc["native_fp64"] = torch.mm(Ar, Br)[r2][:, c2].cpu().numpy()
+        extra["rect_8192x8192x65536_tflops"] = rect
         del Ar, Br, Cr
         torch.cuda.empty_cache()
         if not os.environ.get("OZK_BENCH_NO_32K"):
@@ -520,8 +568,29 @@ def main():
             extra["native_fp64_32768_tflops"] = native_gemm_tflops(n2, torch.float64, 1)
             del A2, B2, C2
             torch.cuda.empty_cache()
-        # accuracy vs native FP64 on a sampled block
-        extra["accuracy"] = accuracy_probe(ctx, A, B, cfg)
+        # errors (componentwise relative, the reference's compare()) per configuration
+        errs = {"main": exact.errors("main", acc), "sgemm": exact.errors("sgemm", sacc),
+                "rect": exact.errors("rect", racc)}
+        extra["accuracy_exact"] = {
+            "how": "max / median |c - r| / |r| over 64 x 64 sampled entries of C (full k) against the exact "
+                   "product (reference oracle.cpp exact_gemm, GMP), phi=%g" % args.phi,
+            "dgemm_16384": errs["main"], "sgemm_16384": errs["sgemm"], "rect_8192x8192x65536": errs["rect"]}
+        extra["phi_sweep_exact_max_rel"] = {ph: {key: v[0] for key, v in exact.errors(f"phi{ph}", d).items()}
+                                            for ph, d in phi_acc.items()}
+        # the speed-up at matching accuracy: the fastest emulation whose max and
+        # median errors are both no larger than native FP64's
+        nat = errs["main"]["native_fp64"]
+        ok = [(sweep[key], key) for key, e in errs["main"].items()
+              if key in sweep and e[0] <= nat[0] and e[1] <= nat[1]]
+        if ok:
+            tf, key = max(ok)
+            extra["at_native_fp64_accuracy"] = {
+                "config": key, "tflops": tf, "max_rel": errs["main"][key][0], "median_rel": errs["main"][key][1],
+                "native_max_rel": nat[0], "native_median_rel": nat[1],
+                "native_fp64_tflops": extra["native_fp64_tflops"],
+                "speedup_vs_native_fp64": tf / extra["native_fp64_tflops"]}
+            out["tflops_at_native_fp64_accuracy"] = tf
+        exact.close()
         out["extra"] = extra
 
     if world == 1 and not os.environ.get("OZK_BENCH_NO_CPU"):  # the CPU leg: rank 0 at N = 1 only
@@ -536,54 +605,73 @@ def main():
         dist.destroy_process_group()
 
 
-def accuracy_probe(ctx, A, B, cfg, short=False):
-    """Max componentwise relative error on a 1024 x 1024 block of C (full k),
-    for this configuration and for native GEMM (cuBLAS, same precision),
-    against the N = 20 accurate-mode FP64 emulation of the same block, which is
-    exact to about one ulp at phi <= 4 (2.2e-16 .. 8.5e-16).
-    cfg None: native only."""
-    import torch
+def sample_idx(size, count, seed):
+    """sorted sample of `count` indices of [0, size) including the first and the last"""
+    import numpy as np
 
-    from paper_2508_03984_b200 import EmuConfig, ScaleMode
+    rng = np.random.default_rng(seed)
+    inner = rng.choice(np.arange(1, size - 1), count - 2, replace=False)
+    return np.array(sorted(set(inner.tolist()) | {0, size - 1}))
 
-    rows = min(1024, A.shape[0])
-    cols = min(1024, B.shape[1])
-    a = A[:rows, :].t().contiguous().t()
-    b = B[:, :cols].t().contiguous().t()
 
-    def emu(c):
-        out = torch.empty((cols, rows), dtype=torch.float64, device=A.device).t()
-        ctx.gemm(a, b, c, out)
+class ExactPool:
+    """the reference's exact GMP product of sampled rows x columns, computed on
+    host threads while the GPU keeps timing (oracle/_ref; checker only)"""
+
+    def __init__(self):
+        from concurrent.futures import ThreadPoolExecutor
+
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from _oracle import RefLib
+
+        self.ref = RefLib() if RefLib.available() else None
+        self.pool = ThreadPoolExecutor(4)
+        self.jobs = {}
+
+    def submit(self, name, A, B, rows, cols):
+        import numpy as np
+        import torch
+
+        if self.ref is None:
+            return
+        a = np.asfortranarray(A[torch.from_numpy(rows).to(A.device)].cpu().numpy())
+        b = np.asfortranarray(B[:, torch.from_numpy(cols).to(B.device)].cpu().numpy())
+        prec = 1 if a.dtype == np.float32 else 0
+        self.jobs[name] = self.pool.submit(self.ref.exact_rounded, a, b, prec)
+
+    def errors(self, name, results):
+        """{key: (max_rel, median_rel)} of each candidate block in `results`"""
+        import numpy as np
+
+        if name not in self.jobs:
+            return {}
+        from _oracle import RefLib
+
+        ex = self.jobs[name].result()
+        out = {}
+        for key, c in results.items():
+            e = RefLib.rel_errors(c, ex)
+            out[key] = (float(e.max()), float(np.median(e)))
         return out
 
-    ref = emu(EmuConfig(n_moduli=20, mode=ScaleMode.Accurate)) if a.dtype == torch.float64 else \
-        _exact_fp32_product(ctx, a, b)
-    den = ref.abs().clamp_min(1e-300)
-
-    def stats(x):
-        r = (x.double() - ref).abs() / den
-        return float(r.max()), float(r.median())
-
-    native = stats(a @ b)
-    if cfg is None:
-        return native[0] if short else {"native_max_rel": native[0], "native_median_rel": native[1]}
-    got = stats(emu(cfg))
-    if short:
-        return got[0]
-    return {"block": f"{rows}x{cols}, full k", "against": "emulated N=20 accurate FP64 (~1 ulp)",
-            "emulated_max_rel": got[0], "emulated_median_rel": got[1],
-            "native_max_rel": native[0], "native_median_rel": native[1]}
+    def close(self):
+        self.pool.shutdown()
 
 
-def _exact_fp32_product(ctx, a, b):
-    """FP32 inputs: their FP64 product through the N = 20 accurate FP64 emulation"""
-    import torch
+def dropin_e2e(n, moduli, mode):
+    """the reference-facing C++ API end to end: tools/dropin_bench (built against
+    include/crtgemm and the product library) times crtgemm::gemm_emulated on
+    Matrix<double> (std::vector storage) at n^3"""
+    exe = os.path.join(ROOT, "paper_2508_03984_b200", "lib", "dropin_bench")
+    if not os.path.exists(exe):
+        return None
+    try:
+        r = subprocess.run([exe, str(n), str(moduli), "0" if mode == "fast" else "1", "2"], capture_output=True,
+                           text=True, timeout=600)
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001  (reported, not fatal)
+        return {"error": str(e)[:200]}
 
-    from paper_2508_03984_b200 import EmuConfig, ScaleMode
-
-    out = torch.empty((b.shape[1], a.shape[0]), dtype=torch.float64, device=a.device).t()
-    ctx.gemm(a.double(), b.double(), EmuConfig(n_moduli=20, mode=ScaleMode.Accurate), out)
-    return out
 
 if __name__ == "__main__":
     main()

@@ -50,10 +50,11 @@ def _worker(rank, world, port, m, n, k, N, mode, phi, outdir, row_block):
 
 
 @pytest.mark.parametrize("mode,row_block", [(0, None), (0, 8), (1, None), (1, 8)])
-@pytest.mark.parametrize("m,n,k,N,phi", [(33, 37, 50, 14, 0.5), (20, 9, 70, 17, 2.0)])
+@pytest.mark.parametrize("m,n,k,N,phi", [(33, 37, 50, 14, 0.5), (20, 9, 70, 17, 2.0), (100, 12, 40, 14, 1.0)])
 def test_sharded_matches_single_process(tmp_path, oracle, mode, row_block, m, n, k, N, phi):
     """row_block=8, fast mode: A streamed in row blocks of 16 rows, one
-    async broadcast per block (accurate mode ignores it: mu needs all columns)"""
+    async broadcast per block (accurate mode ignores it: mu needs all columns);
+    m = 100 gives 7 blocks, so the ring of 3 pack buffers wraps"""
     from paper_2508_03984_b200.gen import gen_matrix
 
     world = 2
