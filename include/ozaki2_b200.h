@@ -295,6 +295,12 @@ int ozk_k3_replays(ozk_handle h, unsigned long long* count, int reset);
  *                            panel height, out[1] column panel width, out[2]
  *                            panels, out[3] operand residue passes beyond one
  *                            per operand */
+/* fast-mode exponent floor (scaling.cpp:50-52): floor(pp_fast - max(1, 0.51
+ * log2 ub)) evaluated like the reference (from_table 0: std::log2 on the host)
+ * or from the step table the kernels use for lines whose budget is near an
+ * integer (from_table 1). Diagnostic; the two agree for every ub >= 1. */
+int ozk_fast_floor(float pp_fast, double ub, int from_table);
+
 int ozk_set_workspace_limit(ozk_handle h, int64_t bytes);
 int64_t ozk_workspace_bytes(ozk_handle h);
 int ozk_release_workspace(ozk_handle h);

@@ -37,7 +37,7 @@ EXPORTED_SYMBOLS = (
     "ozk_shard_stream_begin", "ozk_shard_stream_rows", "ozk_shard_stream_end",
     "ozk_int8_gemm", "ozk_truncate_scale", "ozk_residues", "ozk_mod_u8_array", "ozk_accumulate", "ozk_crt_reduce",
     "ozk_unscale", "ozk_set_workspace_limit", "ozk_workspace_bytes", "ozk_last_plan",
-    "ozk_release_workspace",
+    "ozk_release_workspace", "ozk_fast_floor",
 )
 PROFILE_SLOTS = ("scale", "residues", "products", "reconstruct", "total")
 
@@ -129,6 +129,7 @@ def load() -> C.CDLL:
     L.ozk_workspace_bytes.argtypes = [p]
     L.ozk_last_plan.argtypes = [p, p]
     L.ozk_release_workspace.argtypes = [p]
+    L.ozk_fast_floor.argtypes = [C.c_float, C.c_double, i32]
     L.ozk_plane_ld.restype = i64
     L.ozk_plane_ld.argtypes = [i64]
     L.ozk_stage_residues.argtypes = [p, C.POINTER(OzkConfig), i64, i64, i64, p, i64, p, i64, p, p, p, p]

@@ -48,6 +48,54 @@ void set_error(const std::string& msg) { g_error = msg; }
 
 unsigned long long* k3_replay_counter(bool create);  // k3_tc.cu
 
+int fast_floor_host(float pp_fast, double ub) {
+    // scaling.cpp:50-52, same operations and order (compiled with -ffp-contract=off)
+    const double t = std::max(1.0, 0.51 * std::log2(ub));
+    return static_cast<int>(std::floor(static_cast<double>(pp_fast) - t));
+}
+
+// The step table of fast_floor_host over ub in [1, 2^48] (ub = sum_upper_bound
+// of a line's scaled sum of squares: 1 <= ub < 4 (k + 2) for k < 2^31): each
+// threshold is the smallest double at which the floor drops, found by
+// bisection on the (monotone) bit patterns of positive doubles. Cached per
+// pp_fast (the tables of every modulus count share few values).
+FastFloorTable fast_floor_table(float pp_fast) {
+    static std::mutex mu;
+    static std::vector<std::pair<float, FastFloorTable>> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const auto& e : cache)
+        if (std::memcmp(&e.first, &pp_fast, sizeof(float)) == 0) return e.second;
+    FastFloorTable T{};
+    T.floor0 = fast_floor_host(pp_fast, 1.0);
+    auto bits = [](double x) {
+        uint64_t u;
+        std::memcpy(&u, &x, 8);
+        return u;
+    };
+    auto from = [](uint64_t u) {
+        double x;
+        std::memcpy(&x, &u, 8);
+        return x;
+    };
+    const uint64_t top = bits(0x1.0p48);
+    uint64_t lo = bits(1.0);
+    for (int level = T.floor0 - 1; T.n < 24; --level) {
+        if (fast_floor_host(pp_fast, from(top)) > level) break;
+        uint64_t a = lo, b = top;  // floor(a) > level >= floor(b)
+        while (b - a > 1) {
+            const uint64_t mid = a + (b - a) / 2;
+            if (fast_floor_host(pp_fast, from(mid)) > level)
+                a = mid;
+            else
+                b = mid;
+        }
+        T.thr[T.n++] = from(b);
+        lo = b;
+    }
+    cache.push_back({pp_fast, T});
+    return T;
+}
+
 DevConsts to_dev(const ozk_constants& c) {
     DevConsts d{};
     d.n = c.n_moduli;
@@ -70,6 +118,7 @@ DevConsts to_dev(const ozk_constants& c) {
         d.s1_m52[i] = -c.s1[i] * 0x1p52;
         for (int b = 0; b < 4; ++b) d.negp_sh[b][i] = (0u - static_cast<uint32_t>(c.moduli[i])) << (8 * b);
     }
+    d.fast_floor = fast_floor_table(c.pp_fast);
     return d;
 }
 
@@ -406,6 +455,7 @@ LineFinal line_final(const Job& J, int32_t* exp_out, int32_t* zero_out, const vo
     F.is_f32 = J.in_f32;
     F.line_step = line_step;
     F.elem_step = elem_step;
+    F.fast_floor = J.dc.fast_floor;
     return F;
 }
 
@@ -1396,6 +1446,14 @@ int ozk_k3_replays(ozk_handle h, unsigned long long* count, int reset) {
 }
 
 int64_t ozk_plane_ld(int64_t k) { return plane_ld(k); }
+
+int ozk_fast_floor(float pp_fast, double ub, int from_table) {
+    if (!from_table) return fast_floor_host(pp_fast, ub);
+    const FastFloorTable T = fast_floor_table(pp_fast);
+    int f = T.floor0;
+    for (int i = 0; i < T.n; ++i) f -= ub >= T.thr[i] ? 1 : 0;
+    return f;
+}
 
 int ozk_set_workspace_limit(ozk_handle h, int64_t bytes) {
     if (!h || bytes < 0) return OZK_INPUT_ERROR;

@@ -81,7 +81,10 @@ __device__ void exact_line(const LineFinal& F, int64_t line, int lane) {
         const int cnt = k - h0 < 32 ? static_cast<int>(k - h0) : 32;
         for (int q = 0; q < cnt; ++q) s = __dadd_rn(s, __shfl_sync(0xffffffffu, sq, q));
     }
-    if (lane == 0) F.exp_out[line] = fast_exponent_from_budget(fast_budget(s, k, F.pp_fast), g, F.prec, F.fix);
+    // the floor from the host-built step table: the reference's glibc log2 decides
+    // it even where y = pp - 0.51 log2(ub) is within an ulp of an integer
+    if (lane == 0)
+        F.exp_out[line] = fast_exponent_from_floor(fast_floor_table(fast_ub(s, k), F.fast_floor), g, F.prec, F.fix);
 }
 
 // The last block of a 64-row group (over its k-splits) combines the partials

@@ -153,15 +153,33 @@ __device__ __forceinline__ int exponent_clamp(int prec) { return prec == OZK_FP6
 
 // The fast-mode budget y = pp_fast - max(1, 0.51 log2 ub) of fast_exponent
 // (scaling.cpp:50-52), ub = sum_upper_bound(s, k) (scaling.cpp:45-47).
-__device__ __forceinline__ double fast_budget(double s, int64_t k, float pp_fast) {
+__device__ __forceinline__ double fast_ub(double s, int64_t k) {
     const double factor = __dadd_rn(1.0, __dmul_rn(__dmul_rn(2.0, static_cast<double>(k + 2)), 0x1.0p-53));
-    const double ub = __dmul_rn(s, factor);
-    const double l = __dmul_rn(0.51, log2(ub));
+    return __dmul_rn(s, factor);
+}
+__device__ __forceinline__ double fast_budget(double s, int64_t k, float pp_fast) {
+    const double l = __dmul_rn(0.51, log2(fast_ub(s, k)));
     const double t = l > 1.0 ? l : 1.0;
     return __dsub_rn(static_cast<double>(pp_fast), t);
 }
+// floor(pp_fast - max(1, 0.51 log2 ub)) as the reference's host evaluates it
+// (glibc log2), from the step table built on the host (FastFloorTable): exact
+// for every ub, so no device log2 is involved where the floor is close
+__device__ __forceinline__ int fast_floor_table(double ub, const FastFloorTable& T) {
+    int f = T.floor0;
+#pragma unroll 4
+    for (int i = 0; i < T.n; ++i) f -= ub >= T.thr[i] ? 1 : 0;
+    return f;
+}
 // fast_exponent tail (scaling.cpp:52-55); the reference omits the "- g" term
 // and so do we, unless OZK_FLAG_FAST_EXPONENT_FIX asks for it.
+__device__ __forceinline__ int fast_exponent_from_floor(int fl, int g, int prec, int fix = 0) {
+    int e = fl - (fix ? g : 0);
+    const int cap = magnitude_cap(prec) - 1 - g;
+    e = e < cap ? e : cap;
+    const int cl = exponent_clamp(prec);
+    return clampi(e, -cl, cl);
+}
 __device__ __forceinline__ int fast_exponent_from_budget(double y, int g, int prec, int fix = 0) {
     int e = static_cast<int>(floor(y)) - (fix ? g : 0);
     const int cap = magnitude_cap(prec) - 1 - g;

@@ -16,6 +16,19 @@ namespace ozk {
 void set_error(const std::string& msg);
 const ozk_constants* cached_constants(int n, int precision);
 
+// floor(pp_fast - max(1, 0.51 log2 ub)) of the fast exponent (scaling.cpp:50-52)
+// as a step function of ub >= 1, evaluated on the host with the reference's
+// own arithmetic (std::log2 = glibc): floor0 at ub = 1, one less from each
+// threshold thr[i] up (ascending). Lines whose budget lies near an integer
+// take their floor from here instead of from a device log2.
+struct FastFloorTable {
+    double thr[24];
+    int n;
+    int floor0;
+};
+FastFloorTable fast_floor_table(float pp_fast);
+int fast_floor_host(float pp_fast, double ub);  // the reference's expression, on the host
+
 // Per-call constants as a by-value kernel parameter (about 1 KB).
 struct DevConsts {
     int n;
@@ -32,6 +45,7 @@ struct DevConsts {
     double s1_m52[OZK_MAX_MODULI];  // -s1_i * 2^52: fl(s1*u) = fma(s1, 2^52 + u, -s1 * 2^52) (FP32 tables)
     int fast_fix;  // OZK_FLAG_FAST_EXPONENT_FIX  // -s2_i * 2^52 (for fl(s2*u) = fma(s2, 2^52 + u, -s2 * 2^52))
     uint32_t negp_sh[4][OZK_MAX_MODULI];  // (-p_i mod 2^32) << 8b: K1b packs four residue bytes with IMADs
+    FastFloorTable fast_floor;
 };
 
 DevConsts to_dev(const ozk_constants& c);
@@ -80,6 +94,7 @@ struct LineFinal {
     const void* base;
     int is_f32;
     int64_t line_step, elem_step;
+    FastFloorTable fast_floor;
 };
 int row_stats_splits(int64_t m, int64_t k);
 int64_t row_stat_groups(int64_t m);  // counters a launch_row_stats over m lines needs
