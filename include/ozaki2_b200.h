@@ -230,6 +230,12 @@ int ozk_stage_reconstruct(ozk_handle h, const ozk_config* cfg, int64_t m, int64_
  * (ldc); two's-complement wrapping accumulation; k <= 2^17. */
 int ozk_int8_gemm(ozk_handle h, int64_t m, int64_t n, int64_t k, const int8_t* A, int64_t lda, const int8_t* B,
                   int64_t ldb, int32_t* C, int64_t ldc);
+/* int8_gemm_reference (int8_engine.hpp:27, int8_engine.cpp:66-80): the same
+ * product from a plain CUDA-core triple loop (one thread per entry, uint32
+ * wrapping sum in index order), independent of the tensor-core engine; any
+ * lda >= m, ldb >= k; k <= 2^17. For cross-checking ozk_int8_gemm. */
+int ozk_int8_gemm_reference(ozk_handle h, int64_t m, int64_t n, int64_t k, const int8_t* A, int64_t lda,
+                            const int8_t* B, int64_t ldb, int32_t* C, int64_t ldc);
 /* truncate_scale (residue.cpp:7-22): out = trunc(x * 2^e), e = scale_exp[i]
  * (side 0, rows) or scale_exp[j] (side 1, columns); type OZK_R64F | OZK_R32F */
 int ozk_truncate_scale(ozk_handle h, int type, int64_t rows, int64_t cols, const void* x, int64_t ldx,

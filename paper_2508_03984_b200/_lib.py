@@ -35,7 +35,7 @@ EXPORTED_SYMBOLS = (
     "ozk_kernel_launches", "ozk_profile", "ozk_profile_read", "ozk_k3_replays", "ozk_sync",
     "ozk_shard_begin", "ozk_shard_rowmax", "ozk_shard_end",
     "ozk_shard_stream_begin", "ozk_shard_stream_rows", "ozk_shard_stream_end",
-    "ozk_int8_gemm", "ozk_truncate_scale", "ozk_residues", "ozk_mod_u8_array", "ozk_accumulate", "ozk_crt_reduce",
+    "ozk_int8_gemm", "ozk_int8_gemm_reference", "ozk_truncate_scale", "ozk_residues", "ozk_mod_u8_array", "ozk_accumulate", "ozk_crt_reduce",
     "ozk_unscale", "ozk_set_workspace_limit", "ozk_workspace_bytes", "ozk_last_plan",
     "ozk_release_workspace", "ozk_fast_floor",
 )
@@ -149,6 +149,7 @@ def load() -> C.CDLL:
     L.ozk_shard_stream_rows.argtypes = [p, i64, i64, p, i64]
     L.ozk_shard_stream_end.argtypes = [p]
     L.ozk_int8_gemm.argtypes = [p, i64, i64, i64, p, i64, p, i64, p, i64]
+    L.ozk_int8_gemm_reference.argtypes = [p, i64, i64, i64, p, i64, p, i64, p, i64]
     L.ozk_truncate_scale.argtypes = [p, i32, i64, i64, p, i64, p, i32, p, i64]
     L.ozk_residues.argtypes = [p, C.POINTER(OzkConfig), i64, i64, p, i64, p, i64]
     L.ozk_mod_u8_array.argtypes = [p, i64, p, C.c_int32, C.c_int32, p]

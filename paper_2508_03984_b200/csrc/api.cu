@@ -1851,6 +1851,25 @@ int ozk_int8_gemm(ozk_handle h, int64_t m, int64_t n, int64_t k, const int8_t* A
     return OZK_OK;
 }
 
+int ozk_int8_gemm_reference(ozk_handle h, int64_t m, int64_t n, int64_t k, const int8_t* A, int64_t lda,
+                            const int8_t* B, int64_t ldb, int32_t* C, int64_t ldc) {
+    if (!h) return OZK_INPUT_ERROR;
+    if (m < 0 || n < 0 || k < 0 || lda < m || ldb < k || ldc < m) {
+        set_error("int8_gemm_reference: bad dimensions");
+        return OZK_INPUT_ERROR;
+    }
+    if (k > OZK_ENGINE_MAX_K) {
+        set_error("int8_gemm_reference: k exceeds 2^17");
+        return OZK_INPUT_ERROR;
+    }
+    OZK_CUDA(cudaSetDevice(h->device));
+    if (m == 0 || n == 0) return OZK_OK;
+    launch_int8_gemm_simple(A, B, m, n, k, lda, ldb, C, ldc, h->stream);
+    OZK_TRY(check_launch(h, 1));
+    OZK_CUDA(cudaStreamSynchronize(h->stream));
+    return OZK_OK;
+}
+
 int ozk_truncate_scale(ozk_handle h, int type, int64_t rows, int64_t cols, const void* x, int64_t ldx,
                        const int32_t* scale_exp, int side, void* out, int64_t ldo) {
     if (!h || rows < 0 || cols < 0 || ldx < rows || ldo < rows) return OZK_INPUT_ERROR;

@@ -367,12 +367,26 @@ Int32ProductMatrix int8_gemm(const Matrix<std::int8_t>& a, const Matrix<std::int
 }
 
 // The reference keeps a triple loop here as an in-tree cross-check of its
-// tiled CPU kernel (int8_engine.cpp:66-80); on the GPU both names run the
-// tensor-core engine, whose parity tests check it against the oracle instead.
+// tiled kernel (int8_engine.cpp:66-80); here it is a plain CUDA-core kernel
+// (ozk_int8_gemm_reference), independent of the tensor-core engine, so the
+// cross-check still compares two implementations.
 Int32ProductMatrix int8_gemm_reference(const Matrix<std::int8_t>& a, const Matrix<std::int8_t>& b) {
     if (a.cols != b.rows) throw InputError("int8_gemm_reference: inner dimensions disagree");
     if (a.cols > kEngineMaxK) throw InputError("int8_gemm_reference: k exceeds 2^17");
-    return int8_gemm(a, b, 1);
+    const std::int64_t m = a.rows, k = a.cols, n = b.cols;
+    Int32ProductMatrix out;
+    out.k_used = k;
+    out.data = Matrix<std::int32_t>(m, n);
+    Dev da(static_cast<size_t>(m * k) + 16), db(static_cast<size_t>(k * n) + 16), dc(4 * m * n + 16);
+    up(da.p, a.data.data(), static_cast<size_t>(m * k));
+    up(db.p, b.data.data(), static_cast<size_t>(k * n));
+    {
+        std::lock_guard<std::mutex> lock(g_mtx);
+        check(ozk_int8_gemm_reference(handle_locked(), m, n, k, da.as<std::int8_t>(), m > 0 ? m : 1,
+                                      db.as<std::int8_t>(), k > 0 ? k : 1, dc.as<std::int32_t>(), m > 0 ? m : 1));
+    }
+    down(out.data.data.data(), dc.p, 4 * static_cast<size_t>(m * n));
+    return out;
 }
 
 std::vector<Int32ProductMatrix> blocked_int8_gemm(const Matrix<std::int8_t>& a, const Matrix<std::int8_t>& b,

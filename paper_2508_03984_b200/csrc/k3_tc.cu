@@ -36,6 +36,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 #include "ozk_device.cuh"
 
@@ -167,6 +168,16 @@ struct TcCfg {
     static constexpr int kSmem = 1024 /*align*/ + S * kStageBytes + 2048;
     static_assert((32 - P) * 128 <= 2048, "MMA over-read leaves the allocation");
 };
+
+// rint(y) for |y| < 2^51 by the round-to-nearest-even addition of 1.5 2^52
+// (two DADDs on the FP64 pipe: FRND.F64 issues at ~1/4 of the DADD rate here,
+// tools/micro/fp64_rate.cu): y + M is rounded to an integer, ties to even
+// since M is even, and subtracting M is exact. Q = rint(P_inv c1) with
+// 0 <= c1 < 2^52 2^E1 (checked per call) is far inside the range.
+__device__ __forceinline__ double rint_small(double y) {
+    constexpr double M = 6755399441055744.0;  // 1.5 * 2^52
+    return __dadd_rn(__dadd_rn(y, M), -M);
+}
 
 // (2^52 + T) with T < 2^52 given as a 64-bit integer, as a double
 __device__ __forceinline__ double pair52(uint64_t T) {
@@ -389,6 +400,308 @@ __global__ void __launch_bounds__(kThreads, 4)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Column-tiled variant (the default): a tile is 128 rows x 4 columns of C,
+// landed by ONE TMA box {128 rows, P planes, 4 columns} (column q's planes at
+// q * P * 128 B, the same MN-major SW128 operand layout per column), four MMAs
+// (one per column) into a 64-column TMEM buffer. A consumer thread owns one
+// row, so its mu and the row's unscale range check are loaded once per row
+// chunk instead of per element, and the per-tile bookkeeping (barrier waits,
+// TMEM addressing, exponent loads) is shared by 4 (kCW = 4) or 2 (kCW = 8)
+// elements. kCW = 8: warps w and w + 4 drain the same TMEM lane quarter, two
+// columns each (a warp may only read the lanes of its warp % 4 quarter).
+// Per element: the digit combines, c1 (1 DFMA), c2~ (2 DFMA + DADD), Q (DMUL,
+// FRND), X (DFMA), the interval ends as directed products c2~ (1 -+ rf)
+// (2 DMUL) and sums (2 DADD), C'' (DFMA), and the unscale as one DMUL by 2^e:
+// a correctly rounded product by a power of two IS ldexp's result (both round
+// the exact value once, subnormal or overflowing results included), valid
+// whenever 2^e is a normal double, which |mu|, |nu| <= 511 guarantees; other
+// rows / columns, and undecided intervals, take the warp-uniform slow path.
+constexpr int kTileCols = 4;
+
+template <int P, int S>
+struct Tc4Cfg {
+    static constexpr int kColBytes = P * 128;
+    static constexpr int kStageBytes = kTileCols * kColBytes;
+    static constexpr int kSmem = 1024 + S * kStageBytes + 2048;
+    static_assert((32 - P) * 128 <= 2048, "MMA over-read leaves the allocation");
+};
+
+// wait with the hardware suspend hint: the thread sleeps in try_wait until the
+// phase completes (or the hint expires) instead of re-issuing the poll, so
+// waiting warps leave the issue slots to the warps that have work
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity), "r"(0x989680)
+        : "memory");
+}
+
+template <bool kF32Out, bool kPlain, bool kExact, int P, int S, int kCW>
+__global__ void __launch_bounds__(32 * kCW + 32, kCW == 4 ? 4 : 3)
+    reconstruct_tc4_kernel(const __grid_constant__ CUtensorMap umap, int m, int n, int row_chunks, int tiles,
+                           const int32_t* __restrict__ mu_exp, const int32_t* __restrict__ nu_exp, int nu_vec,
+                           const DevConsts c, const TcParams tp, double lo_fac, double hi_fac, double alpha,
+                           double beta, void* __restrict__ C, int64_t ldc, unsigned long long* __restrict__ replays) {
+    using Cf = Tc4Cfg<P, S>;
+    using OutT = typename std::conditional<kF32Out, float, double>::type;
+    constexpr int kColBytes = Cf::kColBytes, kStageBytes = Cf::kStageBytes;
+    constexpr int kConsumersT = 32 * kCW;
+    constexpr int kCPT = kTileCols * 4 / kCW;  // columns per consumer thread
+    constexpr uint32_t kBufCols = 16 * kTileCols;
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ __align__(8) uint64_t full[S], empty[S], mma_full[2], tmem_empty[2];
+    __shared__ uint32_t tmem_slot;
+    uint8_t* sbuf = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* bdig = sbuf + S * kStageBytes;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n_mod = c.n;
+    if (tid == 0) {
+        for (int st = 0; st < S; ++st) {
+            mbar_init(saddr(&full[st]), 1);
+            mbar_init(saddr(&empty[st]), kCW);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(saddr(&mma_full[b]), 1);
+            mbar_init(saddr(&tmem_empty[b]), kCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = tid; i < 16 * 32; i += blockDim.x) {  // B digits, as in reconstruct_tc_kernel
+        const int b = i >> 5, k = i & 31;
+        uint32_t v = 0;
+        if (k < n_mod && b < 6) v = static_cast<uint32_t>((tp.s1_int[k] >> (8 * b)) & 0xFFu);
+        if (k < n_mod && b >= 6 && b < 14) v = static_cast<uint32_t>((tp.s2_int[k] >> (8 * (b - 6))) & 0xFFu);
+        bdig[b * 128 + ((((k >> 4) ^ (b & 7)) << 4) | (k & 15))] = static_cast<uint8_t>(v);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
+                     "n"(2 * kBufCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_before();
+    __syncthreads();
+    tc_after();
+    const uint32_t tbase = tmem_slot;
+    const uint32_t sb0 = saddr(sbuf);
+    const uint32_t full0 = saddr(&full[0]), empty0 = saddr(&empty[0]);
+    const uint32_t mfull0 = saddr(&mma_full[0]), tempty0 = saddr(&tmem_empty[0]);
+
+    // tile t = chunk + row_chunks * cg: concurrently running blocks cover
+    // neighbouring row chunks of the same columns
+    const int dj = static_cast<int>(gridDim.x) / row_chunks, dr = static_cast<int>(gridDim.x) % row_chunks;
+    int cg = static_cast<int>(blockIdx.x) / row_chunks, chunk = static_cast<int>(blockIdx.x) % row_chunks;
+    const int step = gridDim.x;
+
+    if (warp == kCW) {
+        if (lane == 0) {  // TMA producer: one box per tile
+            const uint64_t pol = evict_first();
+            int st = 0;
+            uint32_t ph = 1;
+            for (int tile = blockIdx.x; tile < tiles; tile += step) {
+                mbar_wait_backoff(empty0 + 8 * st, ph);
+                const uint32_t fb = full0 + 8 * st;
+                mbar_expect_tx(fb, static_cast<uint32_t>(kStageBytes));
+                tma_3d(sb0 + st * kStageBytes, &umap, fb, chunk * 128, 0, cg * kTileCols, pol);
+                chunk += dr;
+                cg += dj;
+                if (chunk >= row_chunks) {
+                    chunk -= row_chunks;
+                    ++cg;
+                }
+                if (++st == S) {
+                    st = 0;
+                    ph ^= 1u;
+                }
+            }
+        } else if (lane == 1) {  // MMA issuer
+            const uint64_t bd = sdesc_sw128(saddr(bdig));
+            int st = 0, b = 0;
+            uint32_t ph = 0, tph = 1;
+            for (int tile = blockIdx.x; tile < tiles; tile += step) {
+                mbar_wait_sleep(full0 + 8 * st, ph);
+                mbar_wait_sleep(tempty0 + 8 * b, tph);
+                tc_after();
+                const uint32_t stage = sb0 + st * kStageBytes;
+#pragma unroll
+                for (int q = 0; q < kTileCols; ++q)
+                    mma_u8(tbase + b * kBufCols + q * 16, sdesc_sw128(stage + q * kColBytes), bd);
+                mma_commit(mfull0 + 8 * b);
+                if (++st == S) {
+                    st = 0;
+                    ph ^= 1u;
+                }
+                b ^= 1;
+                if (b == 0) tph ^= 1u;
+            }
+        }
+        return;
+    }
+
+    // consumers: row 32 (warp % 4) + lane of the chunk, columns q0 .. q0 + kCPT - 1
+    const int quarter = warp & 3;
+    const int q0 = (warp >> 2) * kCPT;
+    const int rin = 32 * quarter + lane;
+    const uint32_t row_lo = static_cast<uint32_t>(rin & 15), row_chunk = static_cast<uint32_t>(rin >> 4);
+    const uint32_t tq = tbase + (static_cast<uint32_t>(32 * quarter) << 16) + q0 * 16;
+    unsigned long long n_replay = 0;
+    // the exponents of tile k + 1 are loaded while tile k is reconstructed (the
+    // loads take a full tile of time; issued right before their use they were
+    // the kernel's largest stall); a full column group of an aligned nu is one
+    // vector load
+    auto load_exps = [&](int ch, int g, int& me_o, int (&ne_o)[kCPT]) {
+        const int r = ch * 128 + rin;
+        me_o = r < m ? __ldg(mu_exp + r) : 0;
+        const int j = g * kTileCols + q0;
+        if (nu_vec && j + kCPT <= n) {
+            if constexpr (kCPT == 4) {
+                const int4 v = __ldg(reinterpret_cast<const int4*>(nu_exp + j));
+                ne_o[0] = v.x;
+                ne_o[1] = v.y;
+                ne_o[2] = v.z;
+                ne_o[3] = v.w;
+            } else {
+                const int2 v = __ldg(reinterpret_cast<const int2*>(nu_exp + j));
+                ne_o[0] = v.x;
+                ne_o[1] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < kCPT; ++q) ne_o[q] = j + q < n ? __ldg(nu_exp + j + q) : 0;
+        }
+    };
+    int me_n, ne_n[kCPT];
+    if (static_cast<int>(blockIdx.x) < tiles) load_exps(chunk, cg, me_n, ne_n);
+    int st = 0, b = 0;
+    uint32_t tph = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += step) {
+        const int me = me_n;
+        int ne[kCPT];
+#pragma unroll
+        for (int q = 0; q < kCPT; ++q) ne[q] = ne_n[q];
+        const int row = chunk * 128 + rin;
+        const int j0 = cg * kTileCols + q0;
+        chunk += dr;
+        cg += dj;
+        if (chunk >= row_chunks) {
+            chunk -= row_chunks;
+            ++cg;
+        }
+        if (tile + step < tiles) load_exps(chunk, cg, me_n, ne_n);
+        mbar_wait_sleep(mfull0 + 8 * b, tph);
+        tc_after();
+        double c1[kCPT], cpp[kCPT];
+        uint32_t und = 0;  // bit q: the interval of column q did not decide
+        {
+            uint32_t v[kCPT][16];
+#pragma unroll
+            for (int q = 0; q < kCPT; ++q) tmem_ld16(tq + b * kBufCols + 16 * q, v[q]);
+            tmem_wait_ld();
+            tc_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty0 + 8 * b);
+#pragma unroll
+            for (int q = 0; q < kCPT; ++q) {
+                const uint32_t* w = v[q];
+                c1[q] = __fma_rn(pair52_xyz(w[0] + (w[1] << 8), w[2] + (w[3] << 8), w[4] + (w[5] << 8)), tp.sc1,
+                                 tp.sc1m);
+                const double Lp = pair52_xyz(w[6] + (w[7] << 8), w[8] + (w[9] << 8), 0u);
+                const double Hp = pair52_xyz(w[10] + (w[11] << 8), w[12] + (w[13] << 8), 0u);
+                const double c2 = __dadd_rn(__fma_rn(Hp, tp.sc2h, tp.sc2hm), __fma_rn(Lp, tp.sc2l, tp.sc2lm));
+                const double qv = rint_small(__dmul_rn(c.P_inv, c1[q]));
+                const double X = __fma_rn(-c.P1, qv, c1[q]);
+                if constexpr (kExact) {
+                    cpp[q] = __fma_rn(-c.P2, qv, __dadd_rn(X, c2));
+                } else {
+                    // c2 lies in [c2~ (1 - rf), c2~ (1 + rf)] (c2~ >= 0); fl(X + .) is
+                    // monotone, so equal sums at both ends are fl(X + c2)
+                    const double slo = __dadd_rn(X, __dmul_rd(c2, lo_fac));
+                    const double shi = __dadd_rn(X, __dmul_ru(c2, hi_fac));
+                    cpp[q] = __fma_rn(-c.P2, qv, slo);
+                    und |= (__double_as_longlong(slo) != __double_as_longlong(shi) ? 1u : 0u) << q;
+                }
+            }
+        }
+        const bool live_row = row < m;
+        const int cols = min(n - j0, kCPT);  // live columns of this thread (may be <= 0)
+        bool ok = static_cast<unsigned>(me + 511) <= 1022u;
+#pragma unroll
+        for (int q = 0; q < kCPT; ++q) ok = ok && static_cast<unsigned>(ne[q] + 511) <= 1022u;
+        OutT* cptr = static_cast<OutT*>(C) + static_cast<int64_t>(j0) * ldc + row;
+        const uint32_t emp = empty0 + 8 * st;
+        if (__all_sync(0xffffffffu, und == 0 && ok)) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(emp);
+            if (live_row) {
+                const int pow_row = (1023 - me) << 20;
+                OutT* p = cptr;
+#pragma unroll
+                for (int q = 0; q < kCPT; ++q, p += ldc) {
+                    if (q < cols) {
+                        double r = __dmul_rn(cpp[q], __hiloint2double(pow_row - (ne[q] << 20), 0));
+                        if (!kPlain) {
+                            const double old = beta != 0.0 ? static_cast<double>(*p) : 0.0;
+                            r = __dadd_rn(__dmul_rn(alpha, r), __dmul_rn(beta, old));
+                        }
+                        *p = static_cast<OutT>(r);
+                    }
+                }
+            }
+        } else {
+            // rare, warp-uniform: an undecided interval (replay the reference's c2,
+            // emulator.cpp:53, from the planes in shared memory) or an unscale
+            // factor that is not a normal power of two (general ldexp)
+            const uint32_t stage = sb0 + st * kStageBytes;
+#pragma unroll
+            for (int q = 0; q < kCPT; ++q) {
+                double cq = cpp[q];
+                if (!kExact && ((und >> q) & 1u)) {
+                    const double qv = rint_small(__dmul_rn(c.P_inv, c1[q]));
+                    const double X = __fma_rn(-c.P1, qv, c1[q]);
+                    const uint32_t line = stage + (q0 + q) * kColBytes + row_lo;
+                    double c2r = 0.0;
+#pragma unroll 1
+                    for (int t = 0; t < n_mod; ++t) {
+                        uint32_t ub;
+                        asm volatile("ld.shared.u8 %0, [%1];"
+                                     : "=r"(ub)
+                                     : "r"(line + t * 128 + ((row_chunk ^ static_cast<uint32_t>(t & 7)) << 4)));
+                        c2r = __dadd_rn(c2r, __fma_rn(c.s2[t], __hiloint2double(0x43300000, static_cast<int>(ub)),
+                                                      c.s2_m52[t]));
+                    }
+                    cq = __fma_rn(-c.P2, qv, __dadd_rn(X, c2r));
+                    if (live_row && q < cols) ++n_replay;
+                }
+                if (live_row && q < cols) {
+                    double r = unscale_fast(cq, -(me + ne[q]));
+                    if (!kPlain) {
+                        const double old = beta != 0.0 ? static_cast<double>(cptr[q * ldc]) : 0.0;
+                        r = __dadd_rn(__dmul_rn(alpha, r), __dmul_rn(beta, old));
+                    }
+                    cptr[q * ldc] = static_cast<OutT>(r);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(emp);
+        }
+        if (++st == S) st = 0;
+        b ^= 1;
+        if (b == 0) tph ^= 1u;
+    }
+    if (replays && n_replay) atomicAdd(replays, n_replay);
+    tc_before();
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumersT) : "memory");
+    if (warp == 0) {
+        tc_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(2 * kBufCols));
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         cudaDriverEntryPointQueryResult q;
@@ -440,10 +753,112 @@ bool launch_t(const CUtensorMap& map, int num_sms, cudaStream_t s, int64_t m, in
     return true;
 }
 
+// the column-tiled kernel (reconstruct_tc4_kernel): kCW consumer warps
+template <bool kF32Out, bool kPlain, bool kExact, int P, int S, int kCW>
+bool launch_t4(const CUtensorMap& map, int num_sms, cudaStream_t s, int64_t m, int64_t n, const int32_t* mu_exp,
+               const int32_t* nu_exp, const DevConsts& c, const TcParams& tp, double lo_fac, double hi_fac,
+               double alpha, double beta, void* C, int64_t ldc, unsigned long long* replays) {
+    using Cf = Tc4Cfg<P, S>;
+    auto kern = reconstruct_tc4_kernel<kF32Out, kPlain, kExact, P, S, kCW>;
+    constexpr int smem = Cf::kSmem;
+    constexpr int threads = 32 * kCW + 32;
+    constexpr int tmem_cols = 2 * 16 * kTileCols;
+    static std::atomic<unsigned long long> attr{0};
+    static std::atomic<int> per_sm_dev[64];
+    const int dev = current_device() & 63;
+    if (needs_setup(attr)) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        mark_setup(attr);
+    }
+    int per_sm = per_sm_dev[dev].load(std::memory_order_relaxed);
+    if (!per_sm) per_sm = [&] {
+        int smem_sm = 0, regs_sm = 0;
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, kern);
+        const int by_smem = smem_sm / (smem + static_cast<int>(fa.sharedSizeBytes) + 1024);
+        const int regs_warp = (fa.numRegs * 32 + 255) / 256 * 256;
+        const int by_regs = regs_sm / (regs_warp * (threads / 32));
+        const int v = std::min(std::min(by_smem, by_regs), 512 / tmem_cols);
+        per_sm_dev[dev].store(v < 1 ? -1 : v, std::memory_order_relaxed);
+        return v < 1 ? -1 : v;
+    }();
+    if (per_sm < 1) return false;
+    const int64_t row_chunks = (m + 127) / 128;
+    const int64_t tiles = row_chunks * ((n + kTileCols - 1) / kTileCols);
+    const int64_t grid = std::min<int64_t>(tiles, static_cast<int64_t>(num_sms) * per_sm);
+    if (tiles + grid >= (int64_t(1) << 31)) return false;  // 32-bit tile arithmetic
+    constexpr int cpt = kTileCols * 4 / kCW;
+    const int nu_vec = reinterpret_cast<uintptr_t>(nu_exp) % (4 * cpt) == 0;
+    kern<<<static_cast<unsigned>(grid), threads, smem, s>>>(
+        map, static_cast<int>(m), static_cast<int>(n), static_cast<int>(row_chunks), static_cast<int>(tiles), mu_exp,
+        nu_exp, nu_vec, c, tp, lo_fac, hi_fac, alpha, beta, C, ldc, replays);
+    return true;
+}
+
+// OZK_K3_TILE=1: the 512-row x 1-column kernel (reconstruct_tc_kernel, A/B timing);
+// OZK_K3_CW: consumer warps of the column-tiled kernel (4 or 8, default 4)
+int k3_tile_mode() {
+    static const int v = [] {
+        const char* e = std::getenv("OZK_K3_TILE");
+        return e ? std::atoi(e) : 4;
+    }();
+    return v;
+}
+int k3_consumer_warps() {
+    static const int v = [] {
+        const char* e = std::getenv("OZK_K3_CW");
+        return e && std::atoi(e) == 8 ? 8 : 4;
+    }();
+    return v;
+}
+
+int k3_stages() {
+    static const int v = [] {
+        const char* e = std::getenv("OZK_K3_STAGES");
+        const int x = e ? std::atoi(e) : 6;
+        return x == 4 || x == 8 ? x : 6;
+    }();
+    return v;
+}
+
+template <bool kF32Out, bool kPlain, bool kExact, int P>
+bool launch_t4_cw(const CUtensorMap& map, int sms, cudaStream_t s, int64_t m, int64_t n, const int32_t* mu_exp,
+                  const int32_t* nu_exp, const DevConsts& c, const TcParams& tp, double lo_fac, double hi_fac,
+                  double alpha, double beta, void* C, int64_t ldc, unsigned long long* replays) {
+    if (k3_consumer_warps() == 8)
+        return launch_t4<kF32Out, kPlain, kExact, P, 4, 8>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
+                                                           alpha, beta, C, ldc, replays);
+    if (k3_stages() == 8)
+        return launch_t4<kF32Out, kPlain, kExact, P, 8, 4>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
+                                                           alpha, beta, C, ldc, replays);
+    if (k3_stages() == 6)
+        return launch_t4<kF32Out, kPlain, kExact, P, 6, 4>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
+                                                           alpha, beta, C, ldc, replays);
+    return launch_t4<kF32Out, kPlain, kExact, P, 4, 4>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac, alpha,
+                                                       beta, C, ldc, replays);
+}
+
 template <bool kF32Out, bool kPlain>
-bool launch_variant(const CUtensorMap& map, int sms, cudaStream_t s, int64_t m, int64_t n, const int32_t* mu_exp,
-                    const int32_t* nu_exp, const DevConsts& c, const TcParams& tp, double alpha, double beta, void* C,
-                    int64_t ldc, unsigned long long* replays) {
+bool launch_variant(const CUtensorMap& map, const CUtensorMap& map4, int sms, cudaStream_t s, int64_t m, int64_t n,
+                    const int32_t* mu_exp, const int32_t* nu_exp, const DevConsts& c, const TcParams& tp,
+                    double lo_fac, double hi_fac, double alpha, double beta, void* C, int64_t ldc,
+                    unsigned long long* replays) {
+    if (k3_tile_mode() != 1) {
+        bool ok;
+        if (tp.rfac == 0.0)
+            ok = launch_t4_cw<kF32Out, kPlain, true, 16>(map4, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
+                                                        alpha, beta, C, ldc, replays);
+        else if (c.n <= 16)
+            ok = launch_t4_cw<kF32Out, kPlain, false, 16>(map4, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
+                                                         alpha, beta, C, ldc, replays);
+        else
+            ok = launch_t4_cw<kF32Out, kPlain, false, 24>(map4, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
+                                                         alpha, beta, C, ldc, replays);
+        if (ok) return true;
+    }
     if (tp.rfac == 0.0)  // c2 exact (N <= 10): no interval, never a replay
         return launch_t<kF32Out, kPlain, true, 16, 4>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc,
                                                       replays);
@@ -533,6 +948,8 @@ bool launch_reconstruct_tc(const uint8_t* u, int64_t ldu, int64_t stride, int64_
     unsigned __int128 total = 0;  // c1 exact and T1 < 2^52 (one-DFMA conversion)
     for (int t = 0; t < c.n; ++t) total += static_cast<unsigned __int128>(tp.s1_int[t]) * static_cast<unsigned>(c.p[t] - 1);
     if (total >= (static_cast<unsigned __int128>(1) << 52)) return false;
+    // Q = rint_small(P_inv c1) needs P_inv c1 < 2^51: c1 < 2^(52 + E1)
+    if (!(c.P_inv >= 0.0) || c.P_inv * std::ldexp(1.0, 52 + E1) >= std::ldexp(1.0, 50)) return false;
     if (E1 < -1000 || E1 > 1023 - 52 || E2 < -1000 || E2 > 1023 - 84) return false;
     tp.sc1 = std::ldexp(1.0, E1);
     tp.sc1m = -std::ldexp(1.0, E1 + 52);
@@ -554,16 +971,26 @@ bool launch_reconstruct_tc(const uint8_t* u, int64_t ldu, int64_t stride, int64_
     }();
     if (replay_all) tp.rfac = 1.0;
 
+    // interval ends as directed products: c2~ (1 - rf) is exact-representable
+    // scaled by a representable factor; 1 + rf rounded up to the 2^-52 grid
+    const double lo_fac = 1.0 - tp.rfac;
+    const double hi_fac = 1.0 + std::ceil(tp.rfac * 0x1p52) * 0x1p-52;
+
     auto enc = encode_fn();
     if (!enc) return false;
     const int P = c.n <= 16 ? 16 : 24;
-    CUtensorMap map;
+    CUtensorMap map, map4;
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(c.n), static_cast<cuuint64_t>(n)};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(stride), static_cast<cuuint64_t>(ldu)};
     cuuint32_t box[3] = {128u, static_cast<cuuint32_t>(P), 1u};
+    cuuint32_t box4[3] = {128u, static_cast<cuuint32_t>(P), static_cast<cuuint32_t>(kTileCols)};
     cuuint32_t estr[3] = {1, 1, 1};
     if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(u), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (enc(&map4, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(u), dims, strides, box4, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
 
@@ -573,11 +1000,14 @@ bool launch_reconstruct_tc(const uint8_t* u, int64_t ldu, int64_t stride, int64_
     unsigned long long* replays = k3_replay_counter(false);
     const bool plain = alpha == 1.0 && beta == 0.0;
     if (c_is_f32)
-        return plain ? launch_variant<true, true>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc, replays)
-                     : launch_variant<true, false>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc,
-                                                   replays);
-    return plain ? launch_variant<false, true>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc, replays)
-                 : launch_variant<false, false>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, alpha, beta, C, ldc, replays);
+        return plain ? launch_variant<true, true>(map, map4, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
+                                                  alpha, beta, C, ldc, replays)
+                     : launch_variant<true, false>(map, map4, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
+                                                   alpha, beta, C, ldc, replays);
+    return plain ? launch_variant<false, true>(map, map4, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac, alpha,
+                                               beta, C, ldc, replays)
+                 : launch_variant<false, false>(map, map4, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac, alpha,
+                                                beta, C, ldc, replays);
 }
 
 }  // namespace ozk

@@ -83,6 +83,23 @@ __global__ void unscale_kernel(const double* __restrict__ cpp, int64_t m, int64_
     }
 }
 
+// int8_gemm_reference (int8_engine.cpp:66-80): the reference's plain triple
+// loop, one thread per C entry on the CUDA cores, uint32 wrapping sum in
+// index order. Deliberately independent of the tensor-core engine (K2), so a
+// caller cross-checking int8_gemm against it compares two implementations.
+__global__ void int8_gemm_simple_kernel(const int8_t* __restrict__ a, const int8_t* __restrict__ b, int64_t m,
+                                        int64_t n, int64_t k, int64_t lda, int64_t ldb, int32_t* __restrict__ c,
+                                        int64_t ldc) {
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < m * n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = e % m, j = e / m;
+        uint32_t s = 0;
+        for (int64_t h = 0; h < k; ++h)
+            s += static_cast<uint32_t>(static_cast<int32_t>(a[i + h * lda]) * static_cast<int32_t>(b[h + j * ldb]));
+        c[i + j * ldc] = static_cast<int32_t>(s);
+    }
+}
+
 // row / column maxima of the int64 bound product (k > 2^19): one block per column
 __global__ void bound_max64_kernel(const long long* __restrict__ cbar, int64_t m, int64_t ld,
                                    unsigned long long* __restrict__ rowmax, unsigned long long* __restrict__ colmax) {
@@ -105,6 +122,11 @@ __global__ void bound_max64_kernel(const long long* __restrict__ cbar, int64_t m
 void launch_bound_max64(const long long* cbar, int64_t m, int64_t n, int64_t ld, unsigned long long* rowmax,
                         unsigned long long* colmax, cudaStream_t s) {
     bound_max64_kernel<<<static_cast<unsigned>(n), kThreads, 0, s>>>(cbar, m, ld, rowmax, colmax);
+}
+
+void launch_int8_gemm_simple(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int64_t k, int64_t lda,
+                             int64_t ldb, int32_t* c, int64_t ldc, cudaStream_t s) {
+    int8_gemm_simple_kernel<<<blocks_for(m * n), kThreads, 0, s>>>(a, b, m, n, k, lda, ldb, c, ldc);
 }
 
 void launch_truncate(int is_f32, const void* x, int64_t rows, int64_t cols, int64_t ldx, const int32_t* se, int side,

@@ -155,6 +155,8 @@ void launch_reconstruct(const uint8_t* u, int64_t ldu, int64_t plane_stride, int
                         int c_is_f32, cudaStream_t s);
 
 // ---- element-wise stage helpers (k_misc.cu) ---------------------------------
+void launch_int8_gemm_simple(const int8_t* a, const int8_t* b, int64_t m, int64_t n, int64_t k, int64_t lda,
+                             int64_t ldb, int32_t* c, int64_t ldc, cudaStream_t s);
 void launch_truncate(int is_f32, const void* x, int64_t rows, int64_t cols, int64_t ldx, const int32_t* se, int side,
                      void* out, int64_t ldo, cudaStream_t s);
 void launch_residues_literal(int is_f32, const void* x, int64_t rows, int64_t cols, int64_t ldx, const DevConsts& c,

@@ -6,7 +6,9 @@ FP32 tables and OZK_K3_TC=0. The library reads both switches once per process,
 so the sweeps run in child processes:
   * OZK_K3_REPLAY_ALL=1 widens the interval so (almost) every element takes the
     replay path — the path the default run reaches only ~100 times per 16384^2;
-  * OZK_K3_TC=0 runs every FP64 case through the all-FP64 kernel."""
+  * OZK_K3_TC=0 runs every FP64 case through the all-FP64 kernel;
+  * OZK_K3_CW=8 runs the column-tiled kernel with 8 consumer warps, and
+    OZK_K3_TILE=1 the earlier 512-row x 1-column kernel."""
 import os
 import subprocess
 import sys
@@ -19,7 +21,9 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("env", [{"OZK_K3_REPLAY_ALL": "1"}, {"OZK_K3_TC": "0"}], ids=["replay_all", "fp64_kernel"])
+@pytest.mark.parametrize("env", [{"OZK_K3_REPLAY_ALL": "1"}, {"OZK_K3_TC": "0"},
+                                 {"OZK_K3_CW": "8", "OZK_K3_REPLAY_ALL": "1"}, {"OZK_K3_TILE": "1"}],
+                         ids=["replay_all", "fp64_kernel", "cw8_replay_all", "row_tile_kernel"])
 def test_k3_variant_random_sweep(env):
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
                         os.path.join(ROOT, "tests", "test_gpu_random.py"), os.path.join(ROOT, "tests", "test_gpu_parity.py")],

@@ -152,7 +152,7 @@ def test_residue_planes(ctx, oracle, prec, N):
 
 @pytest.mark.parametrize("N", [2, 9, 14, 20])
 @pytest.mark.parametrize("c_f32", [False, True])
-@pytest.mark.parametrize("m,n,pad", [(61, 37, 16), (70, 37, 8), (3000, 5, 16)])
+@pytest.mark.parametrize("m,n,pad", [(61, 37, 16), (70, 37, 8), (3000, 5, 16), (129, 6, 16)])
 def test_reconstruct(ctx, oracle, N, c_f32, m, n, pad):
     """pad 16: the bulk-copy kernel (several 1024-row tiles and a partial one at
     m = 3000); pad 8 (ldu = 72, not 16-byte aligned): the register-staged fallback"""
@@ -175,6 +175,39 @@ def test_reconstruct(ctx, oracle, N, c_f32, m, n, pad):
         np.testing.assert_array_equal(got, want.astype(np.float32))
     else:
         np.testing.assert_array_equal(_bits(got), _bits(want))
+
+
+@pytest.mark.parametrize("N", [9, 14, 20])
+@pytest.mark.parametrize("c_f32", [False, True])
+@pytest.mark.parametrize("lo,hi", [(-1021, 1021), (500, 530), (-530, -500), (-511, 511)])
+def test_reconstruct_unscale_range(ctx, oracle, N, c_f32, lo, hi):
+    """unscale (reconstruct.cpp:49-69) across the exponent range: results that
+    are subnormal, overflow to inf, or leave the range of the fast unscale
+    (|mu|, |nu| > 511 -> 2^-(mu+nu) not a normal double) equal std::ldexp's"""
+    rng = np.random.default_rng(N + abs(lo))
+    m, n = 300, 41
+    consts = oracle.constants(N)
+    U = np.stack([rng.integers(0, p, size=(m, n)) for p in consts.moduli[:N]]).astype(np.uint8)
+    mu = rng.integers(lo, hi + 1, size=m).astype(np.int32)
+    nu = rng.integers(lo, hi + 1, size=n).astype(np.int32)
+    c1, c2 = oracle.accumulate(U, N)
+    want = oracle.unscale(oracle.crt_reduce(c1, c2, N), mu, nu)
+    ldu = (m + 15) // 16 * 16
+    Ud = np.zeros((N, n, ldu), np.uint8)
+    Ud[:, :, :m] = U.transpose(0, 2, 1)
+    cdt = torch.float32 if c_f32 else torch.float64
+    Cd = torch.zeros((n, m), dtype=cdt, device="cuda").t()
+    ctx.stage_reconstruct(EmuConfig(n_moduli=N), m, n, torch.from_numpy(Ud).cuda(), ldu,
+                          torch.from_numpy(mu).cuda(), torch.from_numpy(nu).cuda(), Cd)
+    got = Cd.cpu().numpy()
+    if c_f32:
+        with np.errstate(over="ignore"):
+            np.testing.assert_array_equal(got, want.astype(np.float32))
+    else:
+        np.testing.assert_array_equal(_bits(got), _bits(want))
+    if lo == -1021 and not c_f32:
+        fin = want[np.isfinite(want) & (want != 0)]
+        assert (np.abs(fin) < 2.2250738585072014e-308).any() and np.isinf(want).any()
 
 
 GEMM_CASES = [
@@ -498,3 +531,38 @@ def test_fault_injection_corrupt_s1_is_located(ctx, oracle, entry):
     U = torch.zeros((N, n, ldu), dtype=torch.uint8, device="cuda")
     ctx.stage_products(cfg, m, n, k, pa, pb, _lib.OZK_PRODUCTS_U8, U, ldu)
     np.testing.assert_array_equal(U.cpu().numpy()[:, :, :m].transpose(0, 2, 1), oracle.products_u8(a, b, N, 1))
+
+
+@pytest.mark.parametrize("m,n,k,pad", [(1, 1, 1, 0), (17, 33, 45, 3), (300, 129, 1000, 16), (64, 64, 1 << 17, 0)])
+def test_int8_gemm_reference_kernel(ctx, oracle, m, n, k, pad):
+    """ozk_int8_gemm_reference (int8_engine.cpp:66-80): the CUDA-core triple loop
+    against the oracle and against the tensor-core ozk_int8_gemm; padded
+    leading dimensions; k = 2^17 of -128 x -128 wraps like the reference."""
+    import ctypes as C
+
+    rng = np.random.default_rng(m + 7 * n + k)
+    if k == 1 << 17:
+        A = np.full((m, k), -128, np.int8)
+        B = np.full((k, n), -128, np.int8)
+        A[0, :5] = 3
+    else:
+        A = rng.integers(-128, 128, size=(m, k), dtype=np.int8)
+        B = rng.integers(-128, 128, size=(k, n), dtype=np.int8)
+    lda, ldb, ldc = m + pad, k + pad, m + pad
+    da = torch.zeros((k, lda), dtype=torch.int8, device="cuda")
+    da[:, :m] = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+    db = torch.zeros((n, ldb), dtype=torch.int8, device="cuda")
+    db[:, :k] = torch.from_numpy(np.ascontiguousarray(B.T)).cuda()
+    dc = torch.full((n, ldc), 7, dtype=torch.int32, device="cuda")
+    L = ctx._lib
+    _lib.check(L.ozk_int8_gemm_reference(ctx.handle, m, n, k, C.c_void_p(da.data_ptr()), lda,
+                                         C.c_void_p(db.data_ptr()), ldb, C.c_void_p(dc.data_ptr()), ldc))
+    got = dc.cpu().numpy()
+    want = oracle.int8_gemm(A, B)
+    np.testing.assert_array_equal(got[:, :m].T, want)
+    assert (got[:, m:] == 7).all()  # padding rows untouched
+    if lda % 16 == 0 and ldb % 16 == 0:
+        tc = torch.zeros((n, m), dtype=torch.int32, device="cuda")
+        _lib.check(L.ozk_int8_gemm(ctx.handle, m, n, k, C.c_void_p(da.data_ptr()), lda, C.c_void_p(db.data_ptr()),
+                                   ldb, C.c_void_p(tc.data_ptr()), m))
+        np.testing.assert_array_equal(tc.cpu().numpy(), got[:, :m])
