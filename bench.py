@@ -432,7 +432,7 @@ def main():
             ctx.gemm_host(ap, bp, cfg, c=cp)
         e_p = (time.perf_counter() - t0) / 2
         out["e2e_pageable"] = {"value": flop / e_p / 1e12, "unit": "TFLOPS", "ms_per_step": e_p * 1e3,
-                               "path": "ozk_gemm_host (pageable numpy A, B, C)"}
+                               "path": "ozk_gemm_host (pageable numpy A, B, C: pinned staging ring, host_stage.cpp)"}
         del ap, bp, cp
         dropin = dropin_e2e(args.n, args.moduli, args.mode)
         if dropin:

@@ -195,6 +195,8 @@ struct ozk_context {
     int64_t stream_ldc = 0, stream_rows = 0;
     int stream_c_f32 = 0;
     int64_t stream_ldu = 0;  // U pitch of the row-streamed shard's per-block products
+    // pinned staging of pageable host buffers (ozk_gemm_host), created on first use
+    HostStager* stager = nullptr;
     // device workspace limit (0: automatic) and the last call's panel plan
     int64_t ws_limit = 0;
     int64_t last_plan[4] = {0, 0, 0, 0};
@@ -1082,35 +1084,73 @@ int region_products(ozk_context* h, Job& J, int64_t r0, int64_t mr, int64_t c0, 
     return check_launch(h, 1);
 }
 
+// Host <-> device copies of ozk_gemm_host: pinned (or small) caller buffers
+// are DMA'd directly on the copy streams; large pageable ones go through the
+// handle's pinned staging (host_stage.cpp). up() returns a ticket that
+// must be passed to before_wait() before the compute stream waits on the
+// copy's event.
+struct HostIO {
+    ozk_context* h;
+    HostStager* st = nullptr;  // non-null: some buffer is staged
+    bool stage_a = false, stage_b = false, stage_c = false;
+    int64_t up(bool staged, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+               cudaEvent_t done, cudaError_t& err) {
+        if (staged) return st->h2d(dst, dpitch, src, spitch, width, height, done);
+        err = cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyHostToDevice, h->h2d);
+        if (err == cudaSuccess && done) err = cudaEventRecord(done, h->h2d);
+        return 0;
+    }
+    cudaError_t before_wait(int64_t ticket) { return ticket > 0 ? st->wait_issued(ticket) : cudaSuccess; }
+    cudaError_t down(bool staged, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                     size_t height, cudaEvent_t ready) {
+        if (staged) {
+            st->d2h(dst, dpitch, src, spitch, width, height, ready);
+            return cudaSuccess;
+        }
+        cudaError_t e = cudaStreamWaitEvent(h->d2h, ready, 0);
+        if (e == cudaSuccess) e = cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToHost, h->d2h);
+        return e;
+    }
+};
+// every exit of ozk_gemm_host waits for the staging threads (they hold the
+// caller's pointers)
+struct StagerFinish {
+    HostStager* st;
+    ~StagerFinish() {
+        if (st) st->finish();
+    }
+};
+
 // C[r0:r0+mr, c0:c0+nc] from the planes (K2 + K3), then its D2H on the copy stream
 // (the device staging C is m x n with pitch m; the caller's C has pitch ldc)
-int stream_region(ozk_context* h, Job& J, int64_t r0, int64_t mr, int64_t c0, int64_t nc, double alpha, int c_f32,
-                  void* C_host, int64_t ldc, cudaEvent_t done) {
+int stream_region(ozk_context* h, HostIO& io, Job& J, int64_t r0, int64_t mr, int64_t c0, int64_t nc, double alpha,
+                  int c_f32, void* C_host, int64_t ldc, cudaEvent_t done) {
     const int64_t ldd = J.m;
     OZK_TRY(region_products(h, J, r0, mr, c0, nc, alpha, 0.0, h->host_c.p, ldd, c_f32));
     const size_t cs = c_f32 ? 4 : 8;
     const char* cdev = static_cast<const char*>(h->host_c.p) + cs * (c0 * ldd + r0);
     OZK_CUDA(cudaEventRecord(done, h->stream));
-    OZK_CUDA(cudaStreamWaitEvent(h->d2h, done, 0));
-    OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(C_host) + cs * (c0 * ldc + r0), cs * ldc, cdev, cs * ldd, cs * mr,
-                               nc, cudaMemcpyDeviceToHost, h->d2h));
+    OZK_CUDA(io.down(io.stage_c, static_cast<char*>(C_host) + cs * (c0 * ldc + r0), cs * ldc, cdev, cs * ldd, cs * mr,
+                     nc, done));
     return OZK_OK;
 }
 
-int gemm_host_streamed(ozk_context* h, Job& J, double alpha, const void* A, int64_t lda, const void* B, int64_t ldb,
-                       void* C, int64_t ldc, int c_f32) {
+int gemm_host_streamed(ozk_context* h, HostIO& io, Job& J, double alpha, const void* A, int64_t lda, const void* B,
+                       int64_t ldb, void* C, int64_t ldc, int c_f32) {
     const size_t es = J.in_f32 ? 4 : 8;
     const int64_t m = J.m, n = J.n, k = J.k;
     const auto blocks_a = stream_blocks(m), blocks_b = stream_blocks(n);
     const int na = static_cast<int>(blocks_a.size()), nb = static_cast<int>(blocks_b.size());
     std::vector<cudaEvent_t> ev(na + nb + na + nb + 1);
     for (auto& e : ev) OZK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    struct EventGuard {
+    struct EventGuard {  // the staging threads use these events: they finish first
         std::vector<cudaEvent_t>& v;
+        HostStager* st;
         ~EventGuard() {
+            if (st) st->finish();
             for (auto& e : v) cudaEventDestroy(e);
         }
-    } guard{ev};
+    } guard{ev, io.st};
     cudaEvent_t evStart = ev.back();
     auto ev_a = [&](int i) { return ev[i]; };
     auto ev_b = [&](int j) { return ev[na + j]; };
@@ -1120,20 +1160,20 @@ int gemm_host_streamed(ozk_context* h, Job& J, double alpha, const void* A, int6
     OZK_CUDA(cudaStreamWaitEvent(h->h2d, evStart, 0));
     OZK_CUDA(cudaStreamWaitEvent(h->d2h, evStart, 0));
     // the copy stream: A_0, B_0, A_1, B_1, ...
+    std::vector<int64_t> tk_a(na, 0), tk_b(nb, 0);
+    cudaError_t ce = cudaSuccess;
     for (int s = 0; s < na || s < nb; ++s) {
         if (s < na) {
             const int64_t r0 = blocks_a[s].first, mr = blocks_a[s].second;
-            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(h->host_a.p) + es * r0, es * m,
-                                       static_cast<const char*>(A) + es * r0, es * lda, es * mr, k,
-                                       cudaMemcpyHostToDevice, h->h2d));
-            OZK_CUDA(cudaEventRecord(ev_a(s), h->h2d));
+            tk_a[s] = io.up(io.stage_a, static_cast<char*>(h->host_a.p) + es * r0, es * m,
+                            static_cast<const char*>(A) + es * r0, es * lda, es * mr, k, ev_a(s), ce);
+            OZK_CUDA(ce);
         }
         if (s < nb) {
             const int64_t c0 = blocks_b[s].first, nc = blocks_b[s].second;
-            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(h->host_b.p) + es * k * c0, es * k,
-                                       static_cast<const char*>(B) + es * ldb * c0, es * ldb, es * k, nc,
-                                       cudaMemcpyHostToDevice, h->h2d));
-            OZK_CUDA(cudaEventRecord(ev_b(s), h->h2d));
+            tk_b[s] = io.up(io.stage_b, static_cast<char*>(h->host_b.p) + es * k * c0, es * k,
+                            static_cast<const char*>(B) + es * ldb * c0, es * ldb, es * k, nc, ev_b(s), ce);
+            OZK_CUDA(ce);
         }
     }
     StageTimer total(h, OZK_PROFILE_TOTAL);
@@ -1141,16 +1181,18 @@ int gemm_host_streamed(ozk_context* h, Job& J, double alpha, const void* A, int6
     for (int s = 0; s < na || s < nb; ++s) {
         if (s < na) {
             const int64_t r0 = blocks_a[s].first, mr = blocks_a[s].second;
+            OZK_CUDA(io.before_wait(tk_a[s]));
             OZK_CUDA(cudaStreamWaitEvent(h->stream, ev_a(s), 0));
             {
                 StageTimer t(h, OZK_PROFILE_SCALE);
                 OZK_TRY(stream_a_block(h, J, r0, mr));
             }
             rows_in = r0 + mr;
-            if (cols_in > 0) OZK_TRY(stream_region(h, J, r0, mr, 0, cols_in, alpha, c_f32, C, ldc, ev_ra(s)));
+            if (cols_in > 0) OZK_TRY(stream_region(h, io, J, r0, mr, 0, cols_in, alpha, c_f32, C, ldc, ev_ra(s)));
         }
         if (s < nb) {
             const int64_t c0 = blocks_b[s].first, nc = blocks_b[s].second;
+            OZK_CUDA(io.before_wait(tk_b[s]));
             OZK_CUDA(cudaStreamWaitEvent(h->stream, ev_b(s), 0));
             {
                 StageTimer t(h, OZK_PROFILE_SCALE);
@@ -1161,7 +1203,7 @@ int gemm_host_streamed(ozk_context* h, Job& J, double alpha, const void* A, int6
                 OZK_TRY(stage_col_residues(h, J, c0, nc, J.nu, J.pb, J.pb_stride));
             }
             cols_in = c0 + nc;
-            if (rows_in > 0) OZK_TRY(stream_region(h, J, 0, rows_in, c0, nc, alpha, c_f32, C, ldc, ev_rb(s)));
+            if (rows_in > 0) OZK_TRY(stream_region(h, io, J, 0, rows_in, c0, nc, alpha, c_f32, C, ldc, ev_rb(s)));
         }
     }
     return OZK_OK;
@@ -1215,9 +1257,29 @@ int gemm_host(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int
     OZK_TRY(alloc_plan(h, J, P));
     const void* b_src = h->host_b.p;
     const int c_f32 = cfg->c_type == OZK_R32F;
+    // large pageable operands go through the pinned staging ring (OZK_HOST_STAGE=0: plain copies)
+    HostIO io{h};
+    {
+        static const bool stage_on = std::getenv("OZK_HOST_STAGE") == nullptr || std::atoi(std::getenv("OZK_HOST_STAGE")) != 0;
+        const size_t big = size_t(4) << 20;
+        io.stage_a = stage_on && es * rows_a * cols_a >= big && host_is_pageable(A);
+        io.stage_b = stage_on && es * rows_b * (tb ? k : n) >= big && host_is_pageable(B);
+        io.stage_c = stage_on && cs * m * n >= big && host_is_pageable(C);
+        if (io.stage_a || io.stage_b || io.stage_c) {
+            if (!h->stager) h->stager = new HostStager(h->device);
+            OZK_CUDA(h->stager->begin(h->h2d, h->d2h));
+            io.st = h->stager;
+        }
+    }
+    StagerFinish stager_finish{io.st};
+    auto staged_done = [&]() -> int {
+        if (io.st) OZK_CUDA(io.st->finish());
+        return OZK_OK;
+    };
     if (use_streamed(J, cfg, beta)) {
         OZK_CUDA(cudaSetDevice(h->device));
-        OZK_TRY(gemm_host_streamed(h, J, alpha, A, lda, B, ldb, C, ldc, c_f32));
+        OZK_TRY(gemm_host_streamed(h, io, J, alpha, A, lda, B, ldb, C, ldc, c_f32));
+        OZK_TRY(staged_done());
         OZK_CUDA(cudaStreamSynchronize(h->d2h));
         return finish_check(h, J, h->stream);
     }
@@ -1225,12 +1287,14 @@ int gemm_host(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int
     const int nblk = static_cast<int>((n + nb - 1) / nb);
     std::vector<cudaEvent_t> ev(2 * nblk + 2);
     for (auto& e : ev) OZK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    struct EventGuard {
+    struct EventGuard {  // the staging threads use these events: they finish first
         std::vector<cudaEvent_t>& v;
+        HostStager* st;
         ~EventGuard() {
+            if (st) st->finish();
             for (auto& e : v) cudaEventDestroy(e);
         }
-    } guard{ev};
+    } guard{ev, io.st};
     cudaEvent_t evA = ev[0], evStart = ev[1];
     auto ev_b = [&](int b) { return ev[2 + b]; };
     auto ev_c = [&](int b) { return ev[2 + nblk + b]; };
@@ -1242,28 +1306,33 @@ int gemm_host(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int
     OZK_CUDA(cudaEventRecord(evStart, h->stream));
     OZK_CUDA(cudaStreamWaitEvent(h->h2d, evStart, 0));
     OZK_CUDA(cudaStreamWaitEvent(h->d2h, evStart, 0));
-    OZK_CUDA(cudaMemcpy2DAsync(h->host_a.p, es * rows_a, A, es * lda, es * rows_a, cols_a, cudaMemcpyHostToDevice,
-                               h->h2d));
-    OZK_CUDA(cudaEventRecord(evA, h->h2d));
+    cudaError_t ce = cudaSuccess;
+    const int64_t tk_a = io.up(io.stage_a, h->host_a.p, es * rows_a, A, es * lda, es * rows_a, cols_a, evA, ce);
+    OZK_CUDA(ce);
+    std::vector<int64_t> tk_b(nblk, 0);
     for (int b = 0; b < nblk; ++b) {
         int64_t j0, nj;
         block(b, j0, nj);
+        cudaEvent_t after_b = beta != 0.0 ? nullptr : ev_b(b);
         if (tb)  // op(B) columns = rows j0.. of the stored n x k B
-            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(h->host_b.p) + es * j0, es * rows_b,
-                                       static_cast<const char*>(B) + es * j0, es * ldb, es * nj, k,
-                                       cudaMemcpyHostToDevice, h->h2d));
+            tk_b[b] = io.up(io.stage_b, static_cast<char*>(h->host_b.p) + es * j0, es * rows_b,
+                            static_cast<const char*>(B) + es * j0, es * ldb, es * nj, k, after_b, ce);
         else
-            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(h->host_b.p) + es * rows_b * j0, es * rows_b,
-                                       static_cast<const char*>(B) + es * ldb * j0, es * ldb, es * rows_b, nj,
-                                       cudaMemcpyHostToDevice, h->h2d));
-        if (beta != 0.0)
-            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(h->host_c.p) + cs * m * j0, cs * m,
-                                       static_cast<const char*>(C) + cs * ldc * j0, cs * ldc, cs * m, nj,
-                                       cudaMemcpyHostToDevice, h->h2d));
-        OZK_CUDA(cudaEventRecord(ev_b(b), h->h2d));
+            tk_b[b] = io.up(io.stage_b, static_cast<char*>(h->host_b.p) + es * rows_b * j0, es * rows_b,
+                            static_cast<const char*>(B) + es * ldb * j0, es * ldb, es * rows_b, nj, after_b, ce);
+        OZK_CUDA(ce);
+        if (beta != 0.0) {
+            // the block's event after both copies: a direct copy after a staged
+            // one would not be ordered behind it, so C follows B's route
+            const int64_t t = io.up(io.stage_b || io.stage_c, static_cast<char*>(h->host_c.p) + cs * m * j0, cs * m,
+                                    static_cast<const char*>(C) + cs * ldc * j0, cs * ldc, cs * m, nj, ev_b(b), ce);
+            OZK_CUDA(ce);
+            tk_b[b] = std::max(tk_b[b], t);
+        }
     }
     {
         StageTimer total(h, OZK_PROFILE_TOTAL);
+        OZK_CUDA(io.before_wait(tk_a));
         OZK_CUDA(cudaStreamWaitEvent(h->stream, evA, 0));
         OZK_TRY(round_a(h, J, cfg));
         {
@@ -1274,6 +1343,7 @@ int gemm_host(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int
             for (int b = 0; b < nblk; ++b) {  // bound GEMM per arriving block
                 int64_t j0, nj;
                 block(b, j0, nj);
+                OZK_CUDA(io.before_wait(tk_b[b]));
                 OZK_CUDA(cudaStreamWaitEvent(h->stream, ev_b(b), 0));
                 OZK_TRY(round_b(h, J, cfg, b_src, rows_b, j0, nj));
                 StageTimer t(h, OZK_PROFILE_SCALE);
@@ -1290,6 +1360,7 @@ int gemm_host(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int
             int64_t j0, nj;
             block(b, j0, nj);
             if (J.mode == OZK_FAST) {
+                OZK_CUDA(io.before_wait(tk_b[b]));
                 OZK_CUDA(cudaStreamWaitEvent(h->stream, ev_b(b), 0));
                 OZK_TRY(round_b(h, J, cfg, b_src, rows_b, j0, nj));
                 StageTimer t(h, OZK_PROFILE_SCALE);
@@ -1297,12 +1368,11 @@ int gemm_host(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, int
             }
             OZK_TRY(compute_block(h, J, j0, nj, alpha, beta, h->host_c.p, m, c_f32));
             OZK_CUDA(cudaEventRecord(ev_c(b), h->stream));
-            OZK_CUDA(cudaStreamWaitEvent(h->d2h, ev_c(b), 0));
-            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(C) + cs * ldc * j0, cs * ldc,
-                                       static_cast<const char*>(h->host_c.p) + cs * m * j0, cs * m, cs * m, nj,
-                                       cudaMemcpyDeviceToHost, h->d2h));
+            OZK_CUDA(io.down(io.stage_c, static_cast<char*>(C) + cs * ldc * j0, cs * ldc,
+                             static_cast<const char*>(h->host_c.p) + cs * m * j0, cs * m, cs * m, nj, ev_c(b)));
         }
     }
+    OZK_TRY(staged_done());
     OZK_CUDA(cudaStreamSynchronize(h->d2h));
     return finish_check(h, J, h->stream);
 }
@@ -1381,6 +1451,7 @@ int ozk_destroy(ozk_handle h) {
                    &h->host_b, &h->host_c})
         if (b->p) cudaFree(b->p);
     if (h->flags_host) cudaFreeHost(h->flags_host);
+    delete h->stager;
     if (h->side) cudaStreamDestroy(h->side);
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);

@@ -658,7 +658,7 @@ int launch_impl(const K2Launch& L, cudaStream_t s) {
         P.p[i] = L.c->p[i];
         P.pinv[i] = L.c->pinv_mulhi[i];
     }
-    P.group = env_int("OZK_K2_GROUP", 8);
+    P.group = std::max(1, env_int("OZK_K2_GROUP", 8));
     P.snake = env_int("OZK_K2_SNAKE", 1);  // serpentine raster: -1.3 GB DRAM per launch, +0.5 % in the bench (DESIGN)
     P.hints = env_int("OZK_K2_HINTS", 9);  // A evict_last, B evict_first (profiles/r01_k2_hints_sweep.md)
     // Lockstep (default on): co-resident clusters that share A/B panels stay

@@ -50,6 +50,34 @@ struct DevConsts {
 
 DevConsts to_dev(const ozk_constants& c);
 
+// Pinned staging of pageable host buffers for ozk_gemm_host (host_stage.cpp).
+bool host_is_pageable(const void* p);
+class HostStager {
+  public:
+    explicit HostStager(int device);
+    ~HostStager();
+    HostStager(const HostStager&) = delete;
+    HostStager& operator=(const HostStager&) = delete;
+    // start a call on these copy streams (allocates the pinned slots once)
+    cudaError_t begin(cudaStream_t h2d, cudaStream_t d2h);
+    // queue a pitched host -> device copy (width bytes x height columns);
+    // `done` (may be null) is recorded on the H2D stream after it. Returns a
+    // ticket for wait_issued.
+    int64_t h2d(void* dev, size_t dpitch, const void* host, size_t hpitch, size_t width, size_t height,
+                cudaEvent_t done);
+    // block until the copy with this ticket is on the stream (its event recorded)
+    cudaError_t wait_issued(int64_t ticket);
+    // queue a pitched device -> host copy that starts after `ready`
+    void d2h(void* host, size_t hpitch, const void* dev, size_t dpitch, size_t width, size_t height,
+             cudaEvent_t ready);
+    // wait until every queued copy has landed in host memory
+    cudaError_t finish();
+
+  private:
+    struct Impl;
+    Impl* impl_ = nullptr;
+};
+
 // Kernel attributes (dynamic shared memory opt-in, carveout) and launch
 // geometry are per device: a process may drive several GPUs (one handle per
 // device). `done` holds one bit per device ordinal; the attribute is set before

@@ -566,3 +566,62 @@ def test_int8_gemm_reference_kernel(ctx, oracle, m, n, k, pad):
         _lib.check(L.ozk_int8_gemm(ctx.handle, m, n, k, C.c_void_p(da.data_ptr()), lda, C.c_void_p(db.data_ptr()),
                                    ldb, C.c_void_p(tc.data_ptr()), m))
         np.testing.assert_array_equal(tc.cpu().numpy(), got[:, :m])
+
+
+def _pinned_like(x):
+    """a page-locked copy of a column-major host array (numpy view of pinned torch memory)"""
+    t = torch.empty(x.size, dtype=torch.float64 if x.dtype == np.float64 else torch.float32, pin_memory=True)
+    out = t.numpy().reshape(x.shape[::-1]).T  # column-major view
+    out[...] = x
+    return out, t
+
+
+@pytest.mark.parametrize("mode", [ScaleMode.Fast, ScaleMode.Accurate])
+@pytest.mark.parametrize("beta,c32,trans", [(0.0, False, False), (-0.5, False, False), (0.0, True, False),
+                                            (0.0, False, True)])
+def test_host_pageable_staging_equals_pinned(ctx, mode, beta, c32, trans):
+    """ozk_gemm_host with large pageable operands (numpy memory: the pinned
+    staging ring of host_stage.cpp) equals the same call on page-locked
+    operands (direct DMA), bit for bit; fast mode at these sizes takes the
+    row/column streamed pipeline, the other cases the column pipeline"""
+    m, n, k = 2304, 2600, 600
+    a = gen_matrix(k, m, 0.5, 91) if trans else gen_matrix(m, k, 0.5, 91)  # stored operand
+    b = gen_matrix(k, n, 0.5, 92)
+    c0 = gen_matrix(m, n, 0.0, 93)
+    cdt = np.float32 if c32 else np.float64
+    cfg = EmuConfig(n_moduli=14, mode=mode)
+    got = np.asfortranarray(c0.astype(cdt))
+    ctx.gemm_host(a, b, cfg, alpha=1.0, beta=beta, c=got, trans_a=trans)
+    pa, ta = _pinned_like(a)
+    pb, tb = _pinned_like(b)
+    pc, tc = _pinned_like(np.asfortranarray(c0.astype(cdt)))
+    ctx.gemm_host(pa, pb, cfg, alpha=1.0, beta=beta, c=pc, trans_a=trans)
+    np.testing.assert_array_equal(got.view(np.int32 if c32 else np.int64), pc.view(np.int32 if c32 else np.int64))
+
+
+def test_host_pageable_staging_small_slots():
+    """the staging ring with 3000-byte slots (columns split into pieces, many
+    slot reuses per call), in a child process (the slot size is read once)"""
+    import subprocess
+    import sys
+    import os
+    code = r"""
+import numpy as np, torch
+from paper_2508_03984_b200 import Context, EmuConfig, ScaleMode, gen_matrix
+ctx = Context(0)
+m, n, k = 2100, 2200, 700
+a, b = gen_matrix(m, k, 0.5, 1), gen_matrix(k, n, 0.5, 2)
+for mode in (ScaleMode.Fast, ScaleMode.Accurate):
+    cfg = EmuConfig(n_moduli=12, mode=mode)
+    got = ctx.gemm_host(a, b, cfg)
+    A = torch.from_numpy(np.ascontiguousarray(a.T)).cuda().t()
+    B = torch.from_numpy(np.ascontiguousarray(b.T)).cuda().t()
+    C = torch.empty((n, m), dtype=torch.float64, device="cuda").t()
+    ctx.gemm(A, B, cfg, C)
+    assert np.array_equal(got.view(np.int64), C.cpu().numpy().view(np.int64)), mode
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, OZK_HOST_STAGE_SLOT="3000", PYTHONPATH=root))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
