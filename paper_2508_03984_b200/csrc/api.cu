@@ -31,6 +31,8 @@
 #include <cstdlib>
 
 #include "ozaki2_b200.h"
+#include <nvtx3/nvToolsExt.h>
+
 #include "ozk_internal.h"
 
 namespace ozk {
@@ -177,6 +179,9 @@ struct ozk_context {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t launches = 0;
     Buf planes_a, planes_b, u, stats, ints, flags, f32a, f32b, host_a, host_b, host_c, wide, cbar, counters;
+    Buf fused;                  // one-pass K1 row state (k1_fused.cu): A side, then B side; zero between calls
+    uint32_t fused_epoch = 0;   // publication epoch of the one-pass row kernel's group exponents
+    int64_t fused_m = -1, fused_n = -1;  // the shape the state layout was last cleared for
     int32_t* flags_host = nullptr;  // pinned mirror of the device flag word
     // stage timing (ozk_profile): CUDA events on the compute stream
     bool profiling = false;
@@ -236,18 +241,27 @@ int ensure(Buf& b, size_t bytes) {
     return OZK_OK;
 }
 
-// RAII bracket recording a start/stop event pair for one stage slot
+// RAII bracket of one stage: an NVTX range on the host timeline (header-only
+// NVTX v3: a no-op unless a tool such as nsys / ncu --nvtx is attached) and,
+// with ozk_profile on, a start/stop event pair on the compute stream
+const char* stage_name(int slot) {
+    static const char* names[OZK_PROFILE_SLOTS] = {"ozk K1 scale", "ozk K1 residues", "ozk K2 products",
+                                                   "ozk K3 reconstruct", "ozk gemm"};
+    return slot >= 0 && slot < OZK_PROFILE_SLOTS ? names[slot] : "ozk";
+}
 struct StageTimer {
     ozk_context* h;
     int slot;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     StageTimer(ozk_context* hh, int s) : h(hh), slot(s) {
+        nvtxRangePushA(stage_name(s));
         if (!h->profiling) return;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0, h->stream);
     }
     ~StageTimer() {
+        nvtxRangePop();
         if (!h->profiling) return;
         cudaEventRecord(e1, h->stream);
         h->pending.push_back({slot, {e0, e1}});
@@ -583,6 +597,77 @@ int stage_col_residues(ozk_context* h, Job& J, int64_t j0, int64_t nj, const int
     return check_launch(h, 1);
 }
 
+// ---- one-pass K1 (k1_fused.cu) ---------------------------------------------------
+// The line statistics, the exponents and the planes in one pass over an operand
+// (fast mode: the residue planes; accurate mode: the bound plane Abar / Bbar).
+// OZK_K1_FUSED=0 selects the two-kernel path (stats kernel, then planes kernel).
+bool k1_fused_enabled() {
+    static const int v = [] {
+        const char* e = std::getenv("OZK_K1_FUSED");
+        return e && *e ? std::atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
+// the row kernel reads two adjacent rows per lane (16 / 8-byte vectors)
+bool rows_fusable(const void* x, int64_t ld) { return (reinterpret_cast<uintptr_t>(x) & 15) == 0 && ld % 2 == 0; }
+
+// state of the one-pass row kernel: [A side | B side], zeroed when it grows, then self-resetting
+int fused_state(ozk_context* h, const Job& J, void** sa, void** sb) {
+    const size_t a = (rows_fused_state_bytes(J.m) + 255) / 256 * 256;
+    const size_t b = (rows_fused_state_bytes(J.n) + 255) / 256 * 256;
+    // the regions' internal layout follows (m, n): after a shape change stale
+    // group epochs could sit where the next call expects zeroed counters, so
+    // the state is cleared whenever the buffer grows or the shape changes
+    const bool grow = !h->fused.p || a + b > h->fused.bytes;
+    OZK_TRY(ensure(h->fused, a + b));
+    if (grow || h->fused_m != J.m || h->fused_n != J.n) {
+        OZK_CUDA(cudaMemsetAsync(h->fused.p, 0, h->fused.bytes, h->stream));
+        h->fused_m = J.m;
+        h->fused_n = J.n;
+    }
+    *sa = h->fused.p;
+    *sb = static_cast<char*>(h->fused.p) + a;
+    return OZK_OK;
+}
+
+// op(A)'s rows in one pass: mu and its residue planes (fast), or mu' and Abar (accurate)
+bool a_fusable(const Job& J) { return k1_fused_enabled() && (J.ta || rows_fusable(J.a, J.lda)); }
+int stage_rows_fused(ozk_context* h, Job& J, void* state) {
+    const bool fast = J.mode == OZK_FAST;
+    const LineFinal F = line_final(J, fast ? J.mu : J.ma, fast ? nullptr : J.rowmax, J.a, J.ta ? J.lda : 1,
+                                   J.ta ? 1 : J.lda);
+    const int kind = fast ? 0 : 1;
+    if (J.ta)  // stored k x m: the lines are its columns, the planes K-major
+        launch_cols_fused(J.a, J.in_f32, J.k, J.m, J.lda, J.flags, F, J.dc, kind, J.pa, J.lda_p, J.pa_stride,
+                          h->num_sms, h->stream);
+    else
+        launch_rows_fused(J.a, J.in_f32, J.m, J.k, J.lda, ++h->fused_epoch, state, J.flags, F, J.dc, kind, J.pa,
+                          J.lda_p, J.pa_stride, h->num_sms, h->stream);
+    if (!fast && J.wide_bound) OZK_CUDA(cudaMemsetAsync(J.rowmax64, 0, sizeof(unsigned long long) * J.m, h->stream));
+    return check_launch(h, 1);
+}
+
+// columns [j0, j0+nj) of op(B) in one pass: nu and its planes (fast), or nu' and Bbar (accurate)
+bool b_fusable(const Job& J, int64_t j0) { return k1_fused_enabled() && (!J.tb || rows_fusable(b_block(J, j0), J.ldb)); }
+int stage_cols_fused(ozk_context* h, Job& J, int64_t j0, int64_t nj, void* state) {
+    const bool fast = J.mode == OZK_FAST;
+    const void* bj = b_block(J, j0);
+    const LineFinal F = line_final(J, fast ? J.nu + j0 : J.nb + j0, fast ? nullptr : J.colmax + j0, bj,
+                                   J.tb ? 1 : J.ldb, J.tb ? J.ldb : 1);
+    const int kind = fast ? 0 : 1;
+    int8_t* dst = J.pb + b_plane_off(J, j0);
+    if (J.tb)  // stored n x k: the lines are its rows, the planes MN-major
+        launch_rows_fused(bj, J.in_f32, nj, J.k, J.ldb, ++h->fused_epoch, state, J.flags, F, J.dc, kind, dst, J.ld,
+                          J.pb_stride, h->num_sms, h->stream);
+    else
+        launch_cols_fused(bj, J.in_f32, J.k, nj, J.ldb, J.flags, F, J.dc, kind, dst, J.ld, J.pb_stride, h->num_sms,
+                          h->stream);
+    if (!fast && J.wide_bound)
+        OZK_CUDA(cudaMemsetAsync(J.colmax64 + j0, 0, sizeof(unsigned long long) * nj, h->stream));
+    return check_launch(h, 1);
+}
+
 int stage_products(ozk_context* h, Job& J, int64_t j0, int64_t nj, const int8_t* pa, int64_t pa_stride,
                    const int8_t* pb, int64_t pb_stride, int kind, void* out, int64_t ldo, int64_t out_stride) {
     K2Launch L{};
@@ -906,31 +991,57 @@ int gemm_device(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, i
         // A's rows on the handle's stream, B's columns on the side stream: the two
         // chains of small K1 kernels overlap (what bounds small problems); they
         // share no buffers (separate partials, exponents and flag words)
+        // one pass per operand (k1_fused.cu) where the whole problem is one
+        // panel (fast mode writes the residue planes of all of A / B) or in
+        // accurate mode (the bound planes always cover the whole problem)
+        void *st_a = nullptr, *st_b = nullptr;
+        OZK_TRY(fused_state(h, J, &st_a, &st_b));  // before the fork: its first-use memset is on this stream
         OZK_CUDA(cudaEventRecord(h->ev_fork, h->stream));
         OZK_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+        const bool whole = P.single || !fast;
         {
             StageTimer t(h, OZK_PROFILE_SCALE);
             OZK_TRY(round_a(h, J, cfg));
-            OZK_TRY(stage_rows(h, J));
         }
-        if (fast && P.single) {
+        const bool fa = whole && a_fusable(J);
+        {
+            StageTimer t(h, OZK_PROFILE_SCALE);
+            OZK_TRY(fa ? stage_rows_fused(h, J, st_a) : stage_rows(h, J));
+        }
+        if (fast && P.single && !fa) {
             StageTimer t(h, OZK_PROFILE_RESIDUES);
             OZK_TRY(stage_row_residues(h, J, J.mu, J.pa));
         }
-        {
-            OnSideStream side(h);
+        auto b_chain = [&]() -> int {
             {
                 StageTimer t(h, OZK_PROFILE_SCALE);
                 OZK_TRY(round_b(h, J, cfg, J.b, J.ldb, 0, n));
-                OZK_TRY(stage_cols(h, J, 0, n, fast ? 0 : 1));
             }
-            if (fast && P.single) {
+            const bool fb = whole && b_fusable(J, 0);
+            {
+                StageTimer t(h, OZK_PROFILE_SCALE);
+                OZK_TRY(fb ? stage_cols_fused(h, J, 0, n, st_b) : stage_cols(h, J, 0, n, fast ? 0 : 1));
+            }
+            if (fast && P.single && !fb) {
                 StageTimer t(h, OZK_PROFILE_RESIDUES);
                 OZK_TRY(stage_col_residues(h, J, 0, n, J.nu, J.pb, J.pb_stride));
             }
-            OZK_CUDA(cudaEventRecord(h->ev_join, h->stream));
+            return OZK_OK;
+        };
+        // the one-pass kernels each fill the GPU and keep their lines in L2
+        // until the planes pass: concurrent, they evict each other's lines
+        // (measured: 3.3 ms together vs 2.6 ms back to back at 16384^2), so
+        // after a one-pass A the B chain follows on the same stream
+        if (fa) {
+            OZK_TRY(b_chain());
+        } else {
+            {
+                OnSideStream side(h);
+                OZK_TRY(b_chain());
+                OZK_CUDA(cudaEventRecord(h->ev_join, h->stream));
+            }
+            OZK_CUDA(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
         }
-        OZK_CUDA(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
         // the bound GEMM needs both bound operands, mu and nu need its maxima
         if (!fast) OZK_TRY(bound_and_budget(h, J));
         if (!P.single) {
@@ -1446,8 +1557,8 @@ int ozk_create(ozk_handle* handle, int device) {
 int ozk_destroy(ozk_handle h) {
     if (!h) return OZK_OK;
     cudaSetDevice(h->device);
-    for (Buf* b : {&h->wide, &h->cbar, &h->counters, &h->planes_a, &h->planes_b, &h->u, &h->stats, &h->ints, &h->flags, &h->f32a,
-                   &h->f32b, &h->host_a,
+    for (Buf* b : {&h->wide, &h->cbar, &h->counters, &h->fused, &h->planes_a, &h->planes_b, &h->u, &h->stats, &h->ints,
+                   &h->flags, &h->f32a, &h->f32b, &h->host_a,
                    &h->host_b, &h->host_c})
         if (b->p) cudaFree(b->p);
     if (h->flags_host) cudaFreeHost(h->flags_host);
@@ -1535,8 +1646,8 @@ int ozk_set_workspace_limit(ozk_handle h, int64_t bytes) {
 int64_t ozk_workspace_bytes(ozk_handle h) {
     if (!h) return 0;
     int64_t total = 0;
-    for (const Buf* b : {&h->wide, &h->cbar, &h->counters, &h->planes_a, &h->planes_b, &h->u, &h->stats, &h->ints,
-                         &h->flags, &h->f32a, &h->f32b, &h->host_a, &h->host_b, &h->host_c})
+    for (const Buf* b : {&h->wide, &h->cbar, &h->counters, &h->fused, &h->planes_a, &h->planes_b, &h->u, &h->stats,
+                         &h->ints, &h->flags, &h->f32a, &h->f32b, &h->host_a, &h->host_b, &h->host_c})
         total += static_cast<int64_t>(b->bytes);
     return total;
 }

@@ -6,7 +6,9 @@
 // the reference exceptions. A process-wide context (device OZK_DEVICE, default
 // 0) is shared under a mutex, which keeps the API reentrant like the
 // reference (crt_tables.cpp:190-196 is its only shared state).
+#include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -14,6 +16,10 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <vector>
+
+#include <sys/mman.h>
 
 #include <cuda_runtime.h>
 
@@ -55,6 +61,46 @@ ozk_handle handle_locked() {
         check(ozk_create(&g_handle, env ? std::atoi(env) : 0));
     }
     return g_handle;
+}
+
+// The result matrix of a large call: Matrix<double>(m, n) value-initialises
+// fresh pages, and at 16384^2 (2 GB) the first-touch page faults of that
+// memset cost ~0.8 s on one thread — far more than the emulated GEMM. The
+// storage is reserved first, the kernel asked for transparent huge pages,
+// the pages are populated by several threads at once (MADV_POPULATE_WRITE,
+// Linux >= 5.14; silently skipped where unsupported), and only then is the
+// vector resized (value-initialised) over memory that is already mapped.
+// Same type, same contents (zeros) as the reference's Matrix ctor.
+Matrix<double> result_matrix(std::int64_t rows, std::int64_t cols) {
+    constexpr std::size_t kBig = std::size_t(64) << 20;
+    const std::size_t n = static_cast<std::size_t>(rows * cols), bytes = n * sizeof(double);
+    if (bytes < kBig) return Matrix<double>(rows, cols);
+    Matrix<double> c;
+    c.data.reserve(n);
+    const std::size_t page = 4096;
+    const std::uintptr_t lo = (reinterpret_cast<std::uintptr_t>(c.data.data()) + page - 1) / page * page;
+    const std::uintptr_t hi = (reinterpret_cast<std::uintptr_t>(c.data.data()) + bytes) / page * page;
+    if (hi > lo) {
+#ifdef MADV_HUGEPAGE
+        madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
+#endif
+#ifndef MADV_POPULATE_WRITE
+#define MADV_POPULATE_WRITE 23
+#endif
+        const unsigned hw = std::thread::hardware_concurrency();
+        const std::size_t nt = std::min<std::size_t>(hw ? hw : 4, 16);
+        const std::size_t chunk = ((hi - lo) / nt + (std::size_t(2) << 20) - 1) / (std::size_t(2) << 20) * (std::size_t(2) << 20);
+        std::vector<std::thread> ts;
+        for (std::uintptr_t p = lo; p < hi; p += chunk) {
+            const std::size_t len = std::min<std::size_t>(chunk, hi - p);
+            ts.emplace_back([p, len] { madvise(reinterpret_cast<void*>(p), len, MADV_POPULATE_WRITE); });
+        }
+        for (auto& t : ts) t.join();
+    }
+    c.data.resize(n);
+    c.rows = rows;
+    c.cols = cols;
+    return c;
 }
 
 int prec_code(Precision p) { return p == Precision::Fp64 ? OZK_FP64 : OZK_FP32; }
@@ -132,7 +178,7 @@ EmulationResult run(const Matrix<T>& a, const Matrix<T>& b, const EmuConfig& cfg
     r.n_moduli = consts.n();
     r.mode = cfg.mode;
     r.precision = consts.precision;
-    r.c = Matrix<double>(a.rows, b.cols);
+    r.c = result_matrix(a.rows, b.cols);
     std::lock_guard<std::mutex> lock(g_mtx);
     check(ozk_gemm_host(handle_locked(), &c, a.rows, b.cols, a.cols, 1.0, a.data.data(), a.rows, b.data.data(),
                         b.rows, 0.0, r.c.data.data(), a.rows));

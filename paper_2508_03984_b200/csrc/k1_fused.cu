@@ -1,0 +1,505 @@
+// K1 in one pass over each operand: the line statistics, the line exponent
+// and the planes of the same data while it is still in L2 (reference:
+// scaling.cpp:20-133 and residue.cpp:7-42, as in k1_scale.cu / k1_residue.cu).
+//
+// The two-kernel K1 (stats kernel, then planes kernel) reads every FP64 input
+// twice from HBM: 16.1 GB per 16384^3 call against 11.8 GB of compulsory
+// bytes. Here the second read of a line comes from L2, because the planes of
+// a line are written right after its exponent is known:
+//
+//  * cols_fused_kernel — lines are contiguous columns (B, or A stored
+//    transposed): one 512-thread block per column (two per SM), a block-wide
+//    max / sum of squares, the exponent (exact sequential recompute of flagged
+//    lines by warp 0, k1_line.cuh), then the column again (evict-first) into
+//    its K-major planes. In flight: ~2 columns per SM, so a column is re-read
+//    after ~300 other columns' bytes (38 MB at k = 16384), well inside L2.
+//
+//  * rows_fused_kernel — lines are rows of a column-major operand (A, or B
+//    stored transposed): a row's statistics need all k columns, so the work
+//    is cut into 64-row x 128-column slices handed out by a ticket counter in
+//    group-major order. Statistics of slice t accumulate into per-row
+//    max / sum words (atomics; any summation order lies inside the guard band
+//    of the fast exponent, and flagged rows are recomputed exactly); the last
+//    slice of a 64-row group finalizes the group's exponents and publishes
+//    them with an epoch flag. Planes work is handed out by a second ticket
+//    counter that trails the first by D >= splits slices: a planes ticket is
+//    claimed only after the claimer's own statistics ticket is >= D, so every
+//    statistics slice of its group has already been claimed by a running
+//    block that never waits before finishing it — no deadlock whatever the
+//    residency — and with D ~ grid + splits the group is normally finished by
+//    then, so the wait is empty and the slice (64 KB) is re-read from L2.
+//
+// Bit-exactness is unchanged: the exponents come from the same finalize code
+// as the two-kernel path (guard band + exact recompute), and the plane bytes
+// from the same residue_planes8 / bound entries.
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+
+#include "k1_line.cuh"
+#include "ozk_device.cuh"
+
+namespace ozk {
+namespace {
+
+__device__ __forceinline__ uint64_t pol_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// 8 consecutive elements from a 32-byte aligned address, with an L2 policy
+__device__ __forceinline__ void load8h(const double* p, double (&v)[8], uint64_t pol) {
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                 : "l"(p), "l"(pol));
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=d"(v[4]), "=d"(v[5]), "=d"(v[6]), "=d"(v[7])
+                 : "l"(p + 4), "l"(pol));
+}
+__device__ __forceinline__ void load8h(const float* p, float (&v)[8], uint64_t pol) {
+    asm volatile("ld.global.nc.L2::cache_hint.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void load8(const double* p, double (&v)[8]) {
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                 : "l"(p));
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(v[4]), "=d"(v[5]), "=d"(v[6]), "=d"(v[7])
+                 : "l"(p + 4));
+}
+__device__ __forceinline__ void load8(const float* p, float (&v)[8]) {
+    asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(p));
+}
+
+// elements [i, i + 8) of a line (zeros past `len`); vector loads when aligned
+template <typename T>
+__device__ __forceinline__ void line8(const T* p, int64_t i, int64_t len, bool vec, T (&v)[8], uint64_t pol) {
+    if (vec && i + 8 <= len) {
+        load8h(p + i, v, pol);
+        return;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = i + u < len ? p[i + u] : T(0);
+}
+template <typename T>
+__device__ __forceinline__ void line8_first(const T* p, int64_t i, int64_t len, bool vec, T (&v)[8], uint64_t pol) {
+    if (vec && i + 8 <= len) {
+        load8h(p + i, v, pol);
+        return;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = i + u < len ? p[i + u] : T(0);
+}
+
+// Abar/Bbar entry (scaling.cpp:124-132), as in k1_residue.cu
+__device__ __forceinline__ uint32_t bound_entry(double x, int e) {
+    if (e == INT32_MIN) return 0;
+    const double v = (e >= -1022 && e <= 1023) ? __dmul_rn(fabs(x), pow2d(e)) : ldexp(fabs(x), e);
+    return static_cast<uint32_t>(__double2loint(__dadd_ru(v, 0x1.0p52))) & 0xffu;
+}
+
+// the planes (KIND 0: N residue planes; KIND 1: the bound plane) of 8
+// consecutive elements sharing one exponent column-wise (ex: per element)
+template <typename T, int KIND, int kMaxMod>
+__device__ __forceinline__ void write_planes8(const T (&v)[8], const int (&ex)[8], bool active, int8_t* dst0,
+                                              int64_t plane_stride, const DevConsts& c, uint64_t st_pol) {
+    if constexpr (KIND == 1) {
+        if (!active) return;
+        uint32_t b[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) b[u] = bound_entry(static_cast<double>(v[u]), ex[u]);
+        store_plane8<true>(dst0, make_uint2(pack_low_bytes(b[0], b[1], b[2], b[3]), pack_low_bytes(b[4], b[5], b[6], b[7])),
+                           st_pol);
+    } else {
+        T x[8];
+        bool fast = true;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            x[u] = trunc_scaled(v[u], ex[u]);
+            fast &= symmetric_residue_domain(static_cast<double>(x[u]), sizeof(T) == 4 ? OZK_FP32 : OZK_FP64, c.n);
+        }
+        fast = __all_sync(0xffffffffu, fast);  // warp-uniform branch inside residue_planes8
+        if (!active) return;
+        residue_planes8<T, kMaxMod, true>(x, fast, dst0, plane_stride, c, st_pol);
+    }
+}
+
+constexpr int kColThreads = 512;
+constexpr int kColWarps = kColThreads / 32;
+
+template <typename T, int KIND, int kMaxMod>
+__global__ void __launch_bounds__(kColThreads, 2)
+    cols_fused_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx, int vec,
+                      int32_t* __restrict__ nonfinite, const LineFinal F, const DevConsts c,
+                      int8_t* __restrict__ planes, int64_t ld, int64_t plane_stride) {
+    __shared__ double s_mx[kColWarps], s_sm[kColWarps];
+    __shared__ int s_e;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t extent = (rows + 15) / 16 * 16;  // plane_ld(rows)
+    // L2 priorities: first read evict_last (the line must survive until its
+    // planes pass), second read and the plane stores evict_first
+    const uint64_t pol = pol_evict_first(), pol_keep = pol_evict_last();
+    for (int64_t j = blockIdx.x; j < cols; j += gridDim.x) {
+        const T* col = x + j * ldx;
+        double mx = 0.0, s0 = 0.0, s1 = 0.0;
+        for (int64_t i = static_cast<int64_t>(tid) * 8; i < rows; i += 2 * 8 * kColThreads) {
+            T v0[8], v1[8];
+            line8(col, i, rows, vec, v0, pol_keep);
+            line8(col, i + 8 * kColThreads, rows, vec, v1, pol_keep);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const double a = static_cast<double>(v0[u]), b = static_cast<double>(v1[u]);
+                mx = fmax(mx, fmax(fabs(a), fabs(b)));
+                s0 = __fma_rn(a, a, s0);
+                s1 = __fma_rn(b, b, s1);
+            }
+        }
+        double sm = s0 + s1;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            sm += __shfl_xor_sync(0xffffffffu, sm, o);
+        }
+        if (lane == 0) {
+            s_mx[warp] = mx;
+            s_sm[warp] = sm;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            mx = lane < kColWarps ? s_mx[lane] : 0.0;
+            sm = lane < kColWarps ? s_sm[lane] : 0.0;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                sm += __shfl_xor_sync(0xffffffffu, sm, o);
+            }
+            // non-finite inputs (emulator.cpp:19-22): Inf in the max, NaN in the sum
+            if (lane == 0 && (isinf(mx) || isnan(sm))) atomicOr(nonfinite, 1);
+            const bool flag = __shfl_sync(0xffffffffu, lane == 0 ? finalize_line(F, j, mx, sm) : false, 0);
+            if (flag) exact_line(F, j, lane);
+            if (lane == 0) s_e = F.exp_out[j];  // this thread wrote it (finalize / exact_line)
+        }
+        __syncthreads();
+        const int e = s_e;
+        int ex[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) ex[u] = e;
+        // the planes, rows [0, extent): zero padding past `rows` (K2's 16-byte columns)
+        for (int64_t i0 = 0; i0 < extent; i0 += 8 * kColThreads) {
+            const int64_t i = i0 + static_cast<int64_t>(tid) * 8;
+            const bool active = i < extent;
+            T v[8];
+            line8_first(col, active ? i : 0, active ? rows : 0, vec, v, pol);
+            write_planes8<T, KIND, kMaxMod>(v, ex, active, planes + j * ld + i, plane_stride, c, pol);
+        }
+    }
+}
+
+// ---- rows ------------------------------------------------------------------
+constexpr int kRowThreads = 512;
+constexpr int kRowGroup = 64;  // rows per group (one exponent publication)
+constexpr int kSliceCols = 128;  // columns per slice (ticket): 64 KB of FP64 per slice
+
+struct RowsFusedState {
+    double* acc_max;      // [rows] non-negative max |x| bits (atomicMax on the encoding); zero between calls
+    double* acc_sum;      // [rows] sum x^2 (atomicAdd); zero between calls
+    int32_t* grp_cnt;     // [groups] finished statistics slices; zero between calls
+    uint32_t* grp_ready;  // [groups] epoch of the call whose exponents are published
+    uint32_t* tickets;    // [0] statistics, [1] planes; zero between calls
+};
+
+template <typename T, int KIND, int kMaxMod>
+__global__ void __launch_bounds__(kRowThreads, 2)
+    rows_fused_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx, int splits, int lag,
+                      uint32_t epoch, int32_t* __restrict__ nonfinite, const LineFinal F, const DevConsts c,
+                      int8_t* __restrict__ planes, int64_t ld, int64_t plane_stride, const RowsFusedState S) {
+    __shared__ double s_mx[kRowThreads / 32][kRowGroup];
+    __shared__ double s_sm[kRowThreads / 32][kRowGroup];
+    __shared__ int s_exp[kRowGroup];
+    __shared__ int s_flag[kRowGroup];
+    __shared__ int s_nflag, s_last;
+    __shared__ uint32_t s_t, s_p;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t groups = (rows + kRowGroup - 1) / kRowGroup;
+    const uint32_t total = static_cast<uint32_t>(groups * splits);
+    const int64_t extent = (rows + 15) / 16 * 16;  // plane_ld(rows)
+    const uint64_t pol = pol_evict_first(), pol_keep = pol_evict_last();
+    bool stats_left = true;
+    for (;;) {
+        if (tid == 0) {
+            s_t = stats_left ? atomicAdd(S.tickets, 1u) : total;
+            s_p = 0xffffffffu;
+            if (s_t >= static_cast<uint32_t>(lag) || s_t >= total) s_p = atomicAdd(S.tickets + 1, 1u);
+        }
+        __syncthreads();
+        const uint32_t t = s_t, p = s_p;
+        if (t >= total) stats_left = false;
+        if (t < total) {
+            // ---- statistics of slice t: rows [r0, r0 + 64), columns [h0, h1) ----
+            const int64_t g = t / splits;
+            const int64_t r0 = g * kRowGroup, h0 = static_cast<int64_t>(t % splits) * kSliceCols;
+            const int64_t h1 = h0 + kSliceCols < cols ? h0 + kSliceCols : cols;
+            const int64_t ra = r0 + 2 * lane;
+            double mx0 = 0.0, mx1 = 0.0, sa = 0.0, sb = 0.0;
+            if (ra + 1 < rows && (ldx & 1) == 0) {  // two adjacent rows per lane (8 / 16 B)
+#pragma unroll 8
+                for (int64_t h = h0 + warp; h < h1; h += kRowThreads / 32) {
+                    double a, b;
+                    if constexpr (sizeof(T) == 8) {
+                        asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                                     : "=d"(a), "=d"(b)
+                                     : "l"(x + ra + h * ldx), "l"(pol_keep));
+                    } else {
+                        float fa, fb;
+                        asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
+                                     : "=f"(fa), "=f"(fb)
+                                     : "l"(x + ra + h * ldx), "l"(pol_keep));
+                        a = fa;
+                        b = fb;
+                    }
+                    mx0 = fmax(mx0, fabs(a));
+                    mx1 = fmax(mx1, fabs(b));
+                    sa = __fma_rn(a, a, sa);
+                    sb = __fma_rn(b, b, sb);
+                }
+            } else {
+                for (int64_t h = h0 + warp; h < h1; h += kRowThreads / 32) {
+                    const double a = ra < rows ? static_cast<double>(x[ra + h * ldx]) : 0.0;
+                    const double b = ra + 1 < rows ? static_cast<double>(x[ra + 1 + h * ldx]) : 0.0;
+                    mx0 = fmax(mx0, fabs(a));
+                    mx1 = fmax(mx1, fabs(b));
+                    sa = __fma_rn(a, a, sa);
+                    sb = __fma_rn(b, b, sb);
+                }
+            }
+            if (__any_sync(0xffffffffu, isinf(mx0) || isinf(mx1) || isnan(sa + sb)) && lane == 0)
+                atomicOr(nonfinite, 1);
+            s_mx[warp][2 * lane] = mx0;
+            s_mx[warp][2 * lane + 1] = mx1;
+            s_sm[warp][2 * lane] = sa;
+            s_sm[warp][2 * lane + 1] = sb;
+            __syncthreads();
+            if (tid < kRowGroup && r0 + tid < rows) {
+                double M = s_mx[0][tid], Sm = s_sm[0][tid];
+#pragma unroll
+                for (int q = 1; q < kRowThreads / 32; ++q) {
+                    M = fmax(M, s_mx[q][tid]);
+                    Sm += s_sm[q][tid];
+                }
+                atomicMax(reinterpret_cast<unsigned long long*>(S.acc_max + r0 + tid),
+                          static_cast<unsigned long long>(__double_as_longlong(M)));
+                atomicAdd(S.acc_sum + r0 + tid, Sm);
+            }
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) {
+                s_last = atomicAdd(S.grp_cnt + g, 1) == splits - 1;
+                s_nflag = 0;
+            }
+            __syncthreads();
+            if (s_last) {
+                // ---- the group's last slice: finalize its exponents ----
+                __threadfence();
+                if (tid < kRowGroup && r0 + tid < rows) {
+                    const int64_t row = r0 + tid;
+                    const double M = __longlong_as_double(
+                        static_cast<long long>(atomicExch(reinterpret_cast<unsigned long long*>(S.acc_max + row), 0ull)));
+                    const double Sm = __longlong_as_double(static_cast<long long>(
+                        atomicExch(reinterpret_cast<unsigned long long*>(S.acc_sum + row), 0ull)));
+                    if (finalize_line(F, row, M, Sm)) s_flag[atomicAdd(&s_nflag, 1)] = tid;
+                }
+                __syncthreads();
+                for (int w = warp; w < s_nflag; w += kRowThreads / 32) exact_line(F, r0 + s_flag[w], lane);
+                __threadfence();
+                __syncthreads();
+                if (tid == 0) {
+                    S.grp_cnt[g] = 0;  // ready for the next call
+                    st_release(S.grp_ready + g, epoch);
+                }
+            }
+        }
+        if (p != 0xffffffffu) {
+            if (p >= total) {
+                // every block makes exactly one failing planes claim and then no
+                // claims at all: the last one resets both counters for the next call
+                if (tid == 0 && p == total + gridDim.x - 1) {
+                    S.tickets[0] = 0;
+                    S.tickets[1] = 0;
+                }
+                return;
+            }
+            // ---- planes of slice p ----
+            const int64_t g = p / splits;
+            const int64_t r0 = g * kRowGroup, h0 = static_cast<int64_t>(p % splits) * kSliceCols;
+            const int64_t h1 = h0 + kSliceCols < cols ? h0 + kSliceCols : cols;
+            if (tid == 0) {
+                // bounded: a group that never publishes (a corrupted state word)
+                // traps into a launch error instead of hanging the device
+                const unsigned long long t0 = globaltimer_ns();
+                while (ld_acquire(S.grp_ready + g) != epoch) {
+                    __nanosleep(64);
+                    if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+                }
+            }
+            __syncthreads();
+            if (tid < kRowGroup) s_exp[tid] = r0 + tid < rows ? __ldcg(F.exp_out + r0 + tid) : 0;
+            __syncthreads();
+            // 8 rows x 1 column per item: 8 items per column, kSliceCols columns
+            const bool vec_ok = (ldx % (32 / sizeof(T))) == 0 && (reinterpret_cast<uintptr_t>(x) & 31) == 0;
+#pragma unroll 1
+            for (int it = tid; it < kSliceCols * (kRowGroup / 8); it += kRowThreads) {
+                const int64_t h = h0 + it / (kRowGroup / 8);
+                const int64_t rr = r0 + (it % (kRowGroup / 8)) * 8;
+                const bool active = h < h1 && rr < extent;
+                T v[8];
+                const T* src = x + (active ? h : 0) * ldx + (active ? rr : 0);
+                if (active && vec_ok && rr + 8 <= rows) {
+                    load8h(src, v, pol);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = active && rr + u < rows ? src[u] : T(0);
+                }
+                int ex[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) ex[u] = s_exp[(it % (kRowGroup / 8)) * 8 + u];
+                write_planes8<T, KIND, kMaxMod>(v, ex, active, planes + h * ld + rr, plane_stride, c, pol);
+            }
+        }
+        __syncthreads();  // s_t / s_p / shared slices are reused
+    }
+}
+
+template <typename T, int KIND>
+void cols_dispatch(const T* x, int64_t rows, int64_t cols, int64_t ldx, int32_t* nonfinite, const LineFinal& F,
+                   const DevConsts& c, int8_t* planes, int64_t ld, int64_t stride, int num_sms, cudaStream_t s) {
+    const int vec = (reinterpret_cast<uintptr_t>(x) & 31) == 0 && (ldx * static_cast<int64_t>(sizeof(T))) % 32 == 0;
+    const int64_t grid = std::min<int64_t>(cols, 2 * static_cast<int64_t>(num_sms));
+#define OZK_K1F(MAXN)                                                                                        \
+    cols_fused_kernel<T, KIND, MAXN><<<static_cast<unsigned>(grid), kColThreads, 0, s>>>(x, rows, cols, ldx, \
+                                                                                         vec, nonfinite, F, c, \
+                                                                                         planes, ld, stride)
+    if (KIND == 1 || c.n <= 8)
+        OZK_K1F(8);
+    else if (c.n <= 12)
+        OZK_K1F(12);
+    else if (c.n <= 14)
+        OZK_K1F(14);
+    else if (c.n <= 16)
+        OZK_K1F(16);
+    else
+        OZK_K1F(OZK_MAX_MODULI);
+#undef OZK_K1F
+}
+
+template <typename T, int KIND>
+void rows_dispatch(const T* x, int64_t rows, int64_t cols, int64_t ldx, uint32_t epoch, int32_t* nonfinite,
+                   const LineFinal& F, const DevConsts& c, int8_t* planes, int64_t ld, int64_t stride,
+                   const RowsFusedState& S, int num_sms, cudaStream_t s) {
+    const int splits = static_cast<int>((cols + kSliceCols - 1) / kSliceCols);
+    const int64_t groups = (rows + kRowGroup - 1) / kRowGroup;
+    const int64_t total = groups * splits;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rows_fused_kernel<T, KIND, 8>, kRowThreads, 0);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t grid = std::min<int64_t>(total, static_cast<int64_t>(per_sm) * num_sms);
+    // planes trail statistics by about one grid of slices plus one group
+    // (OZK_K1_LAG: that many slices instead, never below one group)
+    int64_t lag = grid + splits;
+    if (const char* e = std::getenv("OZK_K1_LAG")) lag = std::max<int64_t>(splits, std::atoll(e));
+    lag = std::min<int64_t>(total, lag);
+#define OZK_K1F(MAXN)                                                                                          \
+    rows_fused_kernel<T, KIND, MAXN><<<static_cast<unsigned>(grid), kRowThreads, 0, s>>>(                      \
+        x, rows, cols, ldx, splits, static_cast<int>(lag), epoch, nonfinite, F, c, planes, ld, stride, S)
+    if (KIND == 1 || c.n <= 8)
+        OZK_K1F(8);
+    else if (c.n <= 12)
+        OZK_K1F(12);
+    else if (c.n <= 14)
+        OZK_K1F(14);
+    else if (c.n <= 16)
+        OZK_K1F(16);
+    else
+        OZK_K1F(OZK_MAX_MODULI);
+#undef OZK_K1F
+}
+
+}  // namespace
+
+size_t rows_fused_state_bytes(int64_t rows) {
+    const int64_t groups = (rows + kRowGroup - 1) / kRowGroup;
+    return sizeof(double) * 2 * static_cast<size_t>(rows) + sizeof(int32_t) * 2 * static_cast<size_t>(groups) + 64;
+}
+
+void launch_cols_fused(const void* x, int is_f32, int64_t rows, int64_t cols, int64_t ldx, int32_t* nonfinite,
+                       const LineFinal& F, const DevConsts& c, int kind, int8_t* planes, int64_t ld, int64_t stride,
+                       int num_sms, cudaStream_t s) {
+    if (is_f32) {
+        if (kind == 0)
+            cols_dispatch<float, 0>(static_cast<const float*>(x), rows, cols, ldx, nonfinite, F, c, planes, ld, stride,
+                                    num_sms, s);
+        else
+            cols_dispatch<float, 1>(static_cast<const float*>(x), rows, cols, ldx, nonfinite, F, c, planes, ld, stride,
+                                    num_sms, s);
+    } else {
+        if (kind == 0)
+            cols_dispatch<double, 0>(static_cast<const double*>(x), rows, cols, ldx, nonfinite, F, c, planes, ld,
+                                     stride, num_sms, s);
+        else
+            cols_dispatch<double, 1>(static_cast<const double*>(x), rows, cols, ldx, nonfinite, F, c, planes, ld,
+                                     stride, num_sms, s);
+    }
+}
+
+void launch_rows_fused(const void* x, int is_f32, int64_t rows, int64_t cols, int64_t ldx, uint32_t epoch,
+                       void* state, int32_t* nonfinite, const LineFinal& F, const DevConsts& c, int kind,
+                       int8_t* planes, int64_t ld, int64_t stride, int num_sms, cudaStream_t s) {
+    const int64_t groups = (rows + kRowGroup - 1) / kRowGroup;
+    RowsFusedState S;
+    S.acc_max = static_cast<double*>(state);
+    S.acc_sum = S.acc_max + rows;
+    S.grp_cnt = reinterpret_cast<int32_t*>(S.acc_sum + rows);
+    S.grp_ready = reinterpret_cast<uint32_t*>(S.grp_cnt + groups);
+    S.tickets = S.grp_ready + groups;
+    if (is_f32) {
+        if (kind == 0)
+            rows_dispatch<float, 0>(static_cast<const float*>(x), rows, cols, ldx, epoch, nonfinite, F, c, planes, ld,
+                                    stride, S, num_sms, s);
+        else
+            rows_dispatch<float, 1>(static_cast<const float*>(x), rows, cols, ldx, epoch, nonfinite, F, c, planes, ld,
+                                    stride, S, num_sms, s);
+    } else {
+        if (kind == 0)
+            rows_dispatch<double, 0>(static_cast<const double*>(x), rows, cols, ldx, epoch, nonfinite, F, c, planes,
+                                     ld, stride, S, num_sms, s);
+        else
+            rows_dispatch<double, 1>(static_cast<const double*>(x), rows, cols, ldx, epoch, nonfinite, F, c, planes,
+                                     ld, stride, S, num_sms, s);
+    }
+}
+
+}  // namespace ozk

@@ -66,6 +66,7 @@ struct K2Params {
     int p[OZK_MAX_MODULI];
     int pinv[OZK_MAX_MODULI];
     int group;             // tile rows per raster group
+    int order;             // 1: moduli inner per wave of tiles (fused-K3 schedule prototype)
     int snake;             // odd groups sweep the columns right to left (B panels reused across the group edge)
     int hints;             // bit 0: A loads evict_last, bit 1: B loads evict_last, bit 3: B loads
                            // evict_first (bit 2, streaming U stores, measured no gain: removed)
@@ -264,13 +265,29 @@ __host__ __device__ constexpr uint32_t idesc_i8() {
            (static_cast<uint32_t>(Cfg<CG>::kTileN >> 3) << 17) | (static_cast<uint32_t>(Cfg<CG>::kTileM >> 4) << 24);
 }
 
-// work item t -> (modulus, tile row, tile column), grouped raster of 8 tile
-// rows per modulus so the co-resident tiles share A/B panels in L2
+// work item t -> (modulus, tile row, tile column), grouped raster of G tile
+// rows per modulus so the co-resident tiles share A/B panels in L2.
+// order 1 (OZK_K2_ORDER=1, the schedule a K3 fused into K2's epilogue would
+// need: every cluster runs all moduli of its tile back to back, so a tile's N
+// residues meet on chip): waves of W = nclusters tiles, moduli inner — cluster
+// c takes tile (wave * W + c) for modulus 0, 1, ..., N-1. Kept as a measured
+// prototype of that schedule's DRAM cost ("Not fused").
 __device__ __forceinline__ void decode_tile(int t, int tiles_m, int tiles_n, int G, int snake, int& mod, int& tm,
-                                            int& tn) {
+                                            int& tn, int order = 0, int n_mod = 1, int W = 1) {
     const int per_mod = tiles_m * tiles_n;
-    mod = t / per_mod;
-    const int r = t - mod * per_mod;
+    int r;
+    if (order == 1) {
+        const int span = W * n_mod;
+        const int wave = t / span;
+        const int base = wave * W;
+        const int rem = per_mod - base < W ? per_mod - base : W;
+        const int idx = t - wave * span;
+        mod = idx / rem;
+        r = base + idx % rem;
+    } else {
+        mod = t / per_mod;
+        r = t - mod * per_mod;
+    }
     const int group = r / (G * tiles_n);
     const int first = group * G;
     const int gsize = tiles_m - first < G ? tiles_m - first : G;
@@ -380,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             __syncwarp();
             int mod, tm, tn;
-            decode_tile(t, P.tiles_m, P.tiles_n, P.group, P.snake, mod, tm, tn);
+            decode_tile(t, P.tiles_m, P.tiles_n, P.group, P.snake, mod, tm, tn, P.order, P.n_mod, nclusters);
             const int m0 = tm * C::kTileM + static_cast<int>(rank) * C::kBM;
             const int n0 = tn * C::kTileN + static_cast<int>(rank) * C::kBRows;
             for (int kb = 0; kb < P.num_kb; ++kb) {
@@ -486,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int acc = lt & 1;
             const uint32_t acc_phase = (lt >> 1) & 1;
             int mod, tm, tn;
-            decode_tile(t, P.tiles_m, P.tiles_n, P.group, P.snake, mod, tm, tn);
+            decode_tile(t, P.tiles_m, P.tiles_n, P.group, P.snake, mod, tm, tn, P.order, P.n_mod, nclusters);
             mbar_wait(smem_u32(tfull + acc), acc_phase);
             tc_fence_after();
             const int row = tm * C::kTileM + static_cast<int>(rank) * C::kBM + q * 32 + lane;
@@ -660,6 +677,7 @@ int launch_impl(const K2Launch& L, cudaStream_t s) {
     }
     P.group = std::max(1, env_int("OZK_K2_GROUP", 8));
     P.snake = env_int("OZK_K2_SNAKE", 1);  // serpentine raster: -1.3 GB DRAM per launch, +0.5 % in the bench (DESIGN)
+    P.order = env_int("OZK_K2_ORDER", 0);  // 1: moduli-inner waves (fused-K3 schedule prototype)
     P.hints = env_int("OZK_K2_HINTS", 9);  // A evict_last, B evict_first (profiles/r01_k2_hints_sweep.md)
     // Lockstep (default on): co-resident clusters that share A/B panels stay
     // within one tile of each other, so the panels they all stream are still in

@@ -83,9 +83,19 @@ __device__ __forceinline__ uint32_t literal_byte(T x, const DevConsts& c, int t)
 // dst0 + t * plane_stride. fast (warp-uniform): every x of the warp lies in
 // the symmetric-residue domain (one DFMA + one IMAD per element and modulus,
 // bytes packed by IMADs); else the literal rmod_fast sequence.
-template <typename T, int kMaxMod>
+// 8-byte plane store, optionally with an L2 eviction-priority policy
+template <bool kHint>
+__device__ __forceinline__ void store_plane8(int8_t* p, uint2 w, uint64_t pol) {
+    if constexpr (kHint)
+        asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(w.x), "r"(w.y), "l"(pol)
+                     : "memory");
+    else
+        *reinterpret_cast<uint2*>(p) = w;
+}
+
+template <typename T, int kMaxMod, bool kHint = false>
 __device__ __forceinline__ void residue_planes8(const T (&x)[8], bool fast, int8_t* dst0, int64_t plane_stride,
-                                                const DevConsts& c) {
+                                                const DevConsts& c, uint64_t st_pol = 0) {
     constexpr int kBPerThread = 8;
     uint32_t xlo[kBPerThread];
 #pragma unroll
@@ -120,7 +130,7 @@ __device__ __forceinline__ void residue_planes8(const T (&x)[8], bool fast, int8
                     }
                     word = make_uint2(w[0] ^ 0x80808080u, w[1] ^ 0x80808080u);
                 }
-                *reinterpret_cast<uint2*>(dst) = word;
+                store_plane8<kHint>(dst, word, st_pol);
                 dst += plane_stride;
             }
         }
@@ -130,8 +140,9 @@ __device__ __forceinline__ void residue_planes8(const T (&x)[8], bool fast, int8
             uint32_t v[kBPerThread];
 #pragma unroll
             for (int u = 0; u < kBPerThread; ++u) v[u] = literal_byte(x[u], c, t);
-            *reinterpret_cast<uint2*>(dst0 + t * plane_stride) =
-                make_uint2(pack_low_bytes(v[0], v[1], v[2], v[3]), pack_low_bytes(v[4], v[5], v[6], v[7]));
+            store_plane8<kHint>(dst0 + t * plane_stride,
+                                make_uint2(pack_low_bytes(v[0], v[1], v[2], v[3]), pack_low_bytes(v[4], v[5], v[6], v[7])),
+                                st_pol);
         }
     }
 }

@@ -1,0 +1,136 @@
+"""GPU parity of the one-pass K1 (csrc/k1_fused.cu): statistics, exponents and
+planes of each operand in one read from HBM.
+
+The fused kernels are the default for ozk_gemm whenever the whole problem is
+one panel (and for the accurate-mode bound planes), so the rest of the GPU
+suite already runs through them; these cases aim at their own boundaries:
+the 64-row groups and 64-column slices of the row kernel (ragged rows and
+columns, a single slice, many groups), the 512-thread column kernel (columns
+shorter and longer than one block pass, lengths off the 8-element vectors),
+both operand storages (the row kernel serves A and a transposed B, the
+column kernel B and a transposed A), FP32 operands, accurate mode (bound
+planes), flagged lines (exact recompute inside the fused finalize), the
+self-resetting ticket / accumulator state across many calls of different
+shapes on one handle, and non-finite detection. Every result must equal the
+oracle bit for bit (reference emulator.cpp:25-78).
+"""
+import numpy as np
+import pytest
+
+from paper_2508_03984_b200 import EmuConfig, InputError, Precision, ScaleMode, gen_matrix
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _bits(x):
+    return np.ascontiguousarray(x).view(np.int64 if x.dtype == np.float64 else np.int32)
+
+
+def _dev(x: np.ndarray, ld: int | None = None):
+    """host matrix -> column-major CUDA view with leading dimension ld (NaN padding)"""
+    rows, cols = x.shape
+    ld = rows if ld is None else ld
+    buf = np.full((cols, ld), np.nan, dtype=x.dtype)
+    buf[:, :rows] = x.T
+    return torch.from_numpy(buf).cuda().t()[:rows]
+
+
+def _run(ctx, a, b, cfg, ta=False, tb=False, lda=None, ldb=None):
+    m, n = a.shape[0], b.shape[1]
+    A = _dev(np.asfortranarray(a.T) if ta else a, lda)
+    B = _dev(np.asfortranarray(b.T) if tb else b, ldb)
+    C = _dev(np.zeros((m, n)))
+    ctx.gemm(A, B, cfg, C, trans_a=ta, trans_b=tb)
+    return C.cpu().numpy()
+
+
+# row groups of 64 and column slices of 64 (row kernel); 4096-element block
+# passes and 8-element vectors (column kernel)
+SHAPES = [(1, 1, 1), (63, 65, 64), (64, 64, 65), (65, 130, 129), (200, 7, 4097), (1000, 300, 8191),
+          (2049, 64, 6000), (130, 2050, 1000)]
+
+
+@pytest.mark.parametrize("m,n,k", SHAPES)
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, True)])
+@pytest.mark.parametrize("mode", [ScaleMode.Fast, ScaleMode.Accurate])
+def test_fused_k1_shapes(ctx, oracle, m, n, k, ta, tb, mode):
+    a = gen_matrix(m, k, 1.0, 11 + m)
+    b = gen_matrix(k, n, 1.0, 12 + n)
+    got = _run(ctx, a, b, EmuConfig(n_moduli=14, mode=mode), ta, tb)
+    np.testing.assert_array_equal(_bits(got), _bits(oracle.gemm(a, b, 14, int(mode))))
+
+
+@pytest.mark.parametrize("lda_pad,ldb_pad", [(1, 0), (0, 1), (2, 3), (8, 8)])
+def test_fused_k1_leading_dimensions(ctx, oracle, lda_pad, ldb_pad):
+    """odd leading dimensions take the two-kernel rows path, even ones the fused one"""
+    m, n, k = 190, 77, 1500
+    a = gen_matrix(m, k, 0.5, 21)
+    b = gen_matrix(k, n, 0.5, 22)
+    got = _run(ctx, a, b, EmuConfig(n_moduli=16), lda=m + lda_pad, ldb=k + ldb_pad)
+    np.testing.assert_array_equal(_bits(got), _bits(oracle.gemm(a, b, 16, 0)))
+
+
+@pytest.mark.parametrize("N,mode", [(8, ScaleMode.Fast), (10, ScaleMode.Accurate), (6, ScaleMode.Fast)])
+def test_fused_k1_fp32(ctx, oracle, N, mode):
+    m, n, k = 321, 190, 2500
+    a = gen_matrix(m, k, 0.5, 31).astype(np.float32)
+    b = gen_matrix(k, n, 0.5, 32).astype(np.float32)
+    cfg = EmuConfig(n_moduli=N, mode=mode, precision=Precision.Fp32)
+    A, B = _dev(a), _dev(b)
+    C = _dev(np.zeros((m, n)))
+    ctx.gemm(A, B, cfg, C)
+    want = oracle.gemm(a, b, N, int(mode), prec=1)
+    np.testing.assert_array_equal(_bits(C.cpu().numpy()), _bits(want))
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, True)])
+def test_fused_k1_flagged_lines(ctx, oracle, ta, tb):
+    """rows / columns whose maxima leave the a^2-safe range take the exact
+    sequential recompute inside the fused finalize (row groups: the last slice's
+    block; columns: warp 0 of the column's block)"""
+    m, n, k = 190, 130, 3000
+    a = gen_matrix(m, k, 0.5, 41)
+    b = gen_matrix(k, n, 0.5, 42)
+    a[[3, 70, m - 1], :] *= 2.0 ** -450
+    a[[9, 100], :] *= 2.0 ** 510
+    b[:, [0, 64, n - 1]] *= 2.0 ** -450
+    b[:, [11]] *= 2.0 ** 505
+    got = _run(ctx, a, b, EmuConfig(n_moduli=14), ta, tb)
+    np.testing.assert_array_equal(_bits(got), _bits(oracle.gemm(a, b, 14, 0)))
+
+
+def test_fused_k1_state_across_calls(ctx, oracle):
+    """the ticket counters, row accumulators and group counters reset
+    themselves; the group flags are per-call epochs — so many calls of changing
+    shapes on one handle (both K1 streams) stay exact"""
+    rng = np.random.default_rng(5)
+    for it in range(24):
+        m, n, k = (int(v) for v in rng.integers(1, 700, size=3))
+        mode = ScaleMode(int(rng.integers(0, 2)))
+        ta, tb = bool(rng.integers(0, 2)), bool(rng.integers(0, 2))
+        a = gen_matrix(m, k, 1.0, 100 + it)
+        b = gen_matrix(k, n, 1.0, 200 + it)
+        got = _run(ctx, a, b, EmuConfig(n_moduli=13, mode=mode), ta, tb)
+        np.testing.assert_array_equal(_bits(got), _bits(oracle.gemm(a, b, 13, int(mode))),
+                                      err_msg=f"call {it}: {m}x{n}x{k} {mode.name} ta={ta} tb={tb}")
+
+
+@pytest.mark.parametrize("where", ["a_row", "b_col"])
+@pytest.mark.parametrize("bad", [np.inf, np.nan])
+@pytest.mark.parametrize("trans", [False, True])
+def test_fused_k1_nonfinite(ctx, where, bad, trans):
+    m, n, k = 150, 90, 700
+    a = gen_matrix(m, k, 0.5, 51)
+    b = gen_matrix(k, n, 0.5, 52)
+    if where == "a_row":
+        a[77, 300] = bad
+    else:
+        b[650, 45] = bad
+    with pytest.raises(InputError):
+        _run(ctx, a, b, EmuConfig(n_moduli=14), trans, trans)
+    # the handle is still usable afterwards (state reset by the failing call's kernels)
+    a2 = gen_matrix(m, k, 0.5, 53)
+    b2 = gen_matrix(k, n, 0.5, 54)
+    _run(ctx, a2, b2, EmuConfig(n_moduli=14), trans, trans)
