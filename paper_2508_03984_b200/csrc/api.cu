@@ -600,14 +600,22 @@ int stage_col_residues(ozk_context* h, Job& J, int64_t j0, int64_t nj, const int
 // ---- one-pass K1 (k1_fused.cu) ---------------------------------------------------
 // The line statistics, the exponents and the planes in one pass over an operand
 // (fast mode: the residue planes; accurate mode: the bound plane Abar / Bbar).
-// OZK_K1_FUSED=0 selects the two-kernel path (stats kernel, then planes kernel).
-bool k1_fused_enabled() {
+// OZK_K1_FUSED is a mask of the one-pass kernels to use: bit 0 the column
+// kernel (contiguous lines: B, or a transposed A), bit 1 the row kernel
+// (strided lines: A, or a transposed B); 0 selects the two-kernel path (stats
+// kernel, then planes kernel) everywhere. Default 1: in the bench step the
+// column kernel wins (1.01 vs 0.34 + 0.94 ms at 16384^2) and the row kernel
+// loses (1.57 vs 0.39 + 0.94 ms).
+int k1_fused_mask() {
     static const int v = [] {
         const char* e = std::getenv("OZK_K1_FUSED");
         return e && *e ? std::atoi(e) : 1;
     }();
-    return v != 0;
+    return v;
 }
+bool k1_fused_enabled() { return k1_fused_mask() != 0; }
+bool cols_fused_on() { return (k1_fused_mask() & 1) != 0; }
+bool rows_fused_on() { return (k1_fused_mask() & 2) != 0; }
 
 // the row kernel reads two adjacent rows per lane (16 / 8-byte vectors)
 bool rows_fusable(const void* x, int64_t ld) { return (reinterpret_cast<uintptr_t>(x) & 15) == 0 && ld % 2 == 0; }
@@ -632,7 +640,7 @@ int fused_state(ozk_context* h, const Job& J, void** sa, void** sb) {
 }
 
 // op(A)'s rows in one pass: mu and its residue planes (fast), or mu' and Abar (accurate)
-bool a_fusable(const Job& J) { return k1_fused_enabled() && (J.ta || rows_fusable(J.a, J.lda)); }
+bool a_fusable(const Job& J) { return J.ta ? cols_fused_on() : rows_fused_on() && rows_fusable(J.a, J.lda); }
 int stage_rows_fused(ozk_context* h, Job& J, void* state) {
     const bool fast = J.mode == OZK_FAST;
     const LineFinal F = line_final(J, fast ? J.mu : J.ma, fast ? nullptr : J.rowmax, J.a, J.ta ? J.lda : 1,
@@ -649,7 +657,9 @@ int stage_rows_fused(ozk_context* h, Job& J, void* state) {
 }
 
 // columns [j0, j0+nj) of op(B) in one pass: nu and its planes (fast), or nu' and Bbar (accurate)
-bool b_fusable(const Job& J, int64_t j0) { return k1_fused_enabled() && (!J.tb || rows_fusable(b_block(J, j0), J.ldb)); }
+bool b_fusable(const Job& J, int64_t j0) {
+    return !J.tb ? cols_fused_on() : rows_fused_on() && rows_fusable(b_block(J, j0), J.ldb);
+}
 int stage_cols_fused(ozk_context* h, Job& J, int64_t j0, int64_t nj, void* state) {
     const bool fast = J.mode == OZK_FAST;
     const void* bj = b_block(J, j0);
@@ -1028,11 +1038,11 @@ int gemm_device(ozk_context* h, const ozk_config* cfg, const ozk_constants& c, i
             }
             return OZK_OK;
         };
-        // the one-pass kernels each fill the GPU and keep their lines in L2
-        // until the planes pass: concurrent, they evict each other's lines
-        // (measured: 3.3 ms together vs 2.6 ms back to back at 16384^2), so
-        // after a one-pass A the B chain follows on the same stream
-        if (fa) {
+        // two one-pass kernels each fill the GPU and keep their lines in L2
+        // until the planes pass: after a one-pass A a one-pass B follows on
+        // the same stream; otherwise the chains overlap on two streams
+        static const bool one_stream = std::getenv("OZK_K1_ONE_STREAM") != nullptr;  // A/B timing knob
+        if (one_stream || (fa && (J.tb ? rows_fused_on() : cols_fused_on()))) {
             OZK_TRY(b_chain());
         } else {
             {

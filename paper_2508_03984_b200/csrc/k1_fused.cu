@@ -204,6 +204,11 @@ __global__ void __launch_bounds__(kColThreads, 2)
             if (flag) exact_line(F, j, lane);
             if (lane == 0) s_e = F.exp_out[j];  // this thread wrote it (finalize / exact_line)
         }
+        // the first planes chunk is loaded before the exponent is known: its
+        // L2 latency overlaps warp 0's finalize instead of following it
+        const int64_t i_first = static_cast<int64_t>(tid) * 8;
+        T vn[8];
+        line8_first(col, i_first < extent ? i_first : 0, i_first < extent ? rows : 0, vec, vn, pol);
         __syncthreads();
         const int e = s_e;
         int ex[8];
@@ -214,7 +219,11 @@ __global__ void __launch_bounds__(kColThreads, 2)
             const int64_t i = i0 + static_cast<int64_t>(tid) * 8;
             const bool active = i < extent;
             T v[8];
-            line8_first(col, active ? i : 0, active ? rows : 0, vec, v, pol);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = vn[u];
+            const int64_t inext = i + 8 * kColThreads;  // the next chunk in flight during this one's arithmetic
+            if (i0 + 8 * kColThreads < extent)
+                line8_first(col, inext < extent ? inext : 0, inext < extent ? rows : 0, vec, vn, pol);
             write_planes8<T, KIND, kMaxMod>(v, ex, active, planes + j * ld + i, plane_stride, c, pol);
         }
     }

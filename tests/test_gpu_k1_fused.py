@@ -1,10 +1,12 @@
 """GPU parity of the one-pass K1 (csrc/k1_fused.cu): statistics, exponents and
 planes of each operand in one read from HBM.
 
-The fused kernels are the default for ozk_gemm whenever the whole problem is
-one panel (and for the accurate-mode bound planes), so the rest of the GPU
-suite already runs through them; these cases aim at their own boundaries:
-the 64-row groups and 64-column slices of the row kernel (ragged rows and
+The column kernel is the default for ozk_gemm's contiguous lines whenever the
+whole problem is one panel (and for the accurate-mode bound planes), so the
+rest of the GPU suite already runs through it; the row kernel is opt-in
+(OZK_K1_FUSED=3) and this module runs once more with it on (the last test).
+These cases aim at the kernels' own boundaries:
+the 64-row groups and 128-column slices of the row kernel (ragged rows and
 columns, a single slice, many groups), the 512-thread column kernel (columns
 shorter and longer than one block pass, lengths off the 8-element vectors),
 both operand storages (the row kernel serves A and a transposed B, the
@@ -134,3 +136,16 @@ def test_fused_k1_nonfinite(ctx, where, bad, trans):
     a2 = gen_matrix(m, k, 0.5, 53)
     b2 = gen_matrix(k, n, 0.5, 54)
     _run(ctx, a2, b2, EmuConfig(n_moduli=14), trans, trans)
+
+
+def test_row_kernel_enabled_subprocess():
+    """The one-pass row kernel is opt-in (OZK_K1_FUSED=3; the default mask 1
+    uses only the column kernel): this module again with both kernels on."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, OZK_K1_FUSED="3")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", __file__,
+                        "-k", "not subprocess"], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
