@@ -16,18 +16,19 @@
 //
 //  * rows_fused_kernel — lines are rows of a column-major operand (A, or B
 //    stored transposed): a row's statistics need all k columns, so the work
-//    is cut into 64-row x 128-column slices handed out by a ticket counter in
-//    group-major order. Statistics of slice t accumulate into per-row
-//    max / sum words (atomics; any summation order lies inside the guard band
-//    of the fast exponent, and flagged rows are recomputed exactly); the last
-//    slice of a 64-row group finalizes the group's exponents and publishes
-//    them with an epoch flag. Planes work is handed out by a second ticket
-//    counter that trails the first by D >= splits slices: a planes ticket is
-//    claimed only after the claimer's own statistics ticket is >= D, so every
-//    statistics slice of its group has already been claimed by a running
-//    block that never waits before finishing it — no deadlock whatever the
-//    residency — and with D ~ grid + splits the group is normally finished by
-//    then, so the wait is empty and the slice (64 KB) is re-read from L2.
+//    is cut into 64-row x 128-column slices handed out by ticket counters in
+//    group-major order, to two warp-specialised roles per block. Statistics
+//    of a slice accumulate into per-row max / sum words (atomics; any
+//    summation order lies inside the guard band of the fast exponent, and
+//    flagged rows are recomputed exactly); the last slice of a 64-row group
+//    finalizes the group's exponents and publishes them with an epoch flag.
+//    The planes role claims slices from a second counter and waits for its
+//    group's flag; the statistics role stays within `lag` (>= one group) slices
+//    of the planes counter, so the slice (64 KB) is re-read from L2 (~16 MB
+//    between the two reads at k = 16384), and — since a planes ticket that far
+//    behind belongs to a group whose statistics slices are all claimed, and a
+//    claimed statistics slice finishes without waiting — nothing deadlocks
+//    whatever the residency.
 //
 // Bit-exactness is unchanged: the exponents come from the same finalize code
 // as the two-kernel path (guard band + exact recompute), and the plane bytes
@@ -239,36 +240,56 @@ struct RowsFusedState {
     double* acc_sum;      // [rows] sum x^2 (atomicAdd); zero between calls
     int32_t* grp_cnt;     // [groups] finished statistics slices; zero between calls
     uint32_t* grp_ready;  // [groups] epoch of the call whose exponents are published
-    uint32_t* tickets;    // [0] statistics, [1] planes; zero between calls
+    uint32_t* tickets;    // [0] statistics, [1] planes, [2] finished roles; zero between calls
 };
 
+__device__ __forceinline__ void role_sync(int id) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kRowThreads / 2) : "memory");
+}
+
+// Warp-specialised: warps 0-7 run statistics tickets, warps 8-15 planes
+// tickets, each role with its own named barrier, so one role's
+// synchronisation (reductions, atomics, the group finalize, the wait for a
+// group's exponents) never stalls the other role's memory stream.
 template <typename T, int KIND, int kMaxMod>
 __global__ void __launch_bounds__(kRowThreads, 2)
     rows_fused_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx, int splits, int lag,
                       uint32_t epoch, int32_t* __restrict__ nonfinite, const LineFinal F, const DevConsts c,
                       int8_t* __restrict__ planes, int64_t ld, int64_t plane_stride, const RowsFusedState S) {
-    __shared__ double s_mx[kRowThreads / 32][kRowGroup];
-    __shared__ double s_sm[kRowThreads / 32][kRowGroup];
+    constexpr int kRoleThreads = kRowThreads / 2, kRoleWarps = kRoleThreads / 32;
+    __shared__ double s_mx[kRoleWarps][kRowGroup];
+    __shared__ double s_sm[kRoleWarps][kRowGroup];
     __shared__ int s_exp[kRowGroup];
     __shared__ int s_flag[kRowGroup];
     __shared__ int s_nflag, s_last;
     __shared__ uint32_t s_t, s_p;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const bool stats_role = tid < kRoleThreads;
+    const int rt = stats_role ? tid : tid - kRoleThreads;  // thread index inside the role
+    const int rw = rt >> 5;                                  // warp index inside the role
     const int64_t groups = (rows + kRowGroup - 1) / kRowGroup;
     const uint32_t total = static_cast<uint32_t>(groups * splits);
     const int64_t extent = (rows + 15) / 16 * 16;  // plane_ld(rows)
     const uint64_t pol = pol_evict_first(), pol_keep = pol_evict_last();
-    bool stats_left = true;
-    for (;;) {
-        if (tid == 0) {
-            s_t = stats_left ? atomicAdd(S.tickets, 1u) : total;
-            s_p = 0xffffffffu;
-            if (s_t >= static_cast<uint32_t>(lag) || s_t >= total) s_p = atomicAdd(S.tickets + 1, 1u);
-        }
-        __syncthreads();
-        const uint32_t t = s_t, p = s_p;
-        if (t >= total) stats_left = false;
-        if (t < total) {
+    if (stats_role) {
+        for (;;) {
+            if (rt == 0) {
+                // stay within `lag` slices of the planes: the slices between a
+                // statistics read and its planes re-read must fit in L2. No
+                // deadlock for lag >= splits: a planes ticket below
+                // (statistics counter - lag) belongs to a group whose statistics
+                // slices are all claimed already, and claimed statistics slices
+                // finish without waiting, so the planes counter keeps moving.
+                const unsigned long long t0 = globaltimer_ns();
+                while (ld_acquire(S.tickets) > ld_acquire(S.tickets + 1) + static_cast<uint32_t>(lag)) {
+                    __nanosleep(256);
+                    if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+                }
+                s_t = atomicAdd(S.tickets, 1u);
+            }
+            role_sync(1);
+            const uint32_t t = s_t;
+            if (t >= total) break;
             // ---- statistics of slice t: rows [r0, r0 + 64), columns [h0, h1) ----
             const int64_t g = t / splits;
             const int64_t r0 = g * kRowGroup, h0 = static_cast<int64_t>(t % splits) * kSliceCols;
@@ -277,7 +298,7 @@ __global__ void __launch_bounds__(kRowThreads, 2)
             double mx0 = 0.0, mx1 = 0.0, sa = 0.0, sb = 0.0;
             if (ra + 1 < rows && (ldx & 1) == 0) {  // two adjacent rows per lane (8 / 16 B)
 #pragma unroll 8
-                for (int64_t h = h0 + warp; h < h1; h += kRowThreads / 32) {
+                for (int64_t h = h0 + rw; h < h1; h += kRoleWarps) {
                     double a, b;
                     if constexpr (sizeof(T) == 8) {
                         asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
@@ -297,7 +318,7 @@ __global__ void __launch_bounds__(kRowThreads, 2)
                     sb = __fma_rn(b, b, sb);
                 }
             } else {
-                for (int64_t h = h0 + warp; h < h1; h += kRowThreads / 32) {
+                for (int64_t h = h0 + rw; h < h1; h += kRoleWarps) {
                     const double a = ra < rows ? static_cast<double>(x[ra + h * ldx]) : 0.0;
                     const double b = ra + 1 < rows ? static_cast<double>(x[ra + 1 + h * ldx]) : 0.0;
                     mx0 = fmax(mx0, fabs(a));
@@ -308,80 +329,79 @@ __global__ void __launch_bounds__(kRowThreads, 2)
             }
             if (__any_sync(0xffffffffu, isinf(mx0) || isinf(mx1) || isnan(sa + sb)) && lane == 0)
                 atomicOr(nonfinite, 1);
-            s_mx[warp][2 * lane] = mx0;
-            s_mx[warp][2 * lane + 1] = mx1;
-            s_sm[warp][2 * lane] = sa;
-            s_sm[warp][2 * lane + 1] = sb;
-            __syncthreads();
-            if (tid < kRowGroup && r0 + tid < rows) {
-                double M = s_mx[0][tid], Sm = s_sm[0][tid];
+            s_mx[rw][2 * lane] = mx0;
+            s_mx[rw][2 * lane + 1] = mx1;
+            s_sm[rw][2 * lane] = sa;
+            s_sm[rw][2 * lane + 1] = sb;
+            role_sync(1);
+            if (rt < kRowGroup && r0 + rt < rows) {
+                double M = s_mx[0][rt], Sm = s_sm[0][rt];
 #pragma unroll
-                for (int q = 1; q < kRowThreads / 32; ++q) {
-                    M = fmax(M, s_mx[q][tid]);
-                    Sm += s_sm[q][tid];
+                for (int q = 1; q < kRoleWarps; ++q) {
+                    M = fmax(M, s_mx[q][rt]);
+                    Sm += s_sm[q][rt];
                 }
-                atomicMax(reinterpret_cast<unsigned long long*>(S.acc_max + r0 + tid),
+                atomicMax(reinterpret_cast<unsigned long long*>(S.acc_max + r0 + rt),
                           static_cast<unsigned long long>(__double_as_longlong(M)));
-                atomicAdd(S.acc_sum + r0 + tid, Sm);
+                atomicAdd(S.acc_sum + r0 + rt, Sm);
+                __threadfence();
             }
-            __threadfence();
-            __syncthreads();
-            if (tid == 0) {
+            role_sync(1);
+            if (rt == 0) {
                 s_last = atomicAdd(S.grp_cnt + g, 1) == splits - 1;
                 s_nflag = 0;
             }
-            __syncthreads();
+            role_sync(1);
             if (s_last) {
                 // ---- the group's last slice: finalize its exponents ----
                 __threadfence();
-                if (tid < kRowGroup && r0 + tid < rows) {
-                    const int64_t row = r0 + tid;
-                    const double M = __longlong_as_double(
-                        static_cast<long long>(atomicExch(reinterpret_cast<unsigned long long*>(S.acc_max + row), 0ull)));
+                if (rt < kRowGroup && r0 + rt < rows) {
+                    const int64_t row = r0 + rt;
+                    const double M = __longlong_as_double(static_cast<long long>(
+                        atomicExch(reinterpret_cast<unsigned long long*>(S.acc_max + row), 0ull)));
                     const double Sm = __longlong_as_double(static_cast<long long>(
                         atomicExch(reinterpret_cast<unsigned long long*>(S.acc_sum + row), 0ull)));
-                    if (finalize_line(F, row, M, Sm)) s_flag[atomicAdd(&s_nflag, 1)] = tid;
+                    if (finalize_line(F, row, M, Sm)) s_flag[atomicAdd(&s_nflag, 1)] = rt;
                 }
-                __syncthreads();
-                for (int w = warp; w < s_nflag; w += kRowThreads / 32) exact_line(F, r0 + s_flag[w], lane);
+                role_sync(1);
+                for (int w = rw; w < s_nflag; w += kRoleWarps) exact_line(F, r0 + s_flag[w], lane);
                 __threadfence();
-                __syncthreads();
-                if (tid == 0) {
+                role_sync(1);
+                if (rt == 0) {
                     S.grp_cnt[g] = 0;  // ready for the next call
                     st_release(S.grp_ready + g, epoch);
                 }
             }
+            role_sync(1);  // s_t, s_last and the shared partials are reused
         }
-        if (p != 0xffffffffu) {
-            if (p >= total) {
-                // every block makes exactly one failing planes claim and then no
-                // claims at all: the last one resets both counters for the next call
-                if (tid == 0 && p == total + gridDim.x - 1) {
-                    S.tickets[0] = 0;
-                    S.tickets[1] = 0;
-                }
-                return;
-            }
+    } else {
+        const bool vec_ok = (ldx % (32 / sizeof(T))) == 0 && (reinterpret_cast<uintptr_t>(x) & 31) == 0;
+        for (;;) {
+            if (rt == 0) s_p = atomicAdd(S.tickets + 1, 1u);
+            role_sync(2);
+            const uint32_t p = s_p;
+            if (p >= total) break;
             // ---- planes of slice p ----
             const int64_t g = p / splits;
             const int64_t r0 = g * kRowGroup, h0 = static_cast<int64_t>(p % splits) * kSliceCols;
             const int64_t h1 = h0 + kSliceCols < cols ? h0 + kSliceCols : cols;
-            if (tid == 0) {
-                // bounded: a group that never publishes (a corrupted state word)
-                // traps into a launch error instead of hanging the device
+            if (rt == 0) {
+                // the statistics role of every resident block claims and finishes
+                // statistics slices without waiting on anything, so the group is
+                // published; bounded anyway: a corrupted state word traps into a
+                // launch error instead of hanging the device
                 const unsigned long long t0 = globaltimer_ns();
                 while (ld_acquire(S.grp_ready + g) != epoch) {
-                    __nanosleep(64);
+                    __nanosleep(128);
                     if (globaltimer_ns() - t0 > 4000000000ull) __trap();
                 }
             }
-            __syncthreads();
-            if (tid < kRowGroup) s_exp[tid] = r0 + tid < rows ? __ldcg(F.exp_out + r0 + tid) : 0;
-            __syncthreads();
+            role_sync(2);
+            if (rt < kRowGroup) s_exp[rt] = r0 + rt < rows ? __ldcg(F.exp_out + r0 + rt) : 0;
+            role_sync(2);
             // 8 rows x 1 column per item: 8 items per column, kSliceCols columns
-            const bool vec_ok = (ldx % (32 / sizeof(T))) == 0 && (reinterpret_cast<uintptr_t>(x) & 31) == 0;
 #pragma unroll 1
-            for (int it = tid; it < kSliceCols * (kRowGroup / 8); it += kRowThreads) {
+            for (int it = rt; it < kSliceCols * (kRowGroup / 8); it += kRoleThreads) {
                 const int64_t h = h0 + it / (kRowGroup / 8);
                 const int64_t rr = r0 + (it % (kRowGroup / 8)) * 8;
                 const bool active = h < h1 && rr < extent;
@@ -398,8 +418,15 @@ __global__ void __launch_bounds__(kRowThreads, 2)
                 for (int u = 0; u < 8; ++u) ex[u] = s_exp[(it % (kRowGroup / 8)) * 8 + u];
                 write_planes8<T, KIND, kMaxMod>(v, ex, active, planes + h * ld + rr, plane_stride, c, pol);
             }
+            role_sync(2);  // s_p and s_exp are reused
         }
-        __syncthreads();  // s_t / s_p / shared slices are reused
+    }
+    // each role of each block made exactly one failing claim and makes no more:
+    // the last role out resets the counters for the next call
+    if (rt == 0 && atomicAdd(S.tickets + 2, 1u) == 2u * gridDim.x - 1u) {
+        S.tickets[0] = 0;
+        S.tickets[1] = 0;
+        S.tickets[2] = 0;
     }
 }
 
@@ -436,14 +463,13 @@ void rows_dispatch(const T* x, int64_t rows, int64_t cols, int64_t ldx, uint32_t
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rows_fused_kernel<T, KIND, 8>, kRowThreads, 0);
     if (per_sm < 1) per_sm = 1;
     const int64_t grid = std::min<int64_t>(total, static_cast<int64_t>(per_sm) * num_sms);
-    // planes trail statistics by about one grid of slices plus one group
-    // (OZK_K1_LAG: that many slices instead, never below one group)
-    int64_t lag = grid + splits;
-    if (const char* e = std::getenv("OZK_K1_LAG")) lag = std::max<int64_t>(splits, std::atoll(e));
-    lag = std::min<int64_t>(total, lag);
+    // statistics may run this many slices ahead of the planes (>= one group;
+    // OZK_K1_LAG overrides): one group plus half a grid of slices in flight
+    int lag = splits + static_cast<int>(grid / 2);
+    if (const char* e = std::getenv("OZK_K1_LAG")) lag = std::max(splits, std::atoi(e));
 #define OZK_K1F(MAXN)                                                                                          \
     rows_fused_kernel<T, KIND, MAXN><<<static_cast<unsigned>(grid), kRowThreads, 0, s>>>(                      \
-        x, rows, cols, ldx, splits, static_cast<int>(lag), epoch, nonfinite, F, c, planes, ld, stride, S)
+        x, rows, cols, ldx, splits, lag, epoch, nonfinite, F, c, planes, ld, stride, S)
     if (KIND == 1 || c.n <= 8)
         OZK_K1F(8);
     else if (c.n <= 12)
