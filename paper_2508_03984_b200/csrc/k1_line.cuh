@@ -21,28 +21,32 @@ __device__ __forceinline__ bool needs_exact(double y, double mx, int64_t k) {
     return d < guard_band(k) || mx >= 0x1.0p+500 || mx < 0x1.0p-400;
 }
 
-// fast / accurate exponent of one line from its max and sum of squares;
+// fast / accurate exponent of one line from its max and sum of squares (e);
 // returns whether the line needs the exact sequential recompute
-__device__ __forceinline__ bool finalize_line(const LineFinal& F, int64_t line, double mx, double s) {
+__device__ __forceinline__ bool line_exponent(const LineFinal& F, double mx, double s, int& e) {
     if (F.mode == OZK_FAST) {
-        int e = 0;  // zero line: sentinel mu = 1 (scaling.cpp:80, :88)
-        bool flag = false;
-        if (mx != 0.0) {
-            const int g = ilogb(mx);
-            const double y = fast_budget(ldexp(s, -2 * g), F.k, F.pp_fast);
-            e = fast_exponent_from_budget(y, g, F.prec, F.fix);
-            flag = needs_exact(y, mx, F.k);
-        }
-        F.exp_out[line] = e;
-        return flag;
+        e = 0;  // zero line: sentinel mu = 1 (scaling.cpp:80, :88)
+        if (mx == 0.0) return false;
+        const int g = ilogb(mx);
+        const double y = fast_budget(ldexp(s, -2 * g), F.k, F.pp_fast);
+        e = fast_exponent_from_budget(y, g, F.prec, F.fix);
+        return needs_exact(y, mx, F.k);
     }
-    F.exp_out[line] = mx != 0.0 ? 5 - ilogb(mx) : INT32_MIN;
-    if (F.zero_out) F.zero_out[line] = 0;
+    e = mx != 0.0 ? 5 - ilogb(mx) : INT32_MIN;
     return false;
+}
+// the same, written to exp_out (and, accurate mode, the line's bound maximum cleared)
+__device__ __forceinline__ bool finalize_line(const LineFinal& F, int64_t line, double mx, double s) {
+    int e;
+    const bool flag = line_exponent(F, mx, s, e);
+    F.exp_out[line] = e;
+    if (F.mode != OZK_FAST && F.zero_out) F.zero_out[line] = 0;
+    return flag;
 }
 
 // Warp-collective, reference order: s = 0; for h: nh = ldexp(x_h, -g); s += nh*nh (no FMA).
-__device__ void exact_line(const LineFinal& F, int64_t line, int lane) {
+// Returns the fast-mode exponent on every lane.
+__device__ int exact_line_exponent(const LineFinal& F, int64_t line, int lane) {
     const int64_t off = line * F.line_step;
     const int64_t k = F.k;
     double mx = 0.0;
@@ -63,8 +67,11 @@ __device__ void exact_line(const LineFinal& F, int64_t line, int lane) {
     }
     // the floor from the host-built step table: the reference's glibc log2 decides
     // it even where y = pp - 0.51 log2(ub) is within an ulp of an integer
-    if (lane == 0)
-        F.exp_out[line] = fast_exponent_from_floor(fast_floor_table(fast_ub(s, k), F.fast_floor), g, F.prec, F.fix);
+    return fast_exponent_from_floor(fast_floor_table(fast_ub(s, k), F.fast_floor), g, F.prec, F.fix);
+}
+__device__ void exact_line(const LineFinal& F, int64_t line, int lane) {
+    const int e = exact_line_exponent(F, line, lane);
+    if (lane == 0) F.exp_out[line] = e;
 }
 
 }  // namespace

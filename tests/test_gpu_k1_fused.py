@@ -138,14 +138,28 @@ def test_fused_k1_nonfinite(ctx, where, bad, trans):
     _run(ctx, a2, b2, EmuConfig(n_moduli=14), trans, trans)
 
 
-def test_row_kernel_enabled_subprocess():
-    """The one-pass row kernel is opt-in (OZK_K1_FUSED=3; the default mask 1
-    uses only the column kernel): this module again with both kernels on."""
+@pytest.mark.parametrize("mask", ["3", "5"])
+def test_row_kernel_enabled_subprocess(mask):
+    """The one-pass row kernels are opt-in (OZK_K1_FUSED=3: the ticketed one,
+    5: the cluster one; the default mask 1 uses only the column kernel): this
+    module again with each of them on."""
     import os
     import subprocess
     import sys
 
-    env = dict(os.environ, OZK_K1_FUSED="3")
+    env = dict(os.environ, OZK_K1_FUSED=mask)
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", __file__,
                         "-k", "not subprocess"], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("lag", ["1", "100000"])
+def test_fused_k1_row_lag_extremes(ctx, oracle, lag, monkeypatch):
+    """the row kernel's statistics/planes distance at its floor (one group of
+    slices: the deadlock-freedom bound) and unbounded; read per launch"""
+    monkeypatch.setenv("OZK_K1_LAG", lag)
+    for m, n, k in [(700, 90, 5000), (2049, 64, 1000)]:
+        a = gen_matrix(m, k, 1.0, 61 + m)
+        b = gen_matrix(k, n, 1.0, 62 + n)
+        got = _run(ctx, a, b, EmuConfig(n_moduli=14))
+        np.testing.assert_array_equal(_bits(got), _bits(oracle.gemm(a, b, 14, 0)))

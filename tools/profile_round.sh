@@ -10,6 +10,6 @@ OZK_BENCH_NO_CPU=1 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dra
   --clock-control none --csv --log-file gpurun_out/launches_$tag.csv \
   python bench.py --steps 1 --warmup 1 --no-extra --no-e2e > gpurun_out/launches_$tag.log 2>&1
 OZK_BENCH_NO_CPU=1 ncu --set full --clock-control none --import-source on \
-  -k "regex:residue_gemm|planes_kernel|reconstruct|row_stats|col_stats" -c 6 \
+  -k "regex:residue_gemm|planes_kernel|reconstruct|row_stats|col_stats|fused_kernel" -c 5 \
   -o gpurun_out/full_$tag python bench.py --steps 1 --warmup 0 --no-extra --no-e2e > gpurun_out/full_$tag.log 2>&1
 ls -la gpurun_out
