@@ -615,8 +615,7 @@ int k1_fused_mask() {
 }
 bool k1_fused_enabled() { return k1_fused_mask() != 0; }
 bool cols_fused_on() { return (k1_fused_mask() & 1) != 0; }
-bool rows_fused_on() { return (k1_fused_mask() & 6) != 0; }
-bool rows_cluster_on() { return (k1_fused_mask() & 4) != 0; }  // bit 2: the cluster row kernel
+bool rows_fused_on() { return (k1_fused_mask() & 2) != 0; }
 
 // the row kernel reads two adjacent rows per lane (16 / 8-byte vectors)
 bool rows_fusable(const void* x, int64_t ld) { return (reinterpret_cast<uintptr_t>(x) & 15) == 0 && ld % 2 == 0; }
@@ -650,9 +649,6 @@ int stage_rows_fused(ozk_context* h, Job& J, void* state) {
     if (J.ta)  // stored k x m: the lines are its columns, the planes K-major
         launch_cols_fused(J.a, J.in_f32, J.k, J.m, J.lda, J.flags, F, J.dc, kind, J.pa, J.lda_p, J.pa_stride,
                           h->num_sms, h->stream);
-    else if (rows_cluster_on())
-        launch_rows_cluster(J.a, J.in_f32, J.m, J.k, J.lda, J.flags, F, J.dc, kind, J.pa, J.lda_p, J.pa_stride,
-                            h->num_sms, h->stream);
     else
         launch_rows_fused(J.a, J.in_f32, J.m, J.k, J.lda, ++h->fused_epoch, state, J.flags, F, J.dc, kind, J.pa,
                           J.lda_p, J.pa_stride, h->num_sms, h->stream);
@@ -671,10 +667,7 @@ int stage_cols_fused(ozk_context* h, Job& J, int64_t j0, int64_t nj, void* state
                                    J.tb ? 1 : J.ldb, J.tb ? J.ldb : 1);
     const int kind = fast ? 0 : 1;
     int8_t* dst = J.pb + b_plane_off(J, j0);
-    if (J.tb && rows_cluster_on())  // stored n x k: the lines are its rows, the planes MN-major
-        launch_rows_cluster(bj, J.in_f32, nj, J.k, J.ldb, J.flags, F, J.dc, kind, dst, J.ld, J.pb_stride, h->num_sms,
-                            h->stream);
-    else if (J.tb)
+    if (J.tb)  // stored n x k: the lines are its rows, the planes MN-major
         launch_rows_fused(bj, J.in_f32, nj, J.k, J.ldb, ++h->fused_epoch, state, J.flags, F, J.dc, kind, dst, J.ld,
                           J.pb_stride, h->num_sms, h->stream);
     else

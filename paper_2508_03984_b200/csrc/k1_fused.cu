@@ -430,231 +430,6 @@ __global__ void __launch_bounds__(kRowThreads, 2)
     }
 }
 
-// ---- rows, cluster variant ---------------------------------------------------
-// A group of 16 rows (128 B of FP64 per column) is owned by one cluster of 8
-// CTAs, each streaming k/8 of its columns: statistics of the CTA's columns, an
-// exchange of the 8 partial (max, sum) sets through distributed shared memory
-// and one hardware cluster barrier, the exponents (every CTA combines the
-// partials in rank order, so all compute the same values), then the CTA's
-// columns again — from L2: the ~18 clusters in flight hold 18 x 2 MB of A at
-// k = 16384. No tickets, no global flags, no atomics on the data path.
-constexpr int kClThreads = 512;
-constexpr int kClRows = 16;    // rows per group
-constexpr int kCluster = 8;    // CTAs per cluster (portable maximum)
-
-__device__ __forceinline__ void cluster_barrier() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ double ld_dsmem_f64(const double* local, uint32_t rank) {
-    uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local)), ra;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
-    double v;
-    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
-    return v;
-}
-
-template <typename T, int KIND, int kMaxMod>
-__global__ void __launch_bounds__(kClThreads, 1)
-    rows_cluster_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx, int32_t* __restrict__ nonfinite,
-                        const LineFinal F, const DevConsts c, int8_t* __restrict__ planes, int64_t ld,
-                        int64_t plane_stride) {
-    constexpr int kWarps = kClThreads / 32;
-    __shared__ double s_wmx[kWarps][kClRows], s_wsm[kWarps][kClRows];
-    __shared__ double s_part[2][2][kClRows];  // [group parity][max | sum][row]: read by the whole cluster
-    __shared__ int s_exp[kClRows];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t rank = cluster_rank();
-    const int64_t nclusters = gridDim.x / kCluster, cl = blockIdx.x / kCluster;
-    const int64_t groups = (rows + kClRows - 1) / kClRows;
-    const int64_t kc = (cols + kCluster - 1) / kCluster;  // columns per CTA
-    const int64_t c0 = rank * kc, c1 = c0 + kc < cols ? c0 + kc : cols;
-    const uint64_t pol = pol_evict_first(), pol_keep = pol_evict_last();
-    const bool vec_ok = (ldx % (32 / sizeof(T))) == 0 && (reinterpret_cast<uintptr_t>(x) & 31) == 0;
-    // statistics mapping: 8 lanes x 2 rows cover a column's 16 rows, a warp 4
-    // columns per load, the block 64 columns per step
-    const int sub = lane & 7, coff = lane >> 3;
-    int parity = 0;
-    for (int64_t g = cl; g < groups; g += nclusters, parity ^= 1) {
-        const int64_t r0 = g * kClRows;
-        const int64_t ra = r0 + 2 * sub;
-        double mx0 = 0.0, mx1 = 0.0, sa = 0.0, sb = 0.0;
-        if (ra + 1 < rows) {
-#pragma unroll 8
-            for (int64_t h = c0 + warp * 4 + coff; h < c1; h += kWarps * 4) {
-                double a, b;
-                if constexpr (sizeof(T) == 8) {
-                    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-                                 : "=d"(a), "=d"(b)
-                                 : "l"(x + ra + h * ldx), "l"(pol_keep));
-                } else {
-                    float fa, fb;
-                    asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
-                                 : "=f"(fa), "=f"(fb)
-                                 : "l"(x + ra + h * ldx), "l"(pol_keep));
-                    a = fa;
-                    b = fb;
-                }
-                mx0 = fmax(mx0, fabs(a));
-                mx1 = fmax(mx1, fabs(b));
-                sa = __fma_rn(a, a, sa);
-                sb = __fma_rn(b, b, sb);
-            }
-        } else if (ra < rows) {  // the last odd row
-            for (int64_t h = c0 + warp * 4 + coff; h < c1; h += kWarps * 4) {
-                const double a = static_cast<double>(x[ra + h * ldx]);
-                mx0 = fmax(mx0, fabs(a));
-                sa = __fma_rn(a, a, sa);
-            }
-        }
-        if (__any_sync(0xffffffffu, isinf(mx0) || isinf(mx1) || isnan(sa + sb)) && lane == 0) atomicOr(nonfinite, 1);
-        // lanes 8 apart share rows: fold the 4 column offsets of the warp
-#pragma unroll
-        for (int o = 8; o < 32; o <<= 1) {
-            mx0 = fmax(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
-            mx1 = fmax(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
-            sa += __shfl_xor_sync(0xffffffffu, sa, o);
-            sb += __shfl_xor_sync(0xffffffffu, sb, o);
-        }
-        if (lane < 8) {
-            s_wmx[warp][2 * lane] = mx0;
-            s_wmx[warp][2 * lane + 1] = mx1;
-            s_wsm[warp][2 * lane] = sa;
-            s_wsm[warp][2 * lane + 1] = sb;
-        }
-        __syncthreads();
-        if (tid < kClRows) {
-            double M = s_wmx[0][tid], S = s_wsm[0][tid];
-#pragma unroll
-            for (int q = 1; q < kWarps; ++q) {
-                M = fmax(M, s_wmx[q][tid]);
-                S += s_wsm[q][tid];
-            }
-            s_part[parity][0][tid] = M;
-            s_part[parity][1][tid] = S;
-        }
-        cluster_barrier();  // every CTA's partials of this group are visible cluster-wide
-        if (warp == 0) {
-            // every CTA combines the 8 partial sets in rank order (identical
-            // results everywhere) and computes the exponents locally; flagged
-            // rows are recomputed in the reference's order by this warp; rank 0
-            // alone publishes them (exp_out, accurate mode's cleared maxima)
-            double M = 0.0, S = 0.0;
-            if (lane < kClRows) {
-                for (uint32_t q = 0; q < kCluster; ++q) {
-                    M = fmax(M, ld_dsmem_f64(&s_part[parity][0][lane], q));
-                    S += ld_dsmem_f64(&s_part[parity][1][lane], q);
-                }
-            }
-            const int64_t row = r0 + lane;
-            const bool live = lane < kClRows && row < rows;
-            int e = 0;
-            const bool flag = live && line_exponent(F, M, S, e);
-            for (unsigned f = __ballot_sync(0xffffffffu, flag); f; f &= f - 1) {
-                const int r = __ffs(f) - 1;
-                const int ex = exact_line_exponent(F, r0 + r, lane);
-                if (lane == r) e = ex;
-            }
-            if (lane < kClRows) s_exp[lane] = live ? e : 0;
-            if (rank == 0 && live) {
-                F.exp_out[row] = e;
-                if (F.mode != OZK_FAST && F.zero_out) F.zero_out[row] = 0;
-            }
-        }
-        __syncthreads();
-        // planes of rows [r0, r0 + 16) x this CTA's columns: items of 8 rows x 1 column
-        const int64_t extent = (rows + 15) / 16 * 16;
-        const int64_t items = 2 * (c1 - c0);
-        for (int64_t it0 = 0; it0 < items; it0 += 2 * kClThreads) {
-            T v[2][8];
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const int64_t it = it0 + tid + q * kClThreads;
-                const int64_t h = c0 + it / 2;
-                const int64_t rr = r0 + (it & 1) * 8;
-                const bool active = it < items && rr < extent;
-                const T* src = x + (active ? h : 0) * ldx + (active ? rr : 0);
-                if (active && vec_ok && rr + 8 <= rows) {
-                    load8h(src, v[q], pol);
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) v[q][u] = active && rr + u < rows ? src[u] : T(0);
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const int64_t it = it0 + tid + q * kClThreads;
-                const int64_t h = c0 + it / 2;
-                const int64_t rr = r0 + (it & 1) * 8;
-                const bool active = it < items && rr < extent;
-                int ex[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) ex[u] = s_exp[(it & 1) * 8 + u];
-                write_planes8<T, KIND, kMaxMod>(v[q], ex, active, planes + (active ? h : 0) * ld + (active ? rr : 0),
-                                                plane_stride, c, pol);
-            }
-        }
-        // s_wmx / s_exp are reused by the next group; s_part is double-buffered
-        // (a CTA rewrites this parity only after the next cluster barrier, which
-        // every CTA reaches after its reads of this group's partials)
-        __syncthreads();
-    }
-    cluster_barrier();  // no CTA leaves while another may still read its partials
-}
-
-template <typename T, int KIND>
-int rows_cluster_dispatch(const T* x, int64_t rows, int64_t cols, int64_t ldx, int32_t* nonfinite,
-                          const LineFinal& F, const DevConsts& c, int8_t* planes, int64_t ld, int64_t stride,
-                          int num_sms, cudaStream_t s) {
-    const int64_t groups = (rows + kClRows - 1) / kClRows;
-    cudaLaunchConfig_t cfg{};
-    cfg.blockDim = dim3(kClThreads);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = kCluster;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    // one CTA per SM, as many whole clusters as the GPCs hold at once
-    // (~16-18: ~35 MB of A in flight at k = 16384)
-    static int fit_dev[64];
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int fit = fit_dev[dev & 63];
-    if (!fit) {
-        cfg.gridDim = dim3(static_cast<unsigned>(kCluster));
-        if (cudaOccupancyMaxActiveClusters(&fit, rows_cluster_kernel<T, KIND, 8>, &cfg) != cudaSuccess || fit < 1) {
-            cudaGetLastError();
-            fit = std::max(1, num_sms / kCluster);
-        }
-        fit_dev[dev & 63] = fit;
-    }
-    const int64_t nclusters = std::min<int64_t>(groups, fit);
-    cfg.gridDim = dim3(static_cast<unsigned>(nclusters * kCluster));
-    cudaError_t e = cudaSuccess;
-#define OZK_K1C(MAXN) \
-    e = cudaLaunchKernelEx(&cfg, rows_cluster_kernel<T, KIND, MAXN>, x, rows, cols, ldx, nonfinite, F, c, planes, ld, stride)
-    if (KIND == 1 || c.n <= 8)
-        OZK_K1C(8);
-    else if (c.n <= 12)
-        OZK_K1C(12);
-    else if (c.n <= 14)
-        OZK_K1C(14);
-    else if (c.n <= 16)
-        OZK_K1C(16);
-    else
-        OZK_K1C(OZK_MAX_MODULI);
-#undef OZK_K1C
-    return e == cudaSuccess ? 0 : -1;
-}
-
 template <typename T, int KIND>
 void cols_dispatch(const T* x, int64_t rows, int64_t cols, int64_t ldx, int32_t* nonfinite, const LineFinal& F,
                    const DevConsts& c, int8_t* planes, int64_t ld, int64_t stride, int num_sms, cudaStream_t s) {
@@ -732,26 +507,6 @@ void launch_cols_fused(const void* x, int is_f32, int64_t rows, int64_t cols, in
         else
             cols_dispatch<double, 1>(static_cast<const double*>(x), rows, cols, ldx, nonfinite, F, c, planes, ld,
                                      stride, num_sms, s);
-    }
-}
-
-void launch_rows_cluster(const void* x, int is_f32, int64_t rows, int64_t cols, int64_t ldx, int32_t* nonfinite,
-                         const LineFinal& F, const DevConsts& c, int kind, int8_t* planes, int64_t ld, int64_t stride,
-                         int num_sms, cudaStream_t s) {
-    if (is_f32) {
-        if (kind == 0)
-            rows_cluster_dispatch<float, 0>(static_cast<const float*>(x), rows, cols, ldx, nonfinite, F, c, planes, ld,
-                                            stride, num_sms, s);
-        else
-            rows_cluster_dispatch<float, 1>(static_cast<const float*>(x), rows, cols, ldx, nonfinite, F, c, planes, ld,
-                                            stride, num_sms, s);
-    } else {
-        if (kind == 0)
-            rows_cluster_dispatch<double, 0>(static_cast<const double*>(x), rows, cols, ldx, nonfinite, F, c, planes,
-                                             ld, stride, num_sms, s);
-        else
-            rows_cluster_dispatch<double, 1>(static_cast<const double*>(x), rows, cols, ldx, nonfinite, F, c, planes,
-                                             ld, stride, num_sms, s);
     }
 }
 

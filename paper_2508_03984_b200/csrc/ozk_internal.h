@@ -155,11 +155,6 @@ void launch_b_planes(const void* b, int is_f32, int64_t k, int64_t n, int64_t ld
 // holds rows_fused_state_bytes(rows) zeroed bytes (self-resetting) and every
 // launch needs a fresh epoch != 0.
 size_t rows_fused_state_bytes(int64_t rows);
-// rows, cluster variant: 16-row groups, each owned by a cluster of 8 CTAs that
-// exchange their partial statistics through distributed shared memory
-void launch_rows_cluster(const void* x, int is_f32, int64_t rows, int64_t cols, int64_t ldx, int32_t* nonfinite,
-                         const LineFinal& F, const DevConsts& c, int kind, int8_t* planes, int64_t ld, int64_t stride,
-                         int num_sms, cudaStream_t s);
 void launch_cols_fused(const void* x, int is_f32, int64_t rows, int64_t cols, int64_t ldx, int32_t* nonfinite,
                        const LineFinal& F, const DevConsts& c, int kind, int8_t* planes, int64_t ld, int64_t stride,
                        int num_sms, cudaStream_t s);

@@ -138,11 +138,10 @@ def test_fused_k1_nonfinite(ctx, where, bad, trans):
     _run(ctx, a2, b2, EmuConfig(n_moduli=14), trans, trans)
 
 
-@pytest.mark.parametrize("mask", ["3", "5"])
+@pytest.mark.parametrize("mask", ["3"])
 def test_row_kernel_enabled_subprocess(mask):
-    """The one-pass row kernels are opt-in (OZK_K1_FUSED=3: the ticketed one,
-    5: the cluster one; the default mask 1 uses only the column kernel): this
-    module again with each of them on."""
+    """The one-pass row kernel is opt-in (OZK_K1_FUSED=3; the default mask 1
+    uses only the column kernel): this module again with it on."""
     import os
     import subprocess
     import sys
