@@ -118,7 +118,8 @@ DevConsts to_dev(const ozk_constants& c) {
     for (int i = 0; i < c.n_moduli; ++i) {
         d.s2_m52[i] = -c.s2[i] * 0x1p52;
         d.s1_m52[i] = -c.s1[i] * 0x1p52;
-        for (int b = 0; b < 4; ++b) d.negp_sh[b][i] = (0u - static_cast<uint32_t>(c.moduli[i])) << (8 * b);
+        d.negp[i] = 0u - static_cast<uint32_t>(c.moduli[i]);
+        if (i > 0 && c.moduli[i] == 256) d.p256_later = 1;
     }
     d.fast_floor = fast_floor_table(c.pp_fast);
     return d;

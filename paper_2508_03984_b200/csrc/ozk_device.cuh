@@ -78,11 +78,6 @@ __device__ __forceinline__ uint32_t literal_byte(T x, const DevConsts& c, int t)
     return static_cast<uint32_t>(static_cast<uint8_t>(rmod_fast(x, c.p[t], c.pinv64[t], c.pinv32[t], c.n)));
 }
 
-// K1b core (residue.cpp:24-42): the N residue bytes of 8 consecutive
-// truncated-scaled elements x of one column, one 8-byte word per plane at
-// dst0 + t * plane_stride. fast (warp-uniform): every x of the warp lies in
-// the symmetric-residue domain (one DFMA + one IMAD per element and modulus,
-// bytes packed by IMADs); else the literal rmod_fast sequence.
 // 8-byte plane store, optionally with an L2 eviction-priority policy
 template <bool kHint>
 __device__ __forceinline__ void store_plane8(int8_t* p, uint2 w, uint64_t pol) {
@@ -93,46 +88,69 @@ __device__ __forceinline__ void store_plane8(int8_t* p, uint2 w, uint64_t pol) {
         *reinterpret_cast<uint2*>(p) = w;
 }
 
+// K1b core (residue.cpp:24-42): the N residue bytes of 8 consecutive
+// truncated-scaled elements x of one column, one 8-byte word per plane at
+// dst0 + t * plane_stride. fast (warp-uniform): every x of the warp lies in
+// the symmetric-residue domain (one DFMA per element and modulus, one IMAD
+// per element and modulus to pack the bytes); else the literal rmod_fast
+// sequence.
+// kMaxMod: the modulus count rounded up to a bucket (8/12/14/16/20): the
+// modulus loop is unrolled, and only the moduli past the bucket below
+// (kMinMod) test t < n.
+__host__ __device__ constexpr int min_mod_of_bucket(int kMaxMod) {
+    return kMaxMod <= 8 ? 1 : (kMaxMod <= 12 ? 9 : (kMaxMod <= 14 ? 13 : (kMaxMod <= 16 ? 15 : 17)));
+}
 template <typename T, int kMaxMod, bool kHint = false>
 __device__ __forceinline__ void residue_planes8(const T (&x)[8], bool fast, int8_t* dst0, int64_t plane_stride,
                                                 const DevConsts& c, uint64_t st_pol = 0) {
     constexpr int kBPerThread = 8;
+    constexpr int kMinMod = min_mod_of_bucket(kMaxMod);
     uint32_t xlo[kBPerThread];
 #pragma unroll
     for (int u = 0; u < kBPerThread; ++u)
         xlo[u] = static_cast<uint32_t>(__double2loint(__dadd_rn(static_cast<double>(x[u]), kMagic52)));
-    // the fast/literal choice is warp-uniform: branch once, outside the modulus loop
-    if (fast) {
-        // modulus-independent half of the packed residue words (see below)
+    // the fast/literal choice is warp-uniform: branch once, outside the modulus
+    // loop (a table with 256 anywhere but first — never from select_moduli —
+    // takes the literal sequence)
+    if (fast && !c.p256_later) {
+        // four residues r_u in one word without byte shuffles:
+        // xlo_u + qlo_u (-p) = r_u (mod 2^32) with |r_u| <= 127 (p < 256), so
+        // sum_u (xlo_u + 128 + qlo_u (-p)) 2^(8u) = sum_u (r_u + 128) 2^(8u)
+        // exactly (no carries), and XOR 0x80 per byte leaves r_u mod 256. The
+        // modulus-dependent half is (-p) * sum_u qlo_u 2^(8u) (mod 2^32): three
+        // shift-adds and ONE multiply by the modulus' constant per word.
         uint32_t xb[2] = {0u, 0u};
 #pragma unroll
         for (int u = 0; u < kBPerThread; ++u) xb[u >> 2] += (xlo[u] + 128u) << (8 * (u & 3));
         int8_t* dst = dst0;
+        const bool first256 = c.p[0] == 256;  // the tables' first modulus (select_moduli)
 #pragma unroll
         for (int t = 0; t < kMaxMod; ++t) {
-            if (t < c.n) {  // uniform
-                const uint32_t pt = static_cast<uint32_t>(c.p[t]);
-                uint2 word;
-                if (pt == 256) {  // p = 256: the residue is the low byte of x
-                    word = make_uint2(pack_low_bytes(xlo[0], xlo[1], xlo[2], xlo[3]),
-                                      pack_low_bytes(xlo[4], xlo[5], xlo[6], xlo[7]));
-                } else {
-                    // four residues r_u in one word without byte shuffles:
-                    // xlo_u + qlo_u (-p) = r_u (mod 2^32) with |r_u| <= 127, so
-                    // sum_u (xlo_u + 128 + qlo_u (-p)) 2^(8u) = sum_u (r_u + 128) 2^(8u)
-                    // exactly (no carries), and XOR 0x80 per byte leaves r_u mod 256
-                    uint32_t w[2] = {xb[0], xb[1]};
+            if (t >= kMinMod && t >= c.n) break;  // uniform
+            uint2 word;
+            // p = 256: the residue is the low byte of x (+-128 -> 0x80 either way)
+            if (t == 0 && first256) {
+                word = make_uint2(pack_low_bytes(xlo[0], xlo[1], xlo[2], xlo[3]),
+                                  pack_low_bytes(xlo[4], xlo[5], xlo[6], xlo[7]));
+            } else {
+                const double pinv = c.pinv64[t];
+                const uint32_t negp = c.negp[t];
+                uint32_t w[2];
 #pragma unroll
-                    for (int u = 0; u < kBPerThread; ++u) {
+                for (int hlf = 0; hlf < 2; ++hlf) {
+                    uint32_t q = 0;
+#pragma unroll
+                    for (int u = 3; u >= 0; --u) {
                         const uint32_t qlo = static_cast<uint32_t>(
-                            __double2loint(__fma_rn(static_cast<double>(x[u]), c.pinv64[t], kMagic52)));
-                        w[u >> 2] += qlo * c.negp_sh[u & 3][t];
+                            __double2loint(__fma_rn(static_cast<double>(x[4 * hlf + u]), pinv, kMagic52)));
+                        q = (q << 8) + qlo;
                     }
-                    word = make_uint2(w[0] ^ 0x80808080u, w[1] ^ 0x80808080u);
+                    w[hlf] = (xb[hlf] + q * negp) ^ 0x80808080u;
                 }
-                store_plane8<kHint>(dst, word, st_pol);
-                dst += plane_stride;
+                word = make_uint2(w[0], w[1]);
             }
+            store_plane8<kHint>(dst, word, st_pol);
+            dst += plane_stride;
         }
     } else {
 #pragma unroll 1

@@ -44,7 +44,8 @@ struct DevConsts {
     double s2_m52[OZK_MAX_MODULI];
     double s1_m52[OZK_MAX_MODULI];  // -s1_i * 2^52: fl(s1*u) = fma(s1, 2^52 + u, -s1 * 2^52) (FP32 tables)
     int fast_fix;  // OZK_FLAG_FAST_EXPONENT_FIX  // -s2_i * 2^52 (for fl(s2*u) = fma(s2, 2^52 + u, -s2 * 2^52))
-    uint32_t negp_sh[4][OZK_MAX_MODULI];  // (-p_i mod 2^32) << 8b: K1b packs four residue bytes with IMADs
+    uint32_t negp[OZK_MAX_MODULI];  // -p_i mod 2^32: K1b packs four residue bytes with one IMAD per modulus
+    int p256_later;  // some modulus after the first is 256 (never for select_moduli tables): checked K1b loop
     FastFloorTable fast_floor;
 };
 
