@@ -53,6 +53,18 @@ __device__ __forceinline__ void load8(const int32_t* p, int (&v)[8]) {
                  : "l"(p));
 }
 
+// elements [i0, i0 + 8) of a line and (ROW_EXP) their exponents, zeros past len
+template <typename T, bool ROW_EXP>
+__device__ __forceinline__ void load8_guarded(const T* col, const int32_t* exps, int64_t i0, int64_t len, T (&v)[8],
+                                           int (&ev)[8]) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const bool ok = i0 + u < len;
+        v[u] = ok ? col[i0 + u] : T(0);
+        ev[u] = ROW_EXP && ok ? exps[i0 + u] : 0;
+    }
+}
+
 // Column-major rows x cols input -> N column-major int8 planes (ld bytes per
 // column, plane_stride bytes apart). ROW_EXP: the scale exponent is per row
 // (A: mu), else per column (B: nu). Each thread handles 8 consecutive rows of
@@ -81,13 +93,15 @@ __global__ void __launch_bounds__(128)
     if (vec) {
         load8(col + i0, vin);
         if constexpr (ROW_EXP) load8(exps + i0, ein);
+    } else {
+        // ragged / unaligned run (a real branch, not 16 predicated loads on the
+        // common path: that cost ~8 instructions per element in every thread)
+        load8_guarded<T, ROW_EXP>(col, exps, i0, active ? k : 0, vin, ein);
     }
 #pragma unroll
     for (int u = 0; u < kBPerThread; ++u) {
-        const int64_t i = i0 + u;
-        const bool ok = active && i < k;
-        const T v = vec ? vin[u] : (ok ? col[i] : T(0));
-        const int eu = ROW_EXP ? (vec ? ein[u] : (ok ? exps[i] : 0)) : e;
+        const T v = vin[u];
+        const int eu = ROW_EXP ? ein[u] : e;
         if constexpr (ROW_EXP) ex[u] = eu;
         if constexpr (KIND == 0) {
             x[u] = trunc_scaled(v, eu);
