@@ -158,7 +158,8 @@ __global__ void __launch_bounds__(kColThreads, 2)
     cols_fused_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx, int vec,
                       int32_t* __restrict__ nonfinite, const LineFinal F, const DevConsts c,
                       int8_t* __restrict__ planes, int64_t ld, int64_t plane_stride) {
-    __shared__ double s_mx[kColWarps], s_sm[kColWarps];
+    __shared__ uint32_t s_key[kColWarps], s_lo[kColWarps];
+    __shared__ double s_sm[kColWarps];
     __shared__ int s_e;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t extent = (rows + 15) / 16 * 16;  // plane_ld(rows)
@@ -167,7 +168,8 @@ __global__ void __launch_bounds__(kColThreads, 2)
     const uint64_t pol = pol_evict_first(), pol_keep = pol_evict_last();
     for (int64_t j = blockIdx.x; j < cols; j += gridDim.x) {
         const T* col = x + j * ldx;
-        double mx = 0.0, s0 = 0.0, s1 = 0.0;
+        AbsMax am;
+        double s0 = 0.0, s1 = 0.0;
         for (int64_t i = static_cast<int64_t>(tid) * 8; i < rows; i += 2 * 8 * kColThreads) {
             T v0[8], v1[8];
             line8(col, i, rows, vec, v0, pol_keep);
@@ -175,30 +177,30 @@ __global__ void __launch_bounds__(kColThreads, 2)
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const double a = static_cast<double>(v0[u]), b = static_cast<double>(v1[u]);
-                mx = fmax(mx, fmax(fabs(a), fabs(b)));
+                am.add(a);
+                am.add(b);
                 s0 = __fma_rn(a, a, s0);
                 s1 = __fma_rn(b, b, s1);
             }
         }
         double sm = s0 + s1;
+        am.warp_reduce();
 #pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            sm += __shfl_xor_sync(0xffffffffu, sm, o);
-        }
+        for (int o = 16; o; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
         if (lane == 0) {
-            s_mx[warp] = mx;
+            s_key[warp] = am.key;
+            s_lo[warp] = am.lo;
             s_sm[warp] = sm;
         }
         __syncthreads();
         if (warp == 0) {
-            mx = lane < kColWarps ? s_mx[lane] : 0.0;
+            AbsMax bm;
+            if (lane < kColWarps) bm.merge(s_key[lane], s_lo[lane]);
             sm = lane < kColWarps ? s_sm[lane] : 0.0;
+            bm.warp_reduce();
 #pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-                sm += __shfl_xor_sync(0xffffffffu, sm, o);
-            }
+            for (int o = 16; o; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+            const double mx = bm.value();
             // non-finite inputs (emulator.cpp:19-22): Inf in the max, NaN in the sum
             if (lane == 0 && (isinf(mx) || isnan(sm))) atomicOr(nonfinite, 1);
             const bool flag = __shfl_sync(0xffffffffu, lane == 0 ? finalize_line(F, j, mx, sm) : false, 0);

@@ -21,6 +21,36 @@ __device__ __forceinline__ bool needs_exact(double y, double mx, int64_t k) {
     return d < guard_band(k) || mx >= 0x1.0p+500 || mx < 0x1.0p-400;
 }
 
+// max |x| over a line, tracked on the bit patterns: an unsigned max of the high
+// words with the sign shifted out (IEEE order of |x| is the integer order of
+// the pattern) is 2 integer ops per element, where fmax(double) costs a
+// DSETP/FSEL/SEL/LOP3 sequence. It keeps the exponent and the top 19 mantissa
+// bits of max |x| — all the line finalize reads from the maximum (the zero
+// test, ilogb, the [2^-400, 2^500) range, Inf). A line whose nonzero elements
+// all have zero high words (|x| < 2^-1042) comes out as the smallest
+// subnormal, below 2^-400, so it takes the exact recompute, which takes its
+// own maximum.
+struct AbsMax {
+    uint32_t key = 0;  // max over (high word << 1)
+    uint32_t lo = 0;   // OR of the low words
+    __device__ __forceinline__ void add(double x) {
+        key = max(key, static_cast<uint32_t>(__double2hiint(x)) << 1);
+        lo |= static_cast<uint32_t>(__double2loint(x));
+    }
+    __device__ __forceinline__ void merge(uint32_t k, uint32_t l) {
+        key = max(key, k);
+        lo |= l;
+    }
+    __device__ __forceinline__ void warp_reduce() {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) merge(__shfl_xor_sync(0xffffffffu, key, o), __shfl_xor_sync(0xffffffffu, lo, o));
+    }
+    __device__ __forceinline__ double value() const {
+        if (key == 0) return lo ? 0x1p-1074 : 0.0;
+        return __hiloint2double(static_cast<int>(key >> 1), 0);
+    }
+};
+
 // fast / accurate exponent of one line from its max and sum of squares (e);
 // returns whether the line needs the exact sequential recompute
 __device__ __forceinline__ bool line_exponent(const LineFinal& F, double mx, double s, int& e) {

@@ -143,7 +143,8 @@ __global__ void __launch_bounds__(32 * kVecGroups)
     const int64_t j0 = static_cast<int64_t>(blockIdx.y) * k_per_split;
     const int64_t j1 = j0 + k_per_split < k ? j0 + k_per_split : k;
     const double* p = a + row0;
-    double mx0 = 0.0, mx1 = 0.0, s0 = 0.0, s1 = 0.0, t0 = 0.0, t1 = 0.0;
+    AbsMax am0, am1;
+    double s0 = 0.0, s1 = 0.0, t0 = 0.0, t1 = 0.0;
     int64_t j = j0 + g;
     for (; j + 3 * kVecGroups < j1; j += 4 * kVecGroups) {
         double2 v[4];
@@ -151,8 +152,8 @@ __global__ void __launch_bounds__(32 * kVecGroups)
         for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const double2*>(p + (j + u * kVecGroups) * lda));
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            mx0 = fmax(mx0, fabs(v[u].x));
-            mx1 = fmax(mx1, fabs(v[u].y));
+            am0.add(v[u].x);
+            am1.add(v[u].y);
             if (u & 1) {
                 t0 = __fma_rn(v[u].x, v[u].x, t0);
                 t1 = __fma_rn(v[u].y, v[u].y, t1);
@@ -164,13 +165,14 @@ __global__ void __launch_bounds__(32 * kVecGroups)
     }
     for (; j < j1; j += kVecGroups) {
         const double2 v = __ldg(reinterpret_cast<const double2*>(p + j * lda));
-        mx0 = fmax(mx0, fabs(v.x));
-        mx1 = fmax(mx1, fabs(v.y));
+        am0.add(v.x);
+        am1.add(v.y);
         s0 = __fma_rn(v.x, v.x, s0);
         s1 = __fma_rn(v.y, v.y, s1);
     }
     s0 += t0;
     s1 += t1;
+    const double mx0 = am0.value(), mx1 = am1.value();
     if (__any_sync(0xffffffffu, isinf(mx0) || isinf(mx1) || isnan(s0 + s1)) && lane == 0) atomicOr(nonfinite, 1);
     smax[g][2 * lane] = mx0;
     smax[g][2 * lane + 1] = mx1;
@@ -218,19 +220,21 @@ __global__ void __launch_bounds__(256)
         }
     } else {
         const double* p = static_cast<const double*>(b) + col * ldb;
+        AbsMax am;
         for (; i + 96 < k; i += 128) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const double x = p[i + 32 * u];
-                mx = fmax(mx, fabs(x));
+                am.add(x);
                 s[u] = __fma_rn(x, x, s[u]);
             }
         }
         for (; i < k; i += 32) {
             const double x = p[i];
-            mx = fmax(mx, fabs(x));
+            am.add(x);
             s[0] = __fma_rn(x, x, s[0]);
         }
+        mx = am.value();
     }
     double sum = (s[0] + s[1]) + (s[2] + s[3]);
 #pragma unroll
