@@ -162,3 +162,32 @@ def test_fused_k1_row_lag_extremes(ctx, oracle, lag, monkeypatch):
         b = gen_matrix(k, n, 1.0, 62 + n)
         got = _run(ctx, a, b, EmuConfig(n_moduli=14))
         np.testing.assert_array_equal(_bits(got), _bits(oracle.gemm(a, b, 14, 0)))
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, True)])
+def test_fused_k1_subnormal_lines(ctx, oracle, ta, tb):
+    """The line maxima are taken on the high words of the bit patterns
+    (k1_line.cuh AbsMax): lines of subnormals whose high words are all zero
+    (|x| < 2^-1042) must still count as nonzero and take the exact recompute,
+    lines of larger subnormals keep their exponent; the scale exponents and C
+    must match the reference."""
+    m, n, k = 130, 70, 900
+    a = gen_matrix(m, k, 0.5, 91)
+    b = gen_matrix(k, n, 0.5, 92)
+    a[5, :] = np.ldexp(a[5, :], -1062)     # high words 0: only the low words are nonzero
+    a[6, :] = np.ldexp(a[6, :], -1030)     # subnormal, high words nonzero
+    a[7, :] = 0.0
+    a[7, 3] = np.ldexp(1.0, -1070)          # a single tiny element in a zero row
+    b[:, 9] = np.ldexp(b[:, 9], -1062)
+    b[:, 10] = np.ldexp(b[:, 10], -1026)
+    b[:, 11] = 0.0
+    b[400, 11] = -np.ldexp(1.0, -1073)
+    wmu, wnu = oracle.scale(a, b, 14, 0)
+    mu = torch.zeros(m, dtype=torch.int32, device="cuda")
+    nu = torch.zeros(n, dtype=torch.int32, device="cuda")
+    ctx.stage_scale(_dev(a), _dev(b), EmuConfig(n_moduli=14), mu, nu)
+    np.testing.assert_array_equal(mu.cpu().numpy(), wmu)
+    np.testing.assert_array_equal(nu.cpu().numpy(), wnu)
+    for mode in (ScaleMode.Fast, ScaleMode.Accurate):
+        got = _run(ctx, a, b, EmuConfig(n_moduli=14, mode=mode), ta, tb)
+        np.testing.assert_array_equal(_bits(got), _bits(oracle.gemm(a, b, 14, int(mode))))
