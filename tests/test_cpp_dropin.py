@@ -60,3 +60,24 @@ def test_cpp_dropin_bitexact(tmp_path, oracle):
         np.testing.assert_array_equal(got.view(np.int64), oracle.gemm(a, b, 14, mode).view(np.int64))
     gold = open(os.path.join(ROOT, "tests", "golden", "tables_14_fp64.csv")).read()
     assert (tmp_path / "tables_14.csv").read_text() == gold
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_large_result(tmp_path):
+    """A result above 64 MB takes the drop-in's pre-faulted allocation
+    (crtgemm.cpp result_matrix: reserve, huge-page advice, parallel
+    MADV_POPULATE_WRITE, then the value-initialising resize): the values must
+    equal the C ABI host path's bit for bit, zero padding included."""
+    from paper_2508_03984_b200 import EmuConfig, gemm_emulated
+
+    exe = build(tmp_path)
+    a = gen_matrix(3000, 160, 0.5, 73)
+    b = gen_matrix(160, 3000, 0.5, 74)
+    _write(tmp_path / "a.bin", a)
+    _write(tmp_path / "b.bin", b)
+    (tmp_path / "cases.txt").write_text("14 0 0")
+    out = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True)
+    assert out.returncode == 0, (out.returncode, out.stdout, out.stderr)
+    got = _read(tmp_path / "c_0.bin")
+    want = gemm_emulated(a, b, EmuConfig(n_moduli=14)).c
+    np.testing.assert_array_equal(got.view(np.int64), want.view(np.int64))
