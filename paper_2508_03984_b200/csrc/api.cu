@@ -181,7 +181,6 @@ struct ozk_context {
     int64_t launches = 0;
     Buf planes_a, planes_b, u, stats, ints, flags, f32a, f32b, host_a, host_b, host_c, wide, cbar, counters;
     Buf fused;                  // one-pass K1 row state (k1_fused.cu): A side, then B side; zero between calls
-    uint32_t fused_epoch = 0;   // publication epoch of the one-pass row kernel's group exponents
     int64_t fused_m = -1, fused_n = -1;  // the shape the state layout was last cleared for
     int32_t* flags_host = nullptr;  // pinned mirror of the device flag word
     // stage timing (ozk_profile): CUDA events on the compute stream
@@ -625,9 +624,9 @@ bool rows_fusable(const void* x, int64_t ld) { return (reinterpret_cast<uintptr_
 int fused_state(ozk_context* h, const Job& J, void** sa, void** sb) {
     const size_t a = (rows_fused_state_bytes(J.m) + 255) / 256 * 256;
     const size_t b = (rows_fused_state_bytes(J.n) + 255) / 256 * 256;
-    // the regions' internal layout follows (m, n): after a shape change stale
-    // group epochs could sit where the next call expects zeroed counters, so
-    // the state is cleared whenever the buffer grows or the shape changes
+    // the state is all zero between calls, but the regions' layout follows
+    // (m, n): cleared whenever the buffer grows or the shape changes (a call
+    // that failed mid-way cannot leave stale words at a moved offset)
     const bool grow = !h->fused.p || a + b > h->fused.bytes;
     OZK_TRY(ensure(h->fused, a + b));
     if (grow || h->fused_m != J.m || h->fused_n != J.n) {
@@ -641,7 +640,10 @@ int fused_state(ozk_context* h, const Job& J, void** sa, void** sb) {
 }
 
 // op(A)'s rows in one pass: mu and its residue planes (fast), or mu' and Abar (accurate)
-bool a_fusable(const Job& J) { return J.ta ? cols_fused_on() : rows_fused_on() && rows_fusable(J.a, J.lda); }
+bool cols_worth_fusing(int64_t len, int64_t lines);
+bool a_fusable(const Job& J) {
+    return J.ta ? cols_fused_on() && cols_worth_fusing(J.k, J.m) : rows_fused_on() && rows_fusable(J.a, J.lda);
+}
 int stage_rows_fused(ozk_context* h, Job& J, void* state) {
     const bool fast = J.mode == OZK_FAST;
     const LineFinal F = line_final(J, fast ? J.mu : J.ma, fast ? nullptr : J.rowmax, J.a, J.ta ? J.lda : 1,
@@ -651,15 +653,24 @@ int stage_rows_fused(ozk_context* h, Job& J, void* state) {
         launch_cols_fused(J.a, J.in_f32, J.k, J.m, J.lda, J.flags, F, J.dc, kind, J.pa, J.lda_p, J.pa_stride,
                           h->num_sms, h->stream);
     else
-        launch_rows_fused(J.a, J.in_f32, J.m, J.k, J.lda, ++h->fused_epoch, state, J.flags, F, J.dc, kind, J.pa,
+        launch_rows_fused(J.a, J.in_f32, J.m, J.k, J.lda, state, J.flags, F, J.dc, kind, J.pa,
                           J.lda_p, J.pa_stride, h->num_sms, h->stream);
     if (!fast && J.wide_bound) OZK_CUDA(cudaMemsetAsync(J.rowmax64, 0, sizeof(unsigned long long) * J.m, h->stream));
     return check_launch(h, 1);
 }
 
 // columns [j0, j0+nj) of op(B) in one pass: nu and its planes (fast), or nu' and Bbar (accurate)
+// the column kernel gives each column a 512-thread block (8 elements per
+// thread per pass): below ~4096-element columns most of the block idles and
+// its per-column finalize latency shows (1024^3: 0.055 -> 0.062 ms), so short
+// or few columns keep the two-kernel path
+bool cols_worth_fusing(int64_t len, int64_t lines) {
+    static const bool any = std::getenv("OZK_K1_FUSED_ANY") != nullptr;  // tests: every size
+    return any || (len >= 4096 && lines >= 1024);
+}
 bool b_fusable(const Job& J, int64_t j0) {
-    return !J.tb ? cols_fused_on() : rows_fused_on() && rows_fusable(b_block(J, j0), J.ldb);
+    return !J.tb ? cols_fused_on() && cols_worth_fusing(J.k, J.n)
+                 : rows_fused_on() && rows_fusable(b_block(J, j0), J.ldb);
 }
 int stage_cols_fused(ozk_context* h, Job& J, int64_t j0, int64_t nj, void* state) {
     const bool fast = J.mode == OZK_FAST;
@@ -669,7 +680,7 @@ int stage_cols_fused(ozk_context* h, Job& J, int64_t j0, int64_t nj, void* state
     const int kind = fast ? 0 : 1;
     int8_t* dst = J.pb + b_plane_off(J, j0);
     if (J.tb)  // stored n x k: the lines are its rows, the planes MN-major
-        launch_rows_fused(bj, J.in_f32, nj, J.k, J.ldb, ++h->fused_epoch, state, J.flags, F, J.dc, kind, dst, J.ld,
+        launch_rows_fused(bj, J.in_f32, nj, J.k, J.ldb, state, J.flags, F, J.dc, kind, dst, J.ld,
                           J.pb_stride, h->num_sms, h->stream);
     else
         launch_cols_fused(bj, J.in_f32, J.k, nj, J.ldb, J.flags, F, J.dc, kind, dst, J.ld, J.pb_stride, h->num_sms,

@@ -21,7 +21,7 @@
 //    of a slice accumulate into per-row max / sum words (atomics; any
 //    summation order lies inside the guard band of the fast exponent, and
 //    flagged rows are recomputed exactly); the last slice of a 64-row group
-//    finalizes the group's exponents and publishes them with an epoch flag.
+//    finalizes the group's exponents and publishes them with a flag.
 //    The planes role claims slices from a second counter and waits for its
 //    group's flag; the statistics role stays within `lag` (>= one group) slices
 //    of the planes counter, so the slice (64 KB) is re-read from L2 (~16 MB
@@ -241,7 +241,7 @@ struct RowsFusedState {
     double* acc_max;      // [rows] non-negative max |x| bits (atomicMax on the encoding); zero between calls
     double* acc_sum;      // [rows] sum x^2 (atomicAdd); zero between calls
     int32_t* grp_cnt;     // [groups] finished statistics slices; zero between calls
-    uint32_t* grp_ready;  // [groups] epoch of the call whose exponents are published
+    uint32_t* grp_ready;  // [groups] 1: the group's exponents are published; zero between calls
     uint32_t* tickets;    // [0] statistics, [1] planes, [2] finished roles; zero between calls
 };
 
@@ -256,7 +256,7 @@ __device__ __forceinline__ void role_sync(int id) {
 template <typename T, int KIND, int kMaxMod>
 __global__ void __launch_bounds__(kRowThreads, 2)
     rows_fused_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx, int splits, int lag,
-                      uint32_t epoch, int32_t* __restrict__ nonfinite, const LineFinal F, const DevConsts c,
+                      int32_t* __restrict__ nonfinite, const LineFinal F, const DevConsts c,
                       int8_t* __restrict__ planes, int64_t ld, int64_t plane_stride, const RowsFusedState S) {
     constexpr int kRoleThreads = kRowThreads / 2, kRoleWarps = kRoleThreads / 32;
     __shared__ double s_mx[kRoleWarps][kRowGroup];
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kRowThreads, 2)
                 role_sync(1);
                 if (rt == 0) {
                     S.grp_cnt[g] = 0;  // ready for the next call
-                    st_release(S.grp_ready + g, epoch);
+                    st_release(S.grp_ready + g, 1u);
                 }
             }
             role_sync(1);  // s_t, s_last and the shared partials are reused
@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(kRowThreads, 2)
                 // published; bounded anyway: a corrupted state word traps into a
                 // launch error instead of hanging the device
                 const unsigned long long t0 = globaltimer_ns();
-                while (ld_acquire(S.grp_ready + g) != epoch) {
+                while (ld_acquire(S.grp_ready + g) != 1u) {
                     __nanosleep(128);
                     if (globaltimer_ns() - t0 > 4000000000ull) __trap();
                 }
@@ -425,7 +425,11 @@ __global__ void __launch_bounds__(kRowThreads, 2)
     }
     // each role of each block made exactly one failing claim and makes no more:
     // the last role out resets the counters for the next call
+    // (with the group flags, so the state is all zero between calls and a
+    // captured CUDA graph can replay the launch: nothing is baked in per call)
     if (rt == 0 && atomicAdd(S.tickets + 2, 1u) == 2u * gridDim.x - 1u) {
+        const int64_t groups_all = (rows + kRowGroup - 1) / kRowGroup;
+        for (int64_t g = 0; g < groups_all; ++g) S.grp_ready[g] = 0;
         S.tickets[0] = 0;
         S.tickets[1] = 0;
         S.tickets[2] = 0;
@@ -455,7 +459,7 @@ void cols_dispatch(const T* x, int64_t rows, int64_t cols, int64_t ldx, int32_t*
 }
 
 template <typename T, int KIND>
-void rows_dispatch(const T* x, int64_t rows, int64_t cols, int64_t ldx, uint32_t epoch, int32_t* nonfinite,
+void rows_dispatch(const T* x, int64_t rows, int64_t cols, int64_t ldx, int32_t* nonfinite,
                    const LineFinal& F, const DevConsts& c, int8_t* planes, int64_t ld, int64_t stride,
                    const RowsFusedState& S, int num_sms, cudaStream_t s) {
     const int splits = static_cast<int>((cols + kSliceCols - 1) / kSliceCols);
@@ -471,7 +475,7 @@ void rows_dispatch(const T* x, int64_t rows, int64_t cols, int64_t ldx, uint32_t
     if (const char* e = std::getenv("OZK_K1_LAG")) lag = std::max(splits, std::atoi(e));
 #define OZK_K1F(MAXN)                                                                                          \
     rows_fused_kernel<T, KIND, MAXN><<<static_cast<unsigned>(grid), kRowThreads, 0, s>>>(                      \
-        x, rows, cols, ldx, splits, lag, epoch, nonfinite, F, c, planes, ld, stride, S)
+        x, rows, cols, ldx, splits, lag, nonfinite, F, c, planes, ld, stride, S)
     if (KIND == 1 || c.n <= 8)
         OZK_K1F(8);
     else if (c.n <= 12)
@@ -512,7 +516,7 @@ void launch_cols_fused(const void* x, int is_f32, int64_t rows, int64_t cols, in
     }
 }
 
-void launch_rows_fused(const void* x, int is_f32, int64_t rows, int64_t cols, int64_t ldx, uint32_t epoch,
+void launch_rows_fused(const void* x, int is_f32, int64_t rows, int64_t cols, int64_t ldx,
                        void* state, int32_t* nonfinite, const LineFinal& F, const DevConsts& c, int kind,
                        int8_t* planes, int64_t ld, int64_t stride, int num_sms, cudaStream_t s) {
     const int64_t groups = (rows + kRowGroup - 1) / kRowGroup;
@@ -524,17 +528,17 @@ void launch_rows_fused(const void* x, int is_f32, int64_t rows, int64_t cols, in
     S.tickets = S.grp_ready + groups;
     if (is_f32) {
         if (kind == 0)
-            rows_dispatch<float, 0>(static_cast<const float*>(x), rows, cols, ldx, epoch, nonfinite, F, c, planes, ld,
+            rows_dispatch<float, 0>(static_cast<const float*>(x), rows, cols, ldx, nonfinite, F, c, planes, ld,
                                     stride, S, num_sms, s);
         else
-            rows_dispatch<float, 1>(static_cast<const float*>(x), rows, cols, ldx, epoch, nonfinite, F, c, planes, ld,
+            rows_dispatch<float, 1>(static_cast<const float*>(x), rows, cols, ldx, nonfinite, F, c, planes, ld,
                                     stride, S, num_sms, s);
     } else {
         if (kind == 0)
-            rows_dispatch<double, 0>(static_cast<const double*>(x), rows, cols, ldx, epoch, nonfinite, F, c, planes,
+            rows_dispatch<double, 0>(static_cast<const double*>(x), rows, cols, ldx, nonfinite, F, c, planes,
                                      ld, stride, S, num_sms, s);
         else
-            rows_dispatch<double, 1>(static_cast<const double*>(x), rows, cols, ldx, epoch, nonfinite, F, c, planes,
+            rows_dispatch<double, 1>(static_cast<const double*>(x), rows, cols, ldx, nonfinite, F, c, planes,
                                      ld, stride, S, num_sms, s);
     }
 }

@@ -153,13 +153,13 @@ void launch_b_planes(const void* b, int is_f32, int64_t k, int64_t n, int64_t ld
 // (the planes re-read each line from L2). cols: lines are the contiguous
 // columns of a rows x cols operand, planes K-major (column j at j * ld).
 // rows: lines are the rows, planes MN-major (column h at h * ld); `state`
-// holds rows_fused_state_bytes(rows) zeroed bytes (self-resetting) and every
-// launch needs a fresh epoch != 0.
+// holds rows_fused_state_bytes(rows) zeroed bytes (self-resetting: all zero
+// again when the launch ends, so CUDA graphs can replay it).
 size_t rows_fused_state_bytes(int64_t rows);
 void launch_cols_fused(const void* x, int is_f32, int64_t rows, int64_t cols, int64_t ldx, int32_t* nonfinite,
                        const LineFinal& F, const DevConsts& c, int kind, int8_t* planes, int64_t ld, int64_t stride,
                        int num_sms, cudaStream_t s);
-void launch_rows_fused(const void* x, int is_f32, int64_t rows, int64_t cols, int64_t ldx, uint32_t epoch,
+void launch_rows_fused(const void* x, int is_f32, int64_t rows, int64_t cols, int64_t ldx,
                        void* state, int32_t* nonfinite, const LineFinal& F, const DevConsts& c, int kind,
                        int8_t* planes, int64_t ld, int64_t stride, int num_sms, cudaStream_t s);
 // FP64 -> FP32 rounding of an input (emulator.cpp:84-91), column-major with ld

@@ -1,10 +1,12 @@
 """GPU parity of the one-pass K1 (csrc/k1_fused.cu): statistics, exponents and
 planes of each operand in one read from HBM.
 
-The column kernel is the default for ozk_gemm's contiguous lines whenever the
-whole problem is one panel (and for the accurate-mode bound planes), so the
-rest of the GPU suite already runs through it; the row kernel is opt-in
-(OZK_K1_FUSED=3) and this module runs once more with it on (the last test).
+The column kernel is the default for ozk_gemm's contiguous lines of >= 4096
+elements (>= 1024 of them) whenever the whole problem is one panel (and for
+the accurate-mode bound planes), so the full-size suite runs through it; the
+row kernel is opt-in (OZK_K1_FUSED=3). This module runs in-process with the
+defaults and again in subprocesses with the kernels taken at every size
+(OZK_K1_FUSED_ANY=1, masks 1 and 3: the last test).
 These cases aim at the kernels' own boundaries:
 the 64-row groups and 128-column slices of the row kernel (ragged rows and
 columns, a single slice, many groups), the 512-thread column kernel (columns
@@ -104,8 +106,8 @@ def test_fused_k1_flagged_lines(ctx, oracle, ta, tb):
 
 
 def test_fused_k1_state_across_calls(ctx, oracle):
-    """the ticket counters, row accumulators and group counters reset
-    themselves; the group flags are per-call epochs — so many calls of changing
+    """the ticket counters, row accumulators, group counters and group flags
+    reset themselves at the end of each launch — so many calls of changing
     shapes on one handle (both K1 streams) stay exact"""
     rng = np.random.default_rng(5)
     for it in range(24):
@@ -138,15 +140,47 @@ def test_fused_k1_nonfinite(ctx, where, bad, trans):
     _run(ctx, a2, b2, EmuConfig(n_moduli=14), trans, trans)
 
 
-@pytest.mark.parametrize("mask", ["3"])
+@pytest.mark.parametrize("mode", [ScaleMode.Fast, ScaleMode.Accurate])
+def test_fused_k1_cuda_graph_replay(oracle, mode):
+    """a captured call replays on new inputs: the one-pass kernels bake no
+    per-call state into the graph (run again with the row kernel on below)"""
+    from paper_2508_03984_b200 import Context
+
+    m, n, k = 640, 384, 1100
+    ctx = Context(0)
+    cfg = EmuConfig(n_moduli=14, mode=mode, stream_ordered=True)
+    a0, b0 = gen_matrix(m, k, 0.5, 1), gen_matrix(k, n, 0.5, 2)
+    a1, b1 = gen_matrix(m, k, 1.0, 3), gen_matrix(k, n, 1.0, 4)
+    A, B, C = _dev(a0), _dev(b0), _dev(np.zeros((m, n)))
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx.set_stream(s.cuda_stream)
+        ctx.gemm(A, B, cfg, C)  # warm-up: sizes the workspace and clears the state
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+            ctx.gemm(A, B, cfg, C)
+    for a, b in ((a1, b1), (a0, b0), (a1, b1)):
+        A.copy_(_dev(a))
+        B.copy_(_dev(b))
+        g.replay()
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(_bits(C.cpu().numpy()), _bits(oracle.gemm(a, b, 14, int(mode))))
+    ctx.close()
+
+
+@pytest.mark.parametrize("mask", ["1", "3"])
 def test_row_kernel_enabled_subprocess(mask):
-    """The one-pass row kernel is opt-in (OZK_K1_FUSED=3; the default mask 1
-    uses only the column kernel): this module again with it on."""
+    """This module again with the one-pass kernels taken at every size
+    (OZK_K1_FUSED_ANY: by default the column kernel serves only columns of
+    >= 4096 elements, >= 1024 of them): mask 1 the column kernel, mask 3 also
+    the opt-in row kernel."""
     import os
     import subprocess
     import sys
 
-    env = dict(os.environ, OZK_K1_FUSED=mask)
+    env = dict(os.environ, OZK_K1_FUSED=mask, OZK_K1_FUSED_ANY="1")
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", __file__,
                         "-k", "not subprocess"], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
