@@ -33,6 +33,12 @@
 // Bit-exactness is unchanged: the exponents come from the same finalize code
 // as the two-kernel path (guard band + exact recompute), and the plane bytes
 // from the same residue_planes8 / bound entries.
+//
+// Measured (profiles/r02_k1_fused_ab.md): the column kernel runs
+// at 5.6-5.9 TB/s with 0.03-0.13 GB of its second read missing L2 and is the
+// default for columns of >= 4096 elements (>= 1024 of them); the row kernel
+// is bit-exact but slower than row_stats + planes (too few bytes in flight
+// in its planes role) and stays opt-in (OZK_K1_FUSED=3).
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
