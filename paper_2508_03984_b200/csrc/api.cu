@@ -618,7 +618,12 @@ bool cols_fused_on() { return (k1_fused_mask() & 1) != 0; }
 bool rows_fused_on() { return (k1_fused_mask() & 2) != 0; }
 
 // the row kernel reads two adjacent rows per lane (16 / 8-byte vectors)
-bool rows_fusable(const void* x, int64_t ld) { return (reinterpret_cast<uintptr_t>(x) & 15) == 0 && ld % 2 == 0; }
+// and its planes role stages 64-row column runs with bulk copies (16-byte
+// aligned runs of a multiple of 16 bytes): rows and ld multiples of 16 / size
+bool rows_fusable(const void* x, int64_t ld, int64_t rows, int in_f32) {
+    const int64_t q = in_f32 ? 4 : 2;
+    return (reinterpret_cast<uintptr_t>(x) & 15) == 0 && ld % q == 0 && rows % q == 0;
+}
 
 // state of the one-pass row kernel: [A side | B side], zeroed when it grows, then self-resetting
 int fused_state(ozk_context* h, const Job& J, void** sa, void** sb) {
@@ -642,7 +647,8 @@ int fused_state(ozk_context* h, const Job& J, void** sa, void** sb) {
 // op(A)'s rows in one pass: mu and its residue planes (fast), or mu' and Abar (accurate)
 bool cols_worth_fusing(int64_t len, int64_t lines);
 bool a_fusable(const Job& J) {
-    return J.ta ? cols_fused_on() && cols_worth_fusing(J.k, J.m) : rows_fused_on() && rows_fusable(J.a, J.lda);
+    return J.ta ? cols_fused_on() && cols_worth_fusing(J.k, J.m)
+                : rows_fused_on() && rows_fusable(J.a, J.lda, J.m, J.in_f32);
 }
 int stage_rows_fused(ozk_context* h, Job& J, void* state) {
     const bool fast = J.mode == OZK_FAST;
@@ -670,7 +676,7 @@ bool cols_worth_fusing(int64_t len, int64_t lines) {
 }
 bool b_fusable(const Job& J, int64_t j0) {
     return !J.tb ? cols_fused_on() && cols_worth_fusing(J.k, J.n)
-                 : rows_fused_on() && rows_fusable(b_block(J, j0), J.ldb);
+                 : rows_fused_on() && rows_fusable(b_block(J, j0), J.ldb, J.n, J.in_f32);
 }
 int stage_cols_fused(ozk_context* h, Job& J, int64_t j0, int64_t nj, void* state) {
     const bool fast = J.mode == OZK_FAST;

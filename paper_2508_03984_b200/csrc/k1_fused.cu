@@ -16,19 +16,22 @@
 //
 //  * rows_fused_kernel — lines are rows of a column-major operand (A, or B
 //    stored transposed): a row's statistics need all k columns, so the work
-//    is cut into 64-row x 128-column slices handed out by ticket counters in
-//    group-major order, to two warp-specialised roles per block. Statistics
-//    of a slice accumulate into per-row max / sum words (atomics; any
-//    summation order lies inside the guard band of the fast exponent, and
-//    flagged rows are recomputed exactly); the last slice of a 64-row group
-//    finalizes the group's exponents and publishes them with a flag.
-//    The planes role claims slices from a second counter and waits for its
-//    group's flag; the statistics role stays within `lag` (>= one group) slices
-//    of the planes counter, so the slice (64 KB) is re-read from L2 (~16 MB
-//    between the two reads at k = 16384), and — since a planes ticket that far
-//    behind belongs to a group whose statistics slices are all claimed, and a
-//    claimed statistics slice finishes without waiting — nothing deadlocks
-//    whatever the residency.
+//    is cut into 64-row x 64-column slices handed out by ticket counters in
+//    group-major order. Per block: a statistics role (8 warps) accumulates
+//    slice statistics into per-row max / sum words (atomics; any summation
+//    order lies inside the guard band of the fast exponent, and flagged rows
+//    are recomputed exactly), the last slice of a 64-row group finalizes the
+//    group's exponents and publishes them with a flag; a planes producer warp
+//    claims slices from a second counter, waits for the slice's group and
+//    stages the slice's 64 column runs into shared memory with bulk copies
+//    (double-buffered, mbarrier completion: bytes in flight cost no
+//    registers); 7 consumer warps write the planes from shared memory. The
+//    statistics stay within `lag` (>= one group) slices of the planes
+//    counter, so the staged runs are L2 hits, and — since a planes ticket that
+//    far behind belongs to a group whose statistics slices are all claimed,
+//    and a claimed statistics slice finishes without waiting — nothing
+//    deadlocks whatever the residency. All state words clear themselves at
+//    the end of the launch (CUDA graphs can replay it).
 //
 // Bit-exactness is unchanged: the exponents come from the same finalize code
 // as the two-kernel path (guard band + exact recompute), and the plane bytes
@@ -37,8 +40,9 @@
 // Measured (profiles/r02_k1_fused_ab.md): the column kernel runs
 // at 5.6-5.9 TB/s with 0.03-0.13 GB of its second read missing L2 and is the
 // default for columns of >= 4096 elements (>= 1024 of them); the row kernel
-// is bit-exact but slower than row_stats + planes (too few bytes in flight
-// in its planes role) and stays opt-in (OZK_K1_FUSED=3).
+// reads only the compulsory bytes (2.22 of 2.15 GB) but takes 2.07 ms against
+// 0.39 + 0.93 ms for row_stats + planes (its roles keep the SM issue only
+// ~34 % busy), so it stays opt-in (OZK_K1_FUSED=3).
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
@@ -241,7 +245,9 @@ __global__ void __launch_bounds__(kColThreads, 2)
 // ---- rows ------------------------------------------------------------------
 constexpr int kRowThreads = 512;
 constexpr int kRowGroup = 64;  // rows per group (one exponent publication)
-constexpr int kSliceCols = 128;  // columns per slice (ticket): 64 KB of FP64 per slice
+constexpr int kSliceCols = 64;  // columns per slice (ticket): 32 KB of FP64 per slice
+constexpr int kPlaneBufs = 2;   // planes role: slices staged in shared memory (double buffer)
+constexpr int kStatsWarps = 8;  // warps of the statistics role (the rest: planes producer + consumers)
 
 struct RowsFusedState {
     double* acc_max;      // [rows] non-negative max |x| bits (atomicMax on the encoding); zero between calls
@@ -251,8 +257,38 @@ struct RowsFusedState {
     uint32_t* tickets;    // [0] statistics, [1] planes, [2] finished roles; zero between calls
 };
 
-__device__ __forceinline__ void role_sync(int id) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kRowThreads / 2) : "memory");
+__device__ __forceinline__ void role_sync(int id, int count = kRowThreads / 2) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// a contiguous run of global memory into shared memory by the bulk-copy
+// engine (16-byte aligned, multiple of 16 bytes), completing on an mbarrier
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
 }
 
 // Warp-specialised: warps 0-7 run statistics tickets, warps 8-15 planes
@@ -264,13 +300,19 @@ __global__ void __launch_bounds__(kRowThreads, 2)
     rows_fused_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx, int splits, int lag,
                       int32_t* __restrict__ nonfinite, const LineFinal F, const DevConsts c,
                       int8_t* __restrict__ planes, int64_t ld, int64_t plane_stride, const RowsFusedState S) {
-    constexpr int kRoleThreads = kRowThreads / 2, kRoleWarps = kRoleThreads / 32;
+    // statistics: kStatsWarps warps (they read each slice once, from HBM); planes:
+    // one producer warp and the rest consumers (they convert and write N bytes
+    // per element: the heavier half)
+    constexpr int kRoleThreads = 32 * kStatsWarps, kRoleWarps = kStatsWarps;
     __shared__ double s_mx[kRoleWarps][kRowGroup];
     __shared__ double s_sm[kRoleWarps][kRowGroup];
-    __shared__ int s_exp[kRowGroup];
+    __shared__ int s_exp2[kPlaneBufs][kRowGroup];
     __shared__ int s_flag[kRowGroup];
     __shared__ int s_nflag, s_last;
-    __shared__ uint32_t s_t, s_p;
+    __shared__ uint32_t s_t;
+    __shared__ uint32_t s_pslot[kPlaneBufs];
+    __shared__ __align__(8) uint64_t s_full[kPlaneBufs], s_empty[kPlaneBufs];
+    extern __shared__ __align__(128) uint8_t dyn_smem[];  // [kPlaneBufs][kSliceCols][kRowGroup] T
     const int tid = threadIdx.x, lane = tid & 31;
     const bool stats_role = tid < kRoleThreads;
     const int rt = stats_role ? tid : tid - kRoleThreads;  // thread index inside the role
@@ -279,6 +321,14 @@ __global__ void __launch_bounds__(kRowThreads, 2)
     const uint32_t total = static_cast<uint32_t>(groups * splits);
     const int64_t extent = (rows + 15) / 16 * 16;  // plane_ld(rows)
     const uint64_t pol = pol_evict_first(), pol_keep = pol_evict_last();
+    if (tid == 0) {
+        for (int b = 0; b < kPlaneBufs; ++b) {
+            mbar_init(smem_addr(&s_full[b]), 1);
+            mbar_init(smem_addr(&s_empty[b]), kRowThreads / 32 - kStatsWarps - 1);  // one arrival per consumer warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
     if (stats_role) {
         for (;;) {
             if (rt == 0) {
@@ -295,7 +345,7 @@ __global__ void __launch_bounds__(kRowThreads, 2)
                 }
                 s_t = atomicAdd(S.tickets, 1u);
             }
-            role_sync(1);
+            role_sync(1, kRoleThreads);
             const uint32_t t = s_t;
             if (t >= total) break;
             // ---- statistics of slice t: rows [r0, r0 + 64), columns [h0, h1) ----
@@ -341,7 +391,7 @@ __global__ void __launch_bounds__(kRowThreads, 2)
             s_mx[rw][2 * lane + 1] = mx1;
             s_sm[rw][2 * lane] = sa;
             s_sm[rw][2 * lane + 1] = sb;
-            role_sync(1);
+            role_sync(1, kRoleThreads);
             if (rt < kRowGroup && r0 + rt < rows) {
                 double M = s_mx[0][rt], Sm = s_sm[0][rt];
 #pragma unroll
@@ -354,12 +404,12 @@ __global__ void __launch_bounds__(kRowThreads, 2)
                 atomicAdd(S.acc_sum + r0 + rt, Sm);
                 __threadfence();
             }
-            role_sync(1);
+            role_sync(1, kRoleThreads);
             if (rt == 0) {
                 s_last = atomicAdd(S.grp_cnt + g, 1) == splits - 1;
                 s_nflag = 0;
             }
-            role_sync(1);
+            role_sync(1, kRoleThreads);
             if (s_last) {
                 // ---- the group's last slice: finalize its exponents ----
                 __threadfence();
@@ -371,69 +421,101 @@ __global__ void __launch_bounds__(kRowThreads, 2)
                         atomicExch(reinterpret_cast<unsigned long long*>(S.acc_sum + row), 0ull)));
                     if (finalize_line(F, row, M, Sm)) s_flag[atomicAdd(&s_nflag, 1)] = rt;
                 }
-                role_sync(1);
+                role_sync(1, kRoleThreads);
                 for (int w = rw; w < s_nflag; w += kRoleWarps) exact_line(F, r0 + s_flag[w], lane);
                 __threadfence();
-                role_sync(1);
+                role_sync(1, kRoleThreads);
                 if (rt == 0) {
                     S.grp_cnt[g] = 0;  // ready for the next call
                     st_release(S.grp_ready + g, 1u);
                 }
             }
-            role_sync(1);  // s_t, s_last and the shared partials are reused
+            role_sync(1, kRoleThreads);  // s_t, s_last and the shared partials are reused
         }
-    } else {
-        const bool vec_ok = (ldx % (32 / sizeof(T))) == 0 && (reinterpret_cast<uintptr_t>(x) & 31) == 0;
-        for (;;) {
-            if (rt == 0) s_p = atomicAdd(S.tickets + 1, 1u);
-            role_sync(2);
-            const uint32_t p = s_p;
-            if (p >= total) break;
-            // ---- planes of slice p ----
+    } else if (rw == 0) {
+        // ---- planes producer (one warp): claims slices, waits for their group,
+        // stages each slice's columns into shared memory with bulk copies (the
+        // bytes in flight cost no registers) and its group's exponents ----
+        for (int iter = 0;; ++iter) {
+            const int bsl = iter % kPlaneBufs;
+            const uint32_t ph = static_cast<uint32_t>(iter / kPlaneBufs) & 1u;
+            uint32_t p = 0;
+            if (lane == 0) p = atomicAdd(S.tickets + 1, 1u);
+            p = __shfl_sync(0xffffffffu, p, 0);
+            mbar_wait(smem_addr(&s_empty[bsl]), ph ^ 1u);  // the consumers released this buffer
+            if (p >= total) {
+                if (lane == 0) {
+                    s_pslot[bsl] = p;  // the consumers' exit signal
+                    mbar_arrive(smem_addr(&s_full[bsl]));
+                }
+                break;
+            }
             const int64_t g = p / splits;
             const int64_t r0 = g * kRowGroup, h0 = static_cast<int64_t>(p % splits) * kSliceCols;
             const int64_t h1 = h0 + kSliceCols < cols ? h0 + kSliceCols : cols;
-            if (rt == 0) {
-                // the statistics role of every resident block claims and finishes
-                // statistics slices without waiting on anything, so the group is
-                // published; bounded anyway: a corrupted state word traps into a
-                // launch error instead of hanging the device
+            const int64_t nr = rows - r0 < kRowGroup ? rows - r0 : kRowGroup;
+            if (lane == 0) {
+                // statistics never wait on the planes counter's progress except
+                // through `lag`, which admits every statistics slice of this
+                // group, so the group is published; bounded anyway (trap, not hang)
                 const unsigned long long t0 = globaltimer_ns();
                 while (ld_acquire(S.grp_ready + g) != 1u) {
                     __nanosleep(128);
                     if (globaltimer_ns() - t0 > 4000000000ull) __trap();
                 }
             }
-            role_sync(2);
-            if (rt < kRowGroup) s_exp[rt] = r0 + rt < rows ? __ldcg(F.exp_out + r0 + rt) : 0;
-            role_sync(2);
-            // 8 rows x 1 column per item: 8 items per column, kSliceCols columns
+            __syncwarp();
+            s_exp2[bsl][lane] = r0 + lane < rows ? __ldcg(F.exp_out + r0 + lane) : 0;
+            s_exp2[bsl][lane + 32] = r0 + lane + 32 < rows ? __ldcg(F.exp_out + r0 + lane + 32) : 0;
+            if (lane == 0) s_pslot[bsl] = p;
+            __syncwarp();  // the exponents and the slot are written before the arrival
+            const uint32_t bytes = static_cast<uint32_t>(nr * sizeof(T));
+            const uint32_t full = smem_addr(&s_full[bsl]);
+            if (lane == 0) mbar_expect_tx(full, bytes * static_cast<uint32_t>(h1 - h0));
+            __syncwarp();
+            T* buf = reinterpret_cast<T*>(dyn_smem) + static_cast<size_t>(bsl) * kSliceCols * kRowGroup;
+            for (int64_t h = h0 + lane; h < h1; h += 32)
+                bulk_g2s(smem_addr(buf + (h - h0) * kRowGroup), x + r0 + h * ldx, bytes, full, pol);
+        }
+    } else {
+        // ---- planes consumers (7 warps): residue planes of the staged slice ----
+        constexpr int kConsumers = kRowThreads - kRoleThreads - 32;
+        const int ct = rt - 32;
+        for (int iter = 0;; ++iter) {
+            const int bsl = iter % kPlaneBufs;
+            const uint32_t ph = static_cast<uint32_t>(iter / kPlaneBufs) & 1u;
+            mbar_wait(smem_addr(&s_full[bsl]), ph);
+            const uint32_t p = s_pslot[bsl];
+            if (p >= total) break;
+            const int64_t g = p / splits;
+            const int64_t r0 = g * kRowGroup, h0 = static_cast<int64_t>(p % splits) * kSliceCols;
+            const int64_t h1 = h0 + kSliceCols < cols ? h0 + kSliceCols : cols;
+            const T* buf = reinterpret_cast<const T*>(dyn_smem) + static_cast<size_t>(bsl) * kSliceCols * kRowGroup;
+            // 8 rows x 1 column per item: 8 items per column
 #pragma unroll 1
-            for (int it = rt; it < kSliceCols * (kRowGroup / 8); it += kRoleThreads) {
-                const int64_t h = h0 + it / (kRowGroup / 8);
-                const int64_t rr = r0 + (it % (kRowGroup / 8)) * 8;
+            for (int it = ct; it < kSliceCols * (kRowGroup / 8); it += kConsumers) {
+                const int cl = it / (kRowGroup / 8), rc = (it % (kRowGroup / 8)) * 8;
+                const int64_t h = h0 + cl, rr = r0 + rc;
                 const bool active = h < h1 && rr < extent;
                 T v[8];
-                const T* src = x + (active ? h : 0) * ldx + (active ? rr : 0);
-                if (active && vec_ok && rr + 8 <= rows) {
-                    load8h(src, v, pol);
-                } else {
+                const T* src = buf + cl * kRowGroup + rc;
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) v[u] = active && rr + u < rows ? src[u] : T(0);
-                }
+                for (int u = 0; u < 8; ++u) v[u] = active && rr + u < rows ? src[u] : T(0);
                 int ex[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) ex[u] = s_exp[(it % (kRowGroup / 8)) * 8 + u];
-                write_planes8<T, KIND, kMaxMod>(v, ex, active, planes + h * ld + rr, plane_stride, c, pol);
+                for (int u = 0; u < 8; ++u) ex[u] = s_exp2[bsl][rc + u];
+                write_planes8<T, KIND, kMaxMod>(v, ex, active, planes + (active ? h : 0) * ld + (active ? rr : 0),
+                                                plane_stride, c, pol);
             }
-            role_sync(2);  // s_p and s_exp are reused
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_addr(&s_empty[bsl]));
         }
     }
     // each role of each block made exactly one failing claim and makes no more:
     // the last role out resets the counters for the next call
     // (with the group flags, so the state is all zero between calls and a
     // captured CUDA graph can replay the launch: nothing is baked in per call)
-    if (rt == 0 && atomicAdd(S.tickets + 2, 1u) == 2u * gridDim.x - 1u) {
+    if (rt == 0 && atomicAdd(S.tickets + 2, 1u) == 2u * gridDim.x - 1u) {  // stats rt 0 and the producer's lane 0
         const int64_t groups_all = (rows + kRowGroup - 1) / kRowGroup;
         for (int64_t g = 0; g < groups_all; ++g) S.grp_ready[g] = 0;
         S.tickets[0] = 0;
@@ -471,8 +553,10 @@ void rows_dispatch(const T* x, int64_t rows, int64_t cols, int64_t ldx, int32_t*
     const int splits = static_cast<int>((cols + kSliceCols - 1) / kSliceCols);
     const int64_t groups = (rows + kRowGroup - 1) / kRowGroup;
     const int64_t total = groups * splits;
+    constexpr int smem = kPlaneBufs * kSliceCols * kRowGroup * static_cast<int>(sizeof(T));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rows_fused_kernel<T, KIND, 8>, kRowThreads, 0);
+    cudaFuncSetAttribute(rows_fused_kernel<T, KIND, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rows_fused_kernel<T, KIND, 8>, kRowThreads, smem);
     if (per_sm < 1) per_sm = 1;
     const int64_t grid = std::min<int64_t>(total, static_cast<int64_t>(per_sm) * num_sms);
     // statistics may run this many slices ahead of the planes (>= one group;
@@ -480,8 +564,12 @@ void rows_dispatch(const T* x, int64_t rows, int64_t cols, int64_t ldx, int32_t*
     int lag = splits + static_cast<int>(grid / 2);
     if (const char* e = std::getenv("OZK_K1_LAG")) lag = std::max(splits, std::atoi(e));
 #define OZK_K1F(MAXN)                                                                                          \
-    rows_fused_kernel<T, KIND, MAXN><<<static_cast<unsigned>(grid), kRowThreads, 0, s>>>(                      \
-        x, rows, cols, ldx, splits, lag, nonfinite, F, c, planes, ld, stride, S)
+    do {                                                                                                       \
+        cudaFuncSetAttribute(rows_fused_kernel<T, KIND, MAXN>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                             smem);                                                                            \
+        rows_fused_kernel<T, KIND, MAXN><<<static_cast<unsigned>(grid), kRowThreads, smem, s>>>(               \
+            x, rows, cols, ldx, splits, lag, nonfinite, F, c, planes, ld, stride, S);                          \
+    } while (0)
     if (KIND == 1 || c.n <= 8)
         OZK_K1F(8);
     else if (c.n <= 12)
