@@ -419,10 +419,10 @@ __global__ void __launch_bounds__(kThreads, 4)
 // rows / columns, and undecided intervals, take the warp-uniform slow path.
 constexpr int kTileCols = 4;
 
-template <int P, int S>
+template <int P, int S, int kTC = kTileCols>
 struct Tc4Cfg {
     static constexpr int kColBytes = P * 128;
-    static constexpr int kStageBytes = kTileCols * kColBytes;
+    static constexpr int kStageBytes = kTC * kColBytes;
     static constexpr int kSmem = 1024 + S * kStageBytes + 2048;
     static_assert((32 - P) * 128 <= 2048, "MMA over-read leaves the allocation");
 };
@@ -440,18 +440,31 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
-template <bool kF32Out, bool kPlain, bool kExact, int P, int S, int kCW>
+// kFull: every row chunk and column group is complete and nu is 16-byte
+// aligned (m % 128 == 0, n % kTC == 0: the bench shapes), so the per-tile bounds
+// checks, the scalar exponent loads and the per-column store predicates drop out.
+// kTC: columns per tile. kTC = 8 gives each consumer thread 8 columns per tile,
+// reconstructed as two halves of 4 (the TMEM words of one half in registers at
+// a time), so the per-tile work — ring waits, tile indices, exponent loads —
+// is shared by 8 elements; its TMEM accumulator is single-buffered (8 x 16
+// columns), which keeps 4 blocks per SM within the 512 TMEM columns.
+template <bool kF32Out, bool kPlain, bool kExact, int P, int S, int kCW, bool kFull = false, int kTC = kTileCols>
 __global__ void __launch_bounds__(32 * kCW + 32, kCW == 4 ? 4 : 3)
     reconstruct_tc4_kernel(const __grid_constant__ CUtensorMap umap, int m, int n, int row_chunks, int tiles,
                            const int32_t* __restrict__ mu_exp, const int32_t* __restrict__ nu_exp, int nu_vec,
                            const DevConsts c, const TcParams tp, double lo_fac, double hi_fac, double alpha,
                            double beta, void* __restrict__ C, int64_t ldc, unsigned long long* __restrict__ replays) {
-    using Cf = Tc4Cfg<P, S>;
+    using Cf = Tc4Cfg<P, S, kTC>;
     using OutT = typename std::conditional<kF32Out, float, double>::type;
     constexpr int kColBytes = Cf::kColBytes, kStageBytes = Cf::kStageBytes;
     constexpr int kConsumersT = 32 * kCW;
-    constexpr int kCPT = kTileCols * 4 / kCW;  // columns per consumer thread
-    constexpr uint32_t kBufCols = 16 * kTileCols;
+    constexpr int kCPT = kTC * 4 / kCW;  // columns per consumer thread
+    constexpr int kQ = kCPT < 4 ? kCPT : 4;  // columns per half (TMEM words of kQ columns live at once)
+    constexpr int kHalves = kCPT / kQ;
+    static_assert(!kFull || kCPT % 4 == 0, "the full-tile variant loads int4s of nu per thread");
+    static_assert(kTC == kTileCols || (kFull && kCW == 4), "8-column tiles: full tiles, 4 consumer warps");
+    constexpr int kNB = kTC == kTileCols ? 2 : 1;  // TMEM accumulator buffers
+    constexpr uint32_t kBufCols = 16 * kTC;
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t full[S], empty[S], mma_full[2], tmem_empty[2];
     __shared__ uint32_t tmem_slot;
@@ -481,7 +494,7 @@ __global__ void __launch_bounds__(32 * kCW + 32, kCW == 4 ? 4 : 3)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
-                     "n"(2 * kBufCols));
+                     "n"(kNB * kBufCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_before();
@@ -507,7 +520,7 @@ __global__ void __launch_bounds__(32 * kCW + 32, kCW == 4 ? 4 : 3)
                 mbar_wait_backoff(empty0 + 8 * st, ph);
                 const uint32_t fb = full0 + 8 * st;
                 mbar_expect_tx(fb, static_cast<uint32_t>(kStageBytes));
-                tma_3d(sb0 + st * kStageBytes, &umap, fb, chunk * 128, 0, cg * kTileCols, pol);
+                tma_3d(sb0 + st * kStageBytes, &umap, fb, chunk * 128, 0, cg * kTC, pol);
                 chunk += dr;
                 cg += dj;
                 if (chunk >= row_chunks) {
@@ -529,15 +542,17 @@ __global__ void __launch_bounds__(32 * kCW + 32, kCW == 4 ? 4 : 3)
                 tc_after();
                 const uint32_t stage = sb0 + st * kStageBytes;
 #pragma unroll
-                for (int q = 0; q < kTileCols; ++q)
+                for (int q = 0; q < kTC; ++q)
                     mma_u8(tbase + b * kBufCols + q * 16, sdesc_sw128(stage + q * kColBytes), bd);
                 mma_commit(mfull0 + 8 * b);
                 if (++st == S) {
                     st = 0;
                     ph ^= 1u;
                 }
-                b ^= 1;
-                if (b == 0) tph ^= 1u;
+                if (++b == kNB) {
+                    b = 0;
+                    tph ^= 1u;
+                }
             }
         }
         return;
@@ -556,8 +571,20 @@ __global__ void __launch_bounds__(32 * kCW + 32, kCW == 4 ? 4 : 3)
     // vector load
     auto load_exps = [&](int ch, int g, int& me_o, int (&ne_o)[kCPT]) {
         const int r = ch * 128 + rin;
+        const int j = g * kTC + q0;
+        if constexpr (kFull) {
+            me_o = __ldg(mu_exp + r);
+#pragma unroll
+            for (int v4 = 0; v4 < kCPT / 4; ++v4) {
+                const int4 v = __ldg(reinterpret_cast<const int4*>(nu_exp + j) + v4);
+                ne_o[4 * v4] = v.x;
+                ne_o[4 * v4 + 1] = v.y;
+                ne_o[4 * v4 + 2] = v.z;
+                ne_o[4 * v4 + 3] = v.w;
+            }
+            return;
+        }
         me_o = r < m ? __ldg(mu_exp + r) : 0;
-        const int j = g * kTileCols + q0;
         if (nu_vec && j + kCPT <= n) {
             if constexpr (kCPT == 4) {
                 const int4 v = __ldg(reinterpret_cast<const int4*>(nu_exp + j));
@@ -585,7 +612,7 @@ __global__ void __launch_bounds__(32 * kCW + 32, kCW == 4 ? 4 : 3)
 #pragma unroll
         for (int q = 0; q < kCPT; ++q) ne[q] = ne_n[q];
         const int row = chunk * 128 + rin;
-        const int j0 = cg * kTileCols + q0;
+        const int j0 = cg * kTC + q0;
         chunk += dr;
         cg += dj;
         if (chunk >= row_chunks) {
@@ -595,110 +622,122 @@ __global__ void __launch_bounds__(32 * kCW + 32, kCW == 4 ? 4 : 3)
         if (tile + step < tiles) load_exps(chunk, cg, me_n, ne_n);
         mbar_wait_sleep(mfull0 + 8 * b, tph);
         tc_after();
-        double c1[kCPT], cpp[kCPT];
-        uint32_t und = 0;  // bit q: the interval of column q did not decide
-        {
-            uint32_t v[kCPT][16];
-#pragma unroll
-            for (int q = 0; q < kCPT; ++q) tmem_ld16(tq + b * kBufCols + 16 * q, v[q]);
-            tmem_wait_ld();
-            tc_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(tempty0 + 8 * b);
-#pragma unroll
-            for (int q = 0; q < kCPT; ++q) {
-                const uint32_t* w = v[q];
-                c1[q] = __fma_rn(pair52_xyz(w[0] + (w[1] << 8), w[2] + (w[3] << 8), w[4] + (w[5] << 8)), tp.sc1,
-                                 tp.sc1m);
-                const double Lp = pair52_xyz(w[6] + (w[7] << 8), w[8] + (w[9] << 8), 0u);
-                const double Hp = pair52_xyz(w[10] + (w[11] << 8), w[12] + (w[13] << 8), 0u);
-                const double c2 = __dadd_rn(__fma_rn(Hp, tp.sc2h, tp.sc2hm), __fma_rn(Lp, tp.sc2l, tp.sc2lm));
-                const double qv = rint_small(__dmul_rn(c.P_inv, c1[q]));
-                const double X = __fma_rn(-c.P1, qv, c1[q]);
-                if constexpr (kExact) {
-                    cpp[q] = __fma_rn(-c.P2, qv, __dadd_rn(X, c2));
-                } else {
-                    // c2 lies in [c2~ (1 - rf), c2~ (1 + rf)] (c2~ >= 0); fl(X + .) is
-                    // monotone, so equal sums at both ends are fl(X + c2)
-                    const double slo = __dadd_rn(X, __dmul_rd(c2, lo_fac));
-                    const double shi = __dadd_rn(X, __dmul_ru(c2, hi_fac));
-                    cpp[q] = __fma_rn(-c.P2, qv, slo);
-                    und |= (__double_as_longlong(slo) != __double_as_longlong(shi) ? 1u : 0u) << q;
-                }
-            }
-        }
-        const bool live_row = row < m;
-        const int cols = min(n - j0, kCPT);  // live columns of this thread (may be <= 0)
-        bool ok = static_cast<unsigned>(me + 511) <= 1022u;
-#pragma unroll
-        for (int q = 0; q < kCPT; ++q) ok = ok && static_cast<unsigned>(ne[q] + 511) <= 1022u;
-        OutT* cptr = static_cast<OutT*>(C) + static_cast<int64_t>(j0) * ldc + row;
+        const bool live_row = kFull || row < m;
         const uint32_t emp = empty0 + 8 * st;
-        if (__all_sync(0xffffffffu, und == 0 && ok)) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(emp);
-            if (live_row) {
-                const int pow_row = (1023 - me) << 20;
-                OutT* p = cptr;
 #pragma unroll
-                for (int q = 0; q < kCPT; ++q, p += ldc) {
-                    if (q < cols) {
-                        double r = __dmul_rn(cpp[q], __hiloint2double(pow_row - (ne[q] << 20), 0));
-                        if (!kPlain) {
-                            const double old = beta != 0.0 ? static_cast<double>(*p) : 0.0;
-                            r = __dadd_rn(__dmul_rn(alpha, r), __dmul_rn(beta, old));
-                        }
-                        *p = static_cast<OutT>(r);
-                    }
+        for (int h = 0; h < kHalves; ++h) {
+            const int qb = h * kQ;  // this half's first column (of the thread's kCPT)
+            double c1[kQ], cpp[kQ];
+            uint32_t und = 0;  // bit q: the interval of column qb + q did not decide
+            {
+                uint32_t v[kQ][16];
+#pragma unroll
+                for (int q = 0; q < kQ; ++q) tmem_ld16(tq + b * kBufCols + 16 * (qb + q), v[q]);
+                tmem_wait_ld();
+                if (h == kHalves - 1) {  // the accumulator is free for the next tile's MMAs
+                    tc_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(tempty0 + 8 * b);
                 }
-            }
-        } else {
-            // rare, warp-uniform: an undecided interval (replay the reference's c2,
-            // emulator.cpp:53, from the planes in shared memory) or an unscale
-            // factor that is not a normal power of two (general ldexp)
-            const uint32_t stage = sb0 + st * kStageBytes;
 #pragma unroll
-            for (int q = 0; q < kCPT; ++q) {
-                double cq = cpp[q];
-                if (!kExact && ((und >> q) & 1u)) {
+                for (int q = 0; q < kQ; ++q) {
+                    const uint32_t* w = v[q];
+                    c1[q] = __fma_rn(pair52_xyz(w[0] + (w[1] << 8), w[2] + (w[3] << 8), w[4] + (w[5] << 8)), tp.sc1,
+                                     tp.sc1m);
+                    const double Lp = pair52_xyz(w[6] + (w[7] << 8), w[8] + (w[9] << 8), 0u);
+                    const double Hp = pair52_xyz(w[10] + (w[11] << 8), w[12] + (w[13] << 8), 0u);
+                    const double c2 = __dadd_rn(__fma_rn(Hp, tp.sc2h, tp.sc2hm), __fma_rn(Lp, tp.sc2l, tp.sc2lm));
                     const double qv = rint_small(__dmul_rn(c.P_inv, c1[q]));
                     const double X = __fma_rn(-c.P1, qv, c1[q]);
-                    const uint32_t line = stage + (q0 + q) * kColBytes + row_lo;
-                    double c2r = 0.0;
-#pragma unroll 1
-                    for (int t = 0; t < n_mod; ++t) {
-                        uint32_t ub;
-                        asm volatile("ld.shared.u8 %0, [%1];"
-                                     : "=r"(ub)
-                                     : "r"(line + t * 128 + ((row_chunk ^ static_cast<uint32_t>(t & 7)) << 4)));
-                        c2r = __dadd_rn(c2r, __fma_rn(c.s2[t], __hiloint2double(0x43300000, static_cast<int>(ub)),
-                                                      c.s2_m52[t]));
+                    if constexpr (kExact) {
+                        cpp[q] = __fma_rn(-c.P2, qv, __dadd_rn(X, c2));
+                    } else {
+                        // c2 lies in [c2~ (1 - rf), c2~ (1 + rf)] (c2~ >= 0); fl(X + .) is
+                        // monotone, so equal sums at both ends are fl(X + c2)
+                        const double slo = __dadd_rn(X, __dmul_rd(c2, lo_fac));
+                        const double shi = __dadd_rn(X, __dmul_ru(c2, hi_fac));
+                        cpp[q] = __fma_rn(-c.P2, qv, slo);
+                        und |= (__double_as_longlong(slo) != __double_as_longlong(shi) ? 1u : 0u) << q;
                     }
-                    cq = __fma_rn(-c.P2, qv, __dadd_rn(X, c2r));
-                    if (live_row && q < cols) ++n_replay;
-                }
-                if (live_row && q < cols) {
-                    double r = unscale_fast(cq, -(me + ne[q]));
-                    if (!kPlain) {
-                        const double old = beta != 0.0 ? static_cast<double>(cptr[q * ldc]) : 0.0;
-                        r = __dadd_rn(__dmul_rn(alpha, r), __dmul_rn(beta, old));
-                    }
-                    cptr[q * ldc] = static_cast<OutT>(r);
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(emp);
+            const int cols = kFull ? kQ : min(n - (j0 + qb), kQ);  // live columns of this half (may be <= 0)
+            bool ok = static_cast<unsigned>(me + 511) <= 1022u;
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) ok = ok && static_cast<unsigned>(ne[qb + q] + 511) <= 1022u;
+            OutT* cptr = static_cast<OutT*>(C) + static_cast<int64_t>(j0 + qb) * ldc + row;
+            if (__all_sync(0xffffffffu, und == 0 && ok)) {
+                if (h == kHalves - 1) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(emp);
+                }
+                if (live_row) {
+                    const int pow_row = (1023 - me) << 20;
+                    OutT* p = cptr;
+#pragma unroll
+                    for (int q = 0; q < kQ; ++q, p += ldc) {
+                        if (q < cols) {
+                            double r = __dmul_rn(cpp[q], __hiloint2double(pow_row - (ne[qb + q] << 20), 0));
+                            if (!kPlain) {
+                                const double old = beta != 0.0 ? static_cast<double>(*p) : 0.0;
+                                r = __dadd_rn(__dmul_rn(alpha, r), __dmul_rn(beta, old));
+                            }
+                            *p = static_cast<OutT>(r);
+                        }
+                    }
+                }
+            } else {
+                // rare, warp-uniform: an undecided interval (replay the reference's c2,
+                // emulator.cpp:53, from the planes in shared memory) or an unscale
+                // factor that is not a normal power of two (general ldexp)
+                const uint32_t stage = sb0 + st * kStageBytes;
+#pragma unroll
+                for (int q = 0; q < kQ; ++q) {
+                    double cq = cpp[q];
+                    if (!kExact && ((und >> q) & 1u)) {
+                        const double qv = rint_small(__dmul_rn(c.P_inv, c1[q]));
+                        const double X = __fma_rn(-c.P1, qv, c1[q]);
+                        const uint32_t line = stage + (q0 + qb + q) * kColBytes + row_lo;
+                        double c2r = 0.0;
+#pragma unroll 1
+                        for (int t = 0; t < n_mod; ++t) {
+                            uint32_t ub;
+                            asm volatile("ld.shared.u8 %0, [%1];"
+                                         : "=r"(ub)
+                                         : "r"(line + t * 128 + ((row_chunk ^ static_cast<uint32_t>(t & 7)) << 4)));
+                            c2r = __dadd_rn(c2r, __fma_rn(c.s2[t], __hiloint2double(0x43300000, static_cast<int>(ub)),
+                                                          c.s2_m52[t]));
+                        }
+                        cq = __fma_rn(-c.P2, qv, __dadd_rn(X, c2r));
+                        if (live_row && q < cols) ++n_replay;
+                    }
+                    if (live_row && q < cols) {
+                        double r = unscale_fast(cq, -(me + ne[qb + q]));
+                        if (!kPlain) {
+                            const double old = beta != 0.0 ? static_cast<double>(cptr[q * ldc]) : 0.0;
+                            r = __dadd_rn(__dmul_rn(alpha, r), __dmul_rn(beta, old));
+                        }
+                        cptr[q * ldc] = static_cast<OutT>(r);
+                    }
+                }
+                if (h == kHalves - 1) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(emp);
+                }
+            }
         }
         if (++st == S) st = 0;
-        b ^= 1;
-        if (b == 0) tph ^= 1u;
+        if (++b == kNB) {
+            b = 0;
+            tph ^= 1u;
+        }
     }
     if (replays && n_replay) atomicAdd(replays, n_replay);
     tc_before();
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumersT) : "memory");
     if (warp == 0) {
         tc_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(2 * kBufCols));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kNB * kBufCols));
     }
 }
 
@@ -754,15 +793,15 @@ bool launch_t(const CUtensorMap& map, int num_sms, cudaStream_t s, int64_t m, in
 }
 
 // the column-tiled kernel (reconstruct_tc4_kernel): kCW consumer warps
-template <bool kF32Out, bool kPlain, bool kExact, int P, int S, int kCW>
+template <bool kF32Out, bool kPlain, bool kExact, int P, int S, int kCW, bool kFull = false, int kTC = kTileCols>
 bool launch_t4(const CUtensorMap& map, int num_sms, cudaStream_t s, int64_t m, int64_t n, const int32_t* mu_exp,
                const int32_t* nu_exp, const DevConsts& c, const TcParams& tp, double lo_fac, double hi_fac,
                double alpha, double beta, void* C, int64_t ldc, unsigned long long* replays) {
-    using Cf = Tc4Cfg<P, S>;
-    auto kern = reconstruct_tc4_kernel<kF32Out, kPlain, kExact, P, S, kCW>;
+    using Cf = Tc4Cfg<P, S, kTC>;
+    auto kern = reconstruct_tc4_kernel<kF32Out, kPlain, kExact, P, S, kCW, kFull, kTC>;
     constexpr int smem = Cf::kSmem;
     constexpr int threads = 32 * kCW + 32;
-    constexpr int tmem_cols = 2 * 16 * kTileCols;
+    constexpr int tmem_cols = (kTC == kTileCols ? 2 : 1) * 16 * kTC;
     static std::atomic<unsigned long long> attr{0};
     static std::atomic<int> per_sm_dev[64];
     const int dev = current_device() & 63;
@@ -787,10 +826,10 @@ bool launch_t4(const CUtensorMap& map, int num_sms, cudaStream_t s, int64_t m, i
     }();
     if (per_sm < 1) return false;
     const int64_t row_chunks = (m + 127) / 128;
-    const int64_t tiles = row_chunks * ((n + kTileCols - 1) / kTileCols);
+    const int64_t tiles = row_chunks * ((n + kTC - 1) / kTC);
     const int64_t grid = std::min<int64_t>(tiles, static_cast<int64_t>(num_sms) * per_sm);
     if (tiles + grid >= (int64_t(1) << 31)) return false;  // 32-bit tile arithmetic
-    constexpr int cpt = kTileCols * 4 / kCW;
+    constexpr int cpt = kTC * 4 / kCW;
     const int nu_vec = reinterpret_cast<uintptr_t>(nu_exp) % (4 * cpt) == 0;
     kern<<<static_cast<unsigned>(grid), threads, smem, s>>>(
         map, static_cast<int>(m), static_cast<int>(n), static_cast<int>(row_chunks), static_cast<int>(tiles), mu_exp,
@@ -798,7 +837,8 @@ bool launch_t4(const CUtensorMap& map, int num_sms, cudaStream_t s, int64_t m, i
     return true;
 }
 
-// OZK_K3_TILE=1: the 512-row x 1-column kernel (reconstruct_tc_kernel, A/B timing);
+// OZK_K3_TILE=1: the 512-row x 1-column kernel (reconstruct_tc_kernel, A/B timing); 8: the
+// column-tiled kernel with 8-column tiles where the tiles are full (default 4);
 // OZK_K3_CW: consumer warps of the column-tiled kernel (4 or 8, default 4)
 int k3_tile_mode() {
     static const int v = [] {
@@ -815,6 +855,15 @@ int k3_consumer_warps() {
     return v;
 }
 
+// OZK_K3_FULL=0: never take the full-tile instantiation (A/B timing, tests)
+int k3_full_tiles() {
+    static const int v = [] {
+        const char* e = std::getenv("OZK_K3_FULL");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 int k3_stages() {
     static const int v = [] {
         const char* e = std::getenv("OZK_K3_STAGES");
@@ -825,7 +874,7 @@ int k3_stages() {
 }
 
 template <bool kF32Out, bool kPlain, bool kExact, int P>
-bool launch_t4_cw(const CUtensorMap& map, int sms, cudaStream_t s, int64_t m, int64_t n, const int32_t* mu_exp,
+bool launch_t4_cw(const CUtensorMap& map, const CUtensorMap& map8, int sms, cudaStream_t s, int64_t m, int64_t n, const int32_t* mu_exp,
                   const int32_t* nu_exp, const DevConsts& c, const TcParams& tp, double lo_fac, double hi_fac,
                   double alpha, double beta, void* C, int64_t ldc, unsigned long long* replays) {
     if (k3_consumer_warps() == 8)
@@ -834,28 +883,36 @@ bool launch_t4_cw(const CUtensorMap& map, int sms, cudaStream_t s, int64_t m, in
     if (k3_stages() == 8)
         return launch_t4<kF32Out, kPlain, kExact, P, 8, 4>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
                                                            alpha, beta, C, ldc, replays);
-    if (k3_stages() == 6)
+    const bool full = k3_full_tiles() && m % 128 == 0 && reinterpret_cast<uintptr_t>(nu_exp) % 16 == 0;
+    if (full && k3_tile_mode() == 8 && n % 8 == 0)
+        return launch_t4<kF32Out, kPlain, kExact, P, 3, 4, true, 8>(map8, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac,
+                                                                    hi_fac, alpha, beta, C, ldc, replays);
+    if (k3_stages() == 6) {
+        if (full && n % kTileCols == 0)
+            return launch_t4<kF32Out, kPlain, kExact, P, 6, 4, true>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac,
+                                                                     hi_fac, alpha, beta, C, ldc, replays);
         return launch_t4<kF32Out, kPlain, kExact, P, 6, 4>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
                                                            alpha, beta, C, ldc, replays);
+    }
     return launch_t4<kF32Out, kPlain, kExact, P, 4, 4>(map, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac, alpha,
                                                        beta, C, ldc, replays);
 }
 
 template <bool kF32Out, bool kPlain>
-bool launch_variant(const CUtensorMap& map, const CUtensorMap& map4, int sms, cudaStream_t s, int64_t m, int64_t n,
+bool launch_variant(const CUtensorMap& map, const CUtensorMap& map4, const CUtensorMap& map8, int sms, cudaStream_t s, int64_t m, int64_t n,
                     const int32_t* mu_exp, const int32_t* nu_exp, const DevConsts& c, const TcParams& tp,
                     double lo_fac, double hi_fac, double alpha, double beta, void* C, int64_t ldc,
                     unsigned long long* replays) {
     if (k3_tile_mode() != 1) {
         bool ok;
         if (tp.rfac == 0.0)
-            ok = launch_t4_cw<kF32Out, kPlain, true, 16>(map4, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
+            ok = launch_t4_cw<kF32Out, kPlain, true, 16>(map4, map8, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
                                                         alpha, beta, C, ldc, replays);
         else if (c.n <= 16)
-            ok = launch_t4_cw<kF32Out, kPlain, false, 16>(map4, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
+            ok = launch_t4_cw<kF32Out, kPlain, false, 16>(map4, map8, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
                                                          alpha, beta, C, ldc, replays);
         else
-            ok = launch_t4_cw<kF32Out, kPlain, false, 24>(map4, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
+            ok = launch_t4_cw<kF32Out, kPlain, false, 24>(map4, map8, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
                                                          alpha, beta, C, ldc, replays);
         if (ok) return true;
     }
@@ -979,17 +1036,22 @@ bool launch_reconstruct_tc(const uint8_t* u, int64_t ldu, int64_t stride, int64_
     auto enc = encode_fn();
     if (!enc) return false;
     const int P = c.n <= 16 ? 16 : 24;
-    CUtensorMap map, map4;
+    CUtensorMap map, map4, map8;
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(c.n), static_cast<cuuint64_t>(n)};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(stride), static_cast<cuuint64_t>(ldu)};
     cuuint32_t box[3] = {128u, static_cast<cuuint32_t>(P), 1u};
     cuuint32_t box4[3] = {128u, static_cast<cuuint32_t>(P), static_cast<cuuint32_t>(kTileCols)};
+    cuuint32_t box8[3] = {128u, static_cast<cuuint32_t>(P), 8u};
     cuuint32_t estr[3] = {1, 1, 1};
     if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(u), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
     if (enc(&map4, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(u), dims, strides, box4, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (enc(&map8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(u), dims, strides, box8, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
@@ -1000,13 +1062,13 @@ bool launch_reconstruct_tc(const uint8_t* u, int64_t ldu, int64_t stride, int64_
     unsigned long long* replays = k3_replay_counter(false);
     const bool plain = alpha == 1.0 && beta == 0.0;
     if (c_is_f32)
-        return plain ? launch_variant<true, true>(map, map4, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
+        return plain ? launch_variant<true, true>(map, map4, map8, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
                                                   alpha, beta, C, ldc, replays)
-                     : launch_variant<true, false>(map, map4, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
+                     : launch_variant<true, false>(map, map4, map8, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac,
                                                    alpha, beta, C, ldc, replays);
-    return plain ? launch_variant<false, true>(map, map4, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac, alpha,
+    return plain ? launch_variant<false, true>(map, map4, map8, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac, alpha,
                                                beta, C, ldc, replays)
-                 : launch_variant<false, false>(map, map4, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac, alpha,
+                 : launch_variant<false, false>(map, map4, map8, sms, s, m, n, mu_exp, nu_exp, c, tp, lo_fac, hi_fac, alpha,
                                                 beta, C, ldc, replays);
 }
 
