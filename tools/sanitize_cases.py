@@ -49,6 +49,14 @@ for (m, n, k) in [(200, 300, 1000), (257, 129, 4100)]:
     want = 0.5 * orc.gemm(a, b, 14, 0) + 2.0 * C0
     print(f"transA alpha/beta {m}x{n}x{k}: max dev {np.max(np.abs(got - want)):.3g}", flush=True)
 
+# whole 128-row x 4-column (x 8-column with OZK_K3_TILE=8) K3 tiles: the full-tile instantiation
+m, n, k = 256, 64, 300
+a, b = gen_matrix(m, k, 1.0, 8), gen_matrix(k, n, 1.0, 9)
+for N in (14, 20):
+    C = torch.zeros((n, m), dtype=torch.float64, device="cuda").t()
+    ctx.gemm(dev(a), dev(b), EmuConfig(n_moduli=N), C)
+    check(f"full tiles {m}x{n}x{k} N{N}", C.cpu().numpy(), orc.gemm(a, b, N, 0))
+
 if not quick:
     # streamed host pipeline (fast mode, m, n >= 2048)
     m = n = 2048
