@@ -23,7 +23,8 @@
 //   columns 0-5 the base-256 digits of S1_i, 6-13 those of S2_i) -> s32 TMEM,
 // each digit column sum_i D_ib u_i < 2^21. So the per-element FP64 chain of
 // the all-FP64 kernel (4 FP64 ops per element and modulus) becomes a fixed
-// ~15 FP64 ops per element, and K3 streams at the HBM rate.
+// 11 FP64 ops per element (c1 1, c2 2, Q 3, X 1, the interval ends 2 FMAs,
+// C'' 1, unscale 1) in the column-tiled kernel, independent of N.
 //
 // Warp roles: warp 4 lane 0 issues the TMA boxes into an S-slot ring, lane 1
 // the MMAs into a double-buffered TMEM accumulator (2 x 64
@@ -54,6 +55,8 @@ struct TcParams {
     unsigned long long s2_int[OZK_MAX_MODULI];  // S2_i = s2_i / 2^E2
     double sc1, sc1m;                           // 2^E1, -2^(52+E1)
     double sc2h, sc2hm, sc2l, sc2lm;            // 2^(32+E2), -2^(84+E2), 2^E2, -2^(52+E2)
+    double sc2b;                                // -(2^(84+E2) + 2^(52+E2))
+    uint32_t l_hi;                              // high word of 2^(52+E2): (1075 + E2) << 20
     double rfac;                                // (N + 3) 2^-53
 };
 
@@ -183,6 +186,16 @@ __device__ __forceinline__ double rint_small(double y) {
 __device__ __forceinline__ double pair52(uint64_t T) {
     return __hiloint2double(static_cast<int>(static_cast<uint32_t>(T >> 32) | 0x43300000u),
                             static_cast<int>(static_cast<uint32_t>(T)));
+}
+// (2^52 + x + 2^16 y) 2^e for x, y < 2^30 (x + 2^16 y < 2^52), with hi = the high
+// word of 2^(52+e): the integer placed straight into the mantissa of a double
+// of exponent 52 + e (no FP64 operation)
+__device__ __forceinline__ double pair52_xy_hi(uint32_t x, uint32_t y, uint32_t hi_base) {
+    uint32_t lo, hi;
+    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
+        : "=r"(lo), "=r"(hi)
+        : "r"(x), "r"(y << 16), "r"(y >> 16), "r"(hi_base));
+    return __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
 }
 // 2^52 + x + 2^16 y (+ 2^32 z) for x, y, z < 2^30 without 64-bit arithmetic:
 // low word x + (y << 16) with carry, high word 0x43300000 + (y >> 16) + z + carry
@@ -644,18 +657,23 @@ __global__ void __launch_bounds__(32 * kCW + 32, kCW == 4 ? 4 : 3)
                     const uint32_t* w = v[q];
                     c1[q] = __fma_rn(pair52_xyz(w[0] + (w[1] << 8), w[2] + (w[3] << 8), w[4] + (w[5] << 8)), tp.sc1,
                                      tp.sc1m);
-                    const double Lp = pair52_xyz(w[6] + (w[7] << 8), w[8] + (w[9] << 8), 0u);
+                    // c2~ = fl(H 2^(32+E2) + L 2^E2) in two FP64 operations: Lb = (2^52 + L) 2^E2
+                    // is built in the mantissa directly, fma(2^52 + H, 2^(32+E2),
+                    // -(2^(84+E2) + 2^(52+E2))) = H 2^(32+E2) - 2^(52+E2) is exact (<= 46
+                    // significant bits), and the one rounding is the final add
+                    const double Lb = pair52_xy_hi(w[6] + (w[7] << 8), w[8] + (w[9] << 8), tp.l_hi);
                     const double Hp = pair52_xyz(w[10] + (w[11] << 8), w[12] + (w[13] << 8), 0u);
-                    const double c2 = __dadd_rn(__fma_rn(Hp, tp.sc2h, tp.sc2hm), __fma_rn(Lp, tp.sc2l, tp.sc2lm));
+                    const double c2 = __dadd_rn(__fma_rn(Hp, tp.sc2h, tp.sc2b), Lb);
                     const double qv = rint_small(__dmul_rn(c.P_inv, c1[q]));
                     const double X = __fma_rn(-c.P1, qv, c1[q]);
                     if constexpr (kExact) {
                         cpp[q] = __fma_rn(-c.P2, qv, __dadd_rn(X, c2));
                     } else {
                         // c2 lies in [c2~ (1 - rf), c2~ (1 + rf)] (c2~ >= 0); fl(X + .) is
-                        // monotone, so equal sums at both ends are fl(X + c2)
-                        const double slo = __dadd_rn(X, __dmul_rd(c2, lo_fac));
-                        const double shi = __dadd_rn(X, __dmul_ru(c2, hi_fac));
+                        // monotone, so equal sums at both ends are fl(X + c2). The ends
+                        // enter exactly (inside the FMA), one rounding each.
+                        const double slo = __fma_rn(c2, lo_fac, X);
+                        const double shi = __fma_rn(c2, hi_fac, X);
                         cpp[q] = __fma_rn(-c.P2, qv, slo);
                         und |= (__double_as_longlong(slo) != __double_as_longlong(shi) ? 1u : 0u) << q;
                     }
@@ -1014,6 +1032,8 @@ bool launch_reconstruct_tc(const uint8_t* u, int64_t ldu, int64_t stride, int64_
     tp.sc2hm = -std::ldexp(1.0, E2 + 84);
     tp.sc2l = std::ldexp(1.0, E2);
     tp.sc2lm = -std::ldexp(1.0, E2 + 52);
+    tp.sc2b = -(std::ldexp(1.0, E2 + 84) + std::ldexp(1.0, E2 + 52));
+    tp.l_hi = static_cast<uint32_t>(1075 + E2) << 20;
     // with every s2_i u_i and every partial sum on the 2^E2 grid below 2^53
     // the reference's c2 is exact (= S), so the interval collapses
     unsigned __int128 total2 = 0;
